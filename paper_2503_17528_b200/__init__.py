@@ -1,0 +1,227 @@
+"""serinv-b200: FP64 POBTAF / POBTASI (Serinv, arXiv 2503.17528) on NVIDIA B200.
+
+Thin Python binding over libserinv.so (include/serinv.h): argument marshalling
+only -- every step of the factorisation / selected inversion runs in the
+library's sm_100a kernels.  Inputs are torch float64 CUDA tensors in the
+C-ABI layout (row-major blocks):
+
+    diag  [n, b, b]    A_{i,i}      lower [n-1, b, b]  A_{i+1,i}
+    arrow [n, a, b]    A_{n,i}      tip   [a, a]       A_{n,n}
+
+All routines work IN PLACE (like the C-ABI) on the caller's current CUDA
+stream.  There is no CPU fallback: importing works without a GPU, but every
+compute call requires the CUDA library and a device.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+from . import _lib
+from ._lib import BTA, GraphStats, Part
+
+__all__ = ["Handle", "pobtaf", "pobtasi", "selinv", "pselinv", "plan", "version",
+           "NotPositiveDefinite", "SerinvError", "ppobtaf", "ppobtasi", "exchange_bytes",
+           "graph_stats", "default_handle"]
+
+
+class SerinvError(RuntimeError):
+    def __init__(self, status: int, where: str = ""):
+        msg = _lib.lib().serinv_status_string(status).decode()
+        super().__init__(f"{where}: serinv status {status} ({msg})")
+        self.status = status
+
+
+class NotPositiveDefinite(ArithmeticError):
+    """dpotrf-style failure: `row` is the 1-based global row of the first bad pivot."""
+
+    def __init__(self, row: int, b: int, n: int):
+        blk = (row - 1) // b
+        where = "the tip" if blk >= n else f"block {blk}"
+        super().__init__(f"matrix is not positive definite (first non-positive pivot at global row {row}, {where})")
+        self.row = row
+
+
+def version() -> str:
+    return _lib.lib().serinv_version().decode()
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise SerinvError(rc, where)
+
+
+class Handle:
+    """Library handle bound to one CUDA device (caches task graphs per shape)."""
+
+    def __init__(self, device: int | None = None):
+        import torch
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        self._h = ctypes.c_void_p()
+        _check(_lib.lib().serinv_create(ctypes.byref(self._h), self.device), "serinv_create")
+        self._ws = {}
+
+    def close(self):
+        if self._h:
+            _lib.lib().serinv_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def workspace(self, nbytes: int):
+        """Device workspace of at least nbytes (cached, grown on demand)."""
+        import torch
+        ws = self._ws.get("ws")
+        if ws is None or ws.numel() < nbytes:
+            self._ws["ws"] = ws = torch.empty(max(nbytes, 256), dtype=torch.uint8,
+                                              device=f"cuda:{self.device}")
+        return ws
+
+    def scalars(self):
+        import torch
+        s = self._ws.get("scal")
+        if s is None:
+            s = (torch.zeros(1, dtype=torch.int32, device=f"cuda:{self.device}"),
+                 torch.zeros(1, dtype=torch.float64, device=f"cuda:{self.device}"))
+            self._ws["scal"] = s
+        return s
+
+    def last_launches(self) -> int:
+        v = ctypes.c_int(0)
+        _lib.lib().serinv_last_launches(self._h, ctypes.byref(v))
+        return v.value
+
+
+_default = {}
+
+
+def default_handle(device: int | None = None) -> Handle:
+    import torch
+    d = torch.cuda.current_device() if device is None else int(device)
+    h = _default.get(d)
+    if h is None:
+        h = _default[d] = Handle(d)
+    return h
+
+
+def _bta(diag, lower, arrow, tip) -> BTA:
+    import torch
+    if diag.dtype != torch.float64 or not diag.is_cuda:
+        raise TypeError("diag must be a float64 CUDA tensor")
+    n, b = diag.shape[0], diag.shape[1]
+    a = tip.shape[0] if tip is not None else 0
+    for name, t, shp in (("diag", diag, (n, b, b)), ("lower", lower, (n - 1, b, b)),
+                         ("arrow", arrow, (n, a, b)), ("tip", tip, (a, a))):
+        if t is None:
+            if name in ("diag",) or (name == "lower" and n > 1) or (name in ("arrow", "tip") and a > 0):
+                raise ValueError(f"{name} is required")
+            continue
+        if tuple(t.shape) != shp:
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {shp}")
+        if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+            raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
+        if t.device != diag.device:
+            raise ValueError(f"{name} is on {t.device}, diag on {diag.device}")
+
+    def ptr(t):
+        return t.data_ptr() if (t is not None and t.numel() > 0) else None
+    return BTA(n, b, a, ptr(diag), ptr(lower), ptr(arrow), ptr(tip))
+
+
+def _stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _finish(h: Handle, info_t, logdet_t, check: bool, b: int, n: int):
+    if not check:
+        return None
+    info = int(info_t.item())
+    if info:
+        raise NotPositiveDefinite(info, b, n)
+    return float(logdet_t.item()) if logdet_t is not None else None
+
+
+def _run(kind: str, diag, lower, arrow, tip, handle, check, info=None, logdet=None):
+    L = _lib.lib()
+    h = handle or default_handle(diag.device.index)
+    A = _bta(diag, lower, arrow, tip)
+    n, b, a = A.n, A.b, A.a
+    wsq = {"pobtaf": L.serinv_pobtaf_ws, "pobtasi": L.serinv_pobtasi_ws, "selinv": L.serinv_selinv_ws}[kind]
+    nb = ctypes.c_size_t(0)
+    _check(wsq(n, b, a, ctypes.byref(nb)), kind + "_ws")
+    ws = h.workspace(nb.value)
+    si, sl = h.scalars()
+    info = si if info is None else info
+    logdet = sl if logdet is None else logdet
+    if kind == "pobtasi":
+        rc = L.serinv_pobtasi(h._h, ctypes.byref(A), ws.data_ptr(), ws.numel(), info.data_ptr(), _stream())
+        _check(rc, kind)
+        return _finish(h, info, None, check, b, n)
+    fn = L.serinv_pobtaf if kind == "pobtaf" else L.serinv_selinv
+    rc = fn(h._h, ctypes.byref(A), ws.data_ptr(), ws.numel(), info.data_ptr(), logdet.data_ptr(), _stream())
+    _check(rc, kind)
+    return _finish(h, info, logdet, check, b, n)
+
+
+def pobtaf(diag, lower, arrow, tip, *, handle: Handle | None = None, check: bool = True, info=None, logdet=None):
+    """In-place POBTAF (Alg. 1): A -> L.  Returns log det A (check=True)."""
+    return _run("pobtaf", diag, lower, arrow, tip, handle, check, info, logdet)
+
+
+def pobtasi(diag, lower, arrow, tip, *, handle: Handle | None = None, check: bool = True, info=None):
+    """In-place POBTASI (Alg. 2): L -> X (selected inverse on the BTA pattern)."""
+    return _run("pobtasi", diag, lower, arrow, tip, handle, check, info, None)
+
+
+def selinv(diag, lower, arrow, tip, *, handle: Handle | None = None, check: bool = True, info=None, logdet=None):
+    """In-place POBTAF + POBTASI as one task graph: A -> X.  Returns log det A."""
+    return _run("selinv", diag, lower, arrow, tip, handle, check, info, logdet)
+
+
+def plan(n: int, P: int, r: float = 1.0):
+    """Partition plan (reading R6): [(start, end)] for ranks 0..P-1."""
+    starts = (ctypes.c_int64 * (P + 1))()
+    _check(_lib.lib().serinv_plan(n, P, float(r), starts), "serinv_plan")
+    return [(starts[p], starts[p + 1]) for p in range(P)]
+
+
+def pselinv(diag, lower, arrow, tip, P: int, r: float = 1.0, *, handle: Handle | None = None,
+            check: bool = True, info=None, logdet=None):
+    """In-process partitioned selected inversion on one device (PPOBTAF -> POBTARSSI ->
+    PPOBTASI, Sec. 3) with P partitions.  A -> X in place.  Returns log det."""
+    L = _lib.lib()
+    h = handle or default_handle(diag.device.index)
+    A = _bta(diag, lower, arrow, tip)
+    nb = ctypes.c_size_t(0)
+    _check(L.serinv_pselinv_ws(A.n, A.b, A.a, P, float(r), ctypes.byref(nb)), "pselinv_ws")
+    ws = h.workspace(nb.value)
+    si, sl = h.scalars()
+    info = si if info is None else info
+    logdet = sl if logdet is None else logdet
+    rc = L.serinv_pselinv(h._h, ctypes.byref(A), P, float(r), ws.data_ptr(), ws.numel(), info.data_ptr(),
+                          logdet.data_ptr(), _stream())
+    _check(rc, "pselinv")
+    return _finish(h, info, logdet, check, A.b, A.n)
+
+
+def exchange_bytes(b: int, a: int) -> int:
+    nb = ctypes.c_size_t(0)
+    _check(_lib.lib().serinv_exchange_bytes(b, a, ctypes.byref(nb)), "exchange_bytes")
+    return nb.value
+
+
+def graph_stats(kind: int, n: int, b: int, a: int, P: int = 1, r: float = 1.0, handle: Handle | None = None):
+    h = handle or default_handle()
+    st = GraphStats()
+    _check(_lib.lib().serinv_graph_stats(h._h, kind, n, b, a, P, float(r), ctypes.byref(st)), "graph_stats")
+    return dict(tasks=st.tasks, counters=st.counters, flops=st.flops, grid=st.grid, tile=st.tile)
+
+
+from .distributed import ppobtaf, ppobtasi  # noqa: E402

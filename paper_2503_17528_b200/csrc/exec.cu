@@ -1,0 +1,554 @@
+// exec.cu -- persistent dataflow executor for serinv task graphs on B200 (sm_100a).
+//
+// One CTA of 256 threads per claim slot; the grid is sized to the number of
+// co-resident CTAs (148 SMs x occupancy) so every claimed task can wait on
+// earlier tasks without deadlock.  A CTA claims the next task index with one
+// atomic, spins (thread 0, ld.acquire.gpu + nanosleep) until the task's input
+// counters reach their targets, executes the tile task, then publishes its
+// results (__syncthreads + __threadfence + atomicAdd on its signal counters).
+// All tile operands are read through L2 (cp.async.cg / ld.global.cg), never
+// L1, so data produced by other SMs inside the same launch is never stale.
+//
+// FP64 arithmetic: tcgen05 has no f64 kind, so the tensor-core path on
+// sm_100a is the warp-level DMMA (mma.sync.aligned.m8n8k4.f64 -> SASS
+// DMMA.8x8x4, measured 37.1 TFLOP/s chip-wide = the DFMA peak; see
+// profiles/fp64_peaks_r01.json).  Tiles are 64 x 64; each of the 8 warps owns a
+// 16 x 32 sub-tile (2 x 4 DMMA fragments); operands are staged in shared memory
+// by a 3-stage cp.async pipeline over k-chunks of 32, in bank-conflict-free
+// padded layouts (row stride = 4 mod 16 doubles).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "exec.h"
+#include "task.h"
+
+namespace serinv {
+namespace dev {
+
+constexpr int NT = 256;
+constexpr int KC = 32;
+constexpr int STAGES = 3;
+constexpr int LD_MK = KC + 4;            // [row][k] layout stride (36 = 4 mod 16)
+constexpr int LD_KM = SERINV_TILE + 4;   // [k][row] layout stride (68 = 4 mod 16)
+constexpr int OPSZ = SERINV_TILE * LD_MK;  // doubles per operand stage (2304 >= 32*68)
+constexpr int LDT = SERINV_TILE + 4;     // full-tile stride in smem (68)
+constexpr int SMEM_DOUBLES = STAGES * 2 * OPSZ;  // 13824 doubles = 110592 bytes
+static_assert(KC * LD_KM <= OPSZ, "km layout fits the stage");
+static_assert(2 * SERINV_TILE * LDT + 4 * SERINV_TILE <= SMEM_DOUBLES, "post/potrf smem fits");
+
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double *lptr(const Params &p, const Loc &l) { return p.bufs[l.buf] + l.off; }
+
+__device__ void record_info(int *info, int v) {
+  int old = *(volatile int *)info;
+  while (old == 0 || v < old) {
+    int prev = atomicCAS(info, old, v);
+    if (prev == old) break;
+    old = prev;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Operand staging.  op(X) is R x K.  km == false: X stored R x K row-major
+// (elem (r,k) at base[r*ld + k]) -> smem [r][k] stride LD_MK.  km == true: X
+// stored K x R row-major (elem (r,k) at base[k*ld + r]) -> smem [k][r] stride LD_KM.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void load_operand(double *s, const double *base, int ld, bool km, int R, int K, int k0,
+                                             bool vec) {
+  const int tid = threadIdx.x;
+  if (!km) {
+#pragma unroll
+    for (int it = 0; it < (SERINV_TILE * (KC / 2)) / NT; ++it) {
+      int idx = tid + it * NT;
+      int r = idx >> 4, kk = (idx & 15) * 2;
+      int kg = k0 + kk;
+      int nv = (r < R) ? max(0, min(2, K - kg)) : 0;
+      double *dst = s + r * LD_MK + kk;
+      const double *src = base + (int64_t)r * ld + kg;
+      if (vec) {
+        cp_async16(dst, nv ? src : base, nv * 8);
+      } else {
+        dst[0] = nv > 0 ? __ldcg(src) : 0.0;
+        dst[1] = nv > 1 ? __ldcg(src + 1) : 0.0;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int it = 0; it < (KC * (SERINV_TILE / 2)) / NT; ++it) {
+      int idx = tid + it * NT;
+      int kk = idx >> 5, r = (idx & 31) * 2;
+      int kg = k0 + kk;
+      int nv = (kg < K) ? max(0, min(2, R - r)) : 0;
+      double *dst = s + kk * LD_KM + r;
+      const double *src = base + (int64_t)kg * ld + r;
+      if (vec) {
+        cp_async16(dst, nv ? src : base, nv * 8);
+      } else {
+        dst[0] = nv > 0 ? __ldcg(src) : 0.0;
+        dst[1] = nv > 1 ? __ldcg(src + 1) : 0.0;
+      }
+    }
+  }
+}
+
+// acc += A(16x32 warp slab) * B over `ksteps` k-steps of 4; generic strides:
+// A elem (row, k) at As[row*sAr + k*sAk]; B elem (k, col) at Bs[col*sBn + k*sBk].
+__device__ __forceinline__ void mma_steps(const double *As, int sAr, int sAk, const double *Bs, int sBn, int sBk,
+                                          double (&acc)[2][4][2], int ksteps) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = (warp >> 1) * 16 + (lane >> 2);
+  const int c0 = (warp & 1) * 32 + (lane >> 2);
+  const int kq = lane & 3;
+#pragma unroll 4
+  for (int ks = 0; ks < ksteps; ++ks) {
+    const int kk = ks * 4 + kq;
+    double a0 = As[r0 * sAr + kk * sAk];
+    double a1 = As[(r0 + 8) * sAr + kk * sAk];
+    double b[4];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(c0 + ni * 8) * sBn + kk * sBk];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      dmma(acc[0][ni], a0, b[ni]);
+      dmma(acc[1][ni], a1, b[ni]);
+    }
+  }
+}
+
+// Main loop: acc = sum_s op(A_s) op(B_s) over all segments of task T.
+__device__ void gemm_mainloop(const Params &p, const Task &T, double *smem, double (&acc)[2][4][2]) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (T.nseg == 0) return;
+  const Seg *segs = p.segs + T.seg0;
+  int nchunks = 0;
+  for (int s = 0; s < T.nseg; ++s) nchunks += (segs[s].k + KC - 1) / KC;
+  // load-side cursor
+  int ls = 0, lk = 0;
+  auto issue = [&](int stage) {
+    const Seg &S = segs[ls];
+    double *As = smem + stage * 2 * OPSZ;
+    double *Bs = As + OPSZ;
+    bool vecA = ((S.A.off | S.A.ld) & 1) == 0;
+    bool vecB = ((S.B.off | S.B.ld) & 1) == 0;
+    load_operand(As, lptr(p, S.A), S.A.ld, S.ta != 0, T.m, S.k, lk, vecA);
+    load_operand(Bs, lptr(p, S.B), S.B.ld, S.tb == 0, T.n, S.k, lk, vecB);
+    lk += KC;
+    if (lk >= S.k) {
+      lk = 0;
+      ++ls;
+    }
+  };
+  // compute-side cursor (segment layouts)
+  int cs = 0, ck = 0;
+#pragma unroll
+  for (int j = 0; j < STAGES - 1; ++j) {
+    if (j < nchunks) issue(j);
+    cp_commit();
+  }
+  for (int j = 0; j < nchunks; ++j) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    if (j + STAGES - 1 < nchunks) issue((j + STAGES - 1) % STAGES);
+    cp_commit();
+    const Seg &S = segs[cs];
+    const double *As = smem + (j % STAGES) * 2 * OPSZ;
+    const double *Bs = As + OPSZ;
+    const bool akm = S.ta != 0, bkm = S.tb == 0;
+    int kleft = S.k - ck;
+    int ksteps = kleft >= KC ? KC / 4 : (kleft + 3) / 4;
+    mma_steps(As, akm ? 1 : LD_MK, akm ? LD_KM : 1, Bs, bkm ? 1 : LD_MK, bkm ? LD_KM : 1, acc, ksteps);
+    ck += KC;
+    if (ck >= S.k) {
+      ck = 0;
+      ++cs;
+    }
+  }
+  cp_wait<0>();
+  __syncthreads();
+}
+
+// Fragment element coordinates of acc[mi][ni][h].
+__device__ __forceinline__ void frag_rc(int mi, int ni, int h, int &r, int &c) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  r = (warp >> 1) * 16 + mi * 8 + (lane >> 2);
+  c = (warp & 1) * 32 + ni * 8 + 2 * (lane & 3) + h;
+}
+
+// acc = alpha * acc + beta * C0
+__device__ __forceinline__ void apply_c0(const Params &p, const Task &T, double (&acc)[2][4][2]) {
+  const double *c0 = (T.beta != 0.0) ? lptr(p, T.c0) : nullptr;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int r, c;
+        frag_rc(mi, ni, h, r, c);
+        double v = T.alpha * acc[mi][ni][h];
+        if (c0 && r < T.m && c < T.n) v += T.beta * __ldcg(c0 + (int64_t)r * T.c0.ld + c);
+        acc[mi][ni][h] = v;
+      }
+}
+
+__device__ __forceinline__ void acc_to_smem(double *St, const double (&acc)[2][4][2]) {
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int r, c;
+        frag_rc(mi, ni, h, r, c);
+        St[r * LDT + c] = acc[mi][ni][h];
+      }
+}
+
+// load an m x n tile (row-major, ld) into smem [64][LDT], zero padded
+__device__ __forceinline__ void tile_to_smem(double *St, const double *g, int ld, int m, int n) {
+  for (int idx = threadIdx.x; idx < SERINV_TILE * SERINV_TILE; idx += NT) {
+    int r = idx >> 6, c = idx & 63;
+    St[r * LDT + c] = (r < m && c < n) ? __ldcg(g + (int64_t)r * ld + c) : 0.0;
+  }
+}
+
+__device__ void store_acc(const Params &p, const Task &T, const double (&acc)[2][4][2]) {
+  double *o = lptr(p, T.out);
+  const bool vec = ((T.out.off | T.out.ld) & 1) == 0;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      int r, c;
+      frag_rc(mi, ni, 0, r, c);
+      if (r >= T.m) continue;
+      double *dst = o + (int64_t)r * T.out.ld + c;
+      if (vec && c + 1 < T.n) {
+        *reinterpret_cast<double2 *>(dst) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      } else {
+        if (c < T.n) dst[0] = acc[mi][ni][0];
+        if (c + 1 < T.n) dst[1] = acc[mi][ni][1];
+      }
+    }
+  if (T.flags & (TF_MIRROR | TF_ZERO_MIRROR)) {
+    double *o2 = lptr(p, T.out2);
+    const bool zero = (T.flags & TF_ZERO_MIRROR) != 0;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int r, c;
+          frag_rc(mi, ni, h, r, c);
+          if (r < T.m && c < T.n) o2[(int64_t)c * T.out2.ld + r] = zero ? 0.0 : acc[mi][ni][h];
+        }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tile tasks
+// ---------------------------------------------------------------------------
+__device__ void run_gemm(const Params &p, const Task &T, double *smem) {
+  double acc[2][4][2];
+  gemm_mainloop(p, T, smem, acc);
+  apply_c0(p, T, acc);
+  if (T.flags & TF_POST) {
+    double *St = smem;
+    double *Rt = smem + SERINV_TILE * LDT;
+    acc_to_smem(St, acc);
+    tile_to_smem(Rt, lptr(p, T.r), T.r.ld, T.n, T.n);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const bool rt = (T.flags & TF_POST_T) != 0;
+    // out = S * op(R): B(k, j) = R[j][k] (POST_T) or R[k][j]
+    mma_steps(St, LDT, 1, Rt, rt ? LDT : 1, rt ? 1 : LDT, acc, (T.n + 3) / 4);
+    __syncthreads();
+  }
+  store_acc(p, T, acc);
+}
+
+// 16 x 16 thread grid; thread (ty, tx) owns rows ty + 16 ii, cols tx + 16 kk.
+// Right-looking unscaled Cholesky (one barrier per pivot), then row-oriented
+// TRTRI W = L^{-1} (one barrier per row).
+__device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bool factor) {
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int m = T.m;
+  double *St = smem;                          // [64][LDT]  the tile (L after factor)
+  double *cb = smem + SERINV_TILE * LDT;      // [2][64] column / row broadcast
+  double *dv = cb + 2 * SERINV_TILE;          // [64] pivots d_j (then L_jj)
+  double *lg = dv + SERINV_TILE;              // [64] log L_jj
+  if (factor) {
+    double acc[2][4][2];
+    gemm_mainloop(p, T, smem, acc);
+    apply_c0(p, T, acc);
+    acc_to_smem(St, acc);
+  } else {
+    tile_to_smem(St, lptr(p, T.c0), T.c0.ld, m, m);
+  }
+  __syncthreads();
+  double v[4][4];
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) v[ii][kk] = St[(ty + 16 * ii) * LDT + tx + 16 * kk];
+  if (factor) {
+    for (int j = 0; j < m; ++j) {
+      double *buf = cb + (j & 1) * SERINV_TILE;
+      if (tx == (j & 15)) {
+        const int kk = j >> 4;
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+          double x = v[0][0];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q == kk) x = v[ii][q];
+          buf[ty + 16 * ii] = x;
+        }
+      }
+      __syncthreads();
+      const double d = buf[j];
+      const double dinv = 1.0 / d;
+      if (tid == 0) dv[j] = d;
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        const int i = ty + 16 * ii;
+        const double li = buf[i] * dinv;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int k = tx + 16 * kk;
+          if (k > j && k <= i) v[ii][kk] = fma(-li, buf[k], v[ii][kk]);
+        }
+      }
+    }
+    __syncthreads();
+    // scale: L[i][k] = v / sqrt(d_k) (i > k), L[k][k] = sqrt(d_k); zero upper
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = tx + 16 * kk;
+      const double dk = k < m ? dv[k] : 1.0;
+      const double sk = sqrt(dk);
+      const double rs = 1.0 / sk;
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        const int i = ty + 16 * ii;
+        double x = (i > k) ? v[ii][kk] * rs : (i == k ? sk : 0.0);
+        if (i >= m || k >= m) x = 0.0;
+        v[ii][kk] = x;
+        St[i * LDT + k] = x;
+      }
+    }
+    if (tid < m) {
+      double d = dv[tid];
+      lg[tid] = 0.5 * log(d);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int bad = -1;
+      for (int j = 0; j < m; ++j)
+        if (!(dv[j] > 0.0)) {
+          bad = j;
+          break;
+        }
+      if (bad >= 0) record_info(p.info, T.aux1 + bad + 1);
+      if (T.aux0 >= 0) {
+        double s = 0.0;
+        for (int j = 0; j < m; ++j) s += lg[j];
+        *lptr(p, T.r) = s;
+      }
+    }
+    // store L (full tile, zeros above the diagonal)
+    double *o = lptr(p, T.out);
+    for (int idx = tid; idx < m * m; idx += NT) {
+      int r = idx / m, c = idx - r * m;
+      o[(int64_t)r * T.out.ld + c] = St[r * LDT + c];
+    }
+  } else {
+    // TRTRI only: v holds L (lower); zero the strict upper part
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int i = ty + 16 * ii, k = tx + 16 * kk;
+        if (k > i || i >= m || k >= m) {
+          v[ii][kk] = 0.0;
+          St[i * LDT + k] = 0.0;
+        }
+      }
+    __syncthreads();
+    if (tid == 0) {
+      for (int j = 0; j < m; ++j) {
+        double d = St[j * LDT + j];
+        if (!(d != 0.0) || !isfinite(d)) {
+          record_info(p.info, T.aux1 + j + 1);
+          break;
+        }
+      }
+    }
+  }
+  if (!factor || (T.flags & TF_W_OUT)) {
+    // W = L^{-1}, row by row: W[s][c] = (delta_sc - acc[s][c]) / L[s][s];
+    // acc[i][c] += L[i][s] W[s][c] for i > s.  acc kept in w[][] (registers).
+    double w[4][4];
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) w[ii][kk] = 0.0;
+    for (int s = 0; s < m; ++s) {
+      double *buf = cb + (s & 1) * SERINV_TILE;
+      const double lss = St[s * LDT + s];
+      if (ty == (s & 15)) {
+        const int ii = s >> 4;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int c = tx + 16 * kk;
+          double a = w[0][kk];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q == ii) a = w[q][kk];
+          double val = (c <= s) ? (((c == s) ? 1.0 : 0.0) - a) / lss : 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q == ii) w[q][kk] = val;
+          buf[c] = val;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        const int i = ty + 16 * ii;
+        if (i > s && i < m) {
+          const double lis = St[i * LDT + s];
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const int c = tx + 16 * kk;
+            if (c <= s) w[ii][kk] = fma(lis, buf[c], w[ii][kk]);
+          }
+        }
+      }
+    }
+    const Loc &wl = factor ? T.out2 : T.out;
+    double *wo = lptr(p, wl);
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int i = ty + 16 * ii, c = tx + 16 * kk;
+        if (i < m && c < m) wo[(int64_t)i * wl.ld + c] = (c <= i) ? w[ii][kk] : 0.0;
+      }
+  }
+}
+
+__device__ void run_reduce(const Params &p, const Task &T) {
+  const double *src = lptr(p, T.r);
+  const double *c0 = T.beta != 0.0 ? lptr(p, T.c0) : nullptr;
+  double *o = lptr(p, T.out);
+  for (int idx = threadIdx.x; idx < T.m * T.n; idx += NT) {
+    int r = idx / T.n, c = idx - r * T.n;
+    double s = 0.0;
+    for (int j = 0; j < T.aux0; ++j) s += __ldcg(src + T.aux2 * j + (int64_t)r * T.r.ld + c);
+    double v = T.alpha * s;
+    if (c0) v += T.beta * __ldcg(c0 + (int64_t)r * T.c0.ld + c);
+    o[(int64_t)r * T.out.ld + c] = v;
+  }
+}
+
+__device__ void run_copy(const Params &p, const Task &T) {
+  const double *c0 = lptr(p, T.c0);
+  double *o = lptr(p, T.out);
+  const bool tr = (T.flags & TF_TRANS_C0) != 0;
+  for (int idx = threadIdx.x; idx < T.m * T.n; idx += NT) {
+    int r = idx / T.n, c = idx - r * T.n;
+    double v = tr ? __ldcg(c0 + (int64_t)c * T.c0.ld + r) : __ldcg(c0 + (int64_t)r * T.c0.ld + c);
+    o[(int64_t)r * T.out.ld + c] = T.alpha * v;
+  }
+}
+
+__device__ void run_logdet(const Params &p, const Task &T, double *smem) {
+  const double *slots = lptr(p, T.r);
+  double s = 0.0;
+  for (int j = threadIdx.x; j < T.aux0; j += NT) s += __ldcg(slots + j);
+  smem[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = NT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) smem[threadIdx.x] += smem[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int inf = *(volatile int *)p.info;
+    *lptr(p, T.out) = inf ? __longlong_as_double(0x7ff8000000000000ULL) : 2.0 * smem[0];
+  }
+}
+
+}  // namespace dev
+
+extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev::Params p) {
+  using namespace dev;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_task;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(p.claim, 1);
+    __syncthreads();
+    const int t = s_task;
+    if (t >= p.ntasks) break;
+    const Task T = p.tasks[t];
+    if (threadIdx.x == 0) {
+      for (int w = 0; w < T.nwait; ++w) {
+        const Wait W = p.waits[T.wait0 + w];
+        if (ld_acquire(p.ctr + W.ctr) >= W.target) continue;
+        int ns = 32;
+        while (ld_acquire(p.ctr + W.ctr) < W.target) {
+          __nanosleep(ns);
+          ns = min(ns * 2, 256);
+        }
+      }
+    }
+    __syncthreads();
+    switch (T.type) {
+      case TK_GEMM: run_gemm(p, T, smem); break;
+      case TK_POTRF: run_potrf_trtri(p, T, smem, true); break;
+      case TK_TRTRI: run_potrf_trtri(p, T, smem, false); break;
+      case TK_REDUCE: run_reduce(p, T); break;
+      case TK_COPY: run_copy(p, T); break;
+      case TK_LOGDET: run_logdet(p, T, smem); break;
+      default: break;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      for (int s = 0; s < T.nsig; ++s) atomicAdd(p.ctr + p.sigs[T.sig0 + s], 1);
+    }
+  }
+}
+
+int exec_smem_bytes() { return dev::SMEM_DOUBLES * 8; }
+
+}  // namespace serinv

@@ -1,0 +1,98 @@
+// graph.h -- host-side task-graph builder and scheduler (C++17, no CUDA).
+//
+// The block algorithms of PAPER.md (Alg. 1 POBTAF, Alg. 2 POBTASI, Alg. 3-6
+// PPOBTAF / PPOBTASI, Sec. 3.3 POBTARSSI) are lowered to a DAG of 64 x 64 tile
+// tasks (task.h).  The lowering is exact block algebra: a block Cholesky at
+// block size b equals the tiled Cholesky at tile size 64 on the same pattern,
+// and the Takahashi recurrence of Alg. 2 / Alg. 6 is evaluated with the
+// inverted diagonal blocks W_X = L_XX^{-1} ("invert L_ii once", P:567-569,
+// P:649):  X_{Y,X} = -sum_Z X_{Y,Z} (L_{Z,X} W_X),
+//          X_{X,X} = W_X^T W_X - sum_Y X_{Y,X}^T (L_{Y,X} W_X).
+// The scheduler orders tasks by a list-scheduling simulation with critical-
+// path (bottom-level) priority so the persistent executor claims the
+// latency-critical POTRF/TRSM chain first and fills the idle SMs with the
+// bulk updates and the inversion precompute.
+#pragma once
+#include <cstdint>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "task.h"
+
+namespace serinv {
+
+constexpr int TILE = SERINV_TILE;
+
+// Finalised graph: flat arrays ready for upload.
+struct Graph {
+  std::vector<Task> tasks;
+  std::vector<Seg> segs;
+  std::vector<Wait> waits;
+  std::vector<int32_t> sigs;
+  int32_t nctr = 0;
+  double flops = 0.0;        // executed FP64 flops (model)
+  int grid = 0;              // worker count the schedule was simulated for
+  int64_t ws_doubles = 0;    // workspace doubles used (excluding counters)
+  int64_t nslots = 0;        // logdet slots
+  double sim_ns = 0.0;       // simulated makespan of the schedule (ns)
+  std::string error;         // non-empty if building failed
+};
+
+// A storage place for a block: base Loc (top-left) of a rows x cols block.
+struct BlkRef {
+  Loc base{};
+  int rows = 0, cols = 0;
+  bool zero_init = false;    // starts as fill-in zero (beta = 0 on first write)
+  bool valid = false;
+};
+
+// Generic description of one elimination problem (one partition, the whole
+// matrix, or a reduced system) on top of which factor / inverse tasks are built.
+struct Problem {
+  // nodes in elimination order
+  std::vector<int> size;          // node size (b or a)
+  std::vector<char> elim;         // factorised here
+  std::vector<int64_t> rowbase;   // global row of the node's first row (info)
+  std::vector<std::vector<int>> rows;     // rows[X]: nodes Y > X with blk(Y,X) nonzero (elim X)
+  std::map<std::pair<int, int>, BlkRef> blk;   // (Y, X), Y >= X
+  std::vector<char> accum;        // targets in this node's column receive whole-node update groups
+  // workspace placements (filled by the builder)
+  std::vector<Loc> W;             // W_X = L_XX^{-1}
+  std::vector<Loc> Lam;           // Lambda_X = W_X^T W_X
+  std::map<std::pair<int, int>, Loc> Lchk;     // Lchk(Z,X) = L_{Z,X} W_X
+  std::vector<int64_t> slot;      // logdet slot base per node (-1: none)
+};
+
+struct BuildOptions {
+  int grid = 296;          // persistent CTAs (for the simulated schedule)
+  int update_group = 4;    // tile columns per chained update task (regular targets)
+  bool schedule = true;
+};
+
+// Sequential problems (whole matrix).  kind: 0 = pobtaf, 1 = pobtasi, 2 = selinv.
+Graph build_sequential(int kind, int64_t n, int64_t b, int64_t a, const BuildOptions &opt);
+
+// Workspace bytes for the sequential kinds (doubles region + counters).
+int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a);
+
+// In-process partitioned pipeline on one device (PPOBTAF -> POBTARSSI -> PPOBTASI).
+Graph build_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, const BuildOptions &opt);
+int64_t pselinv_ws_bytes(int64_t n, int64_t b, int64_t a, int P, double r);
+
+// Distributed per-rank graphs.  phase 0 = ppobtaf (+ pack into EXT0 send buffer),
+// phase 1 = ppobtasi (assemble from EXT1 recv buffer, POBTARSSI, backward).
+Graph build_distributed(int phase, int P, int rank, int64_t n_global, int64_t start,
+                        int64_t count, int64_t b, int64_t a, const BuildOptions &opt);
+int64_t distributed_ws_bytes(int P, int rank, int64_t n_global, int64_t start, int64_t count,
+                             int64_t b, int64_t a);
+int64_t exchange_doubles(int64_t b, int64_t a);
+
+// Partition plan (reading R6).  Returns false if infeasible.
+bool plan_partitions(int64_t n, int P, double r, std::vector<int64_t> &starts);
+
+// Bytes reserved at the end of the workspace for counters (+1 claim counter).
+int64_t counter_bytes(int32_t nctr);
+
+}  // namespace serinv

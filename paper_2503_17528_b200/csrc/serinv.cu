@@ -1,0 +1,395 @@
+// serinv.cu -- C-ABI of libserinv.so (include/serinv.h).
+//
+// Each compute entry point: validate arguments, fetch (or build + upload) the
+// cached task graph for the problem shape, reset its dependency counters, and
+// launch ONE persistent executor kernel (exec.cu) on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/serinv.h"
+#include "graph.h"
+#include "task.h"
+
+#include "exec.h"
+
+using namespace serinv;
+
+namespace {
+
+struct DevGraph {
+  Graph g;                 // host copy (stats); task arrays freed after upload
+  void *blob = nullptr;    // tasks | segs | waits | sigs
+  int32_t *ctr = nullptr;  // nctr + 1 (claim counter last)
+  const Task *d_tasks = nullptr;
+  const Seg *d_segs = nullptr;
+  const Wait *d_waits = nullptr;
+  const int32_t *d_sigs = nullptr;
+  int64_t ntasks = 0;
+  ~DevGraph() {
+    if (blob) cudaFree(blob);
+    if (ctr) cudaFree(ctr);
+  }
+};
+
+typedef std::tuple<int, int64_t, int64_t, int64_t, int, int64_t, int, int64_t, int64_t> GKey;
+
+}  // namespace
+
+struct serinv_ctx {
+  int device = 0;
+  int sms = 0;
+  int grid = 0;
+  int smem = 0;
+  int last_launches = 0;
+  double *dummy = nullptr;  // logdet sink when the caller passes NULL
+  std::map<GKey, std::unique_ptr<DevGraph>> cache;
+  std::mutex mu;
+};
+
+namespace {
+
+inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+int upload(DevGraph &dg) {
+  Graph &g = dg.g;
+  size_t bt = g.tasks.size() * sizeof(Task), bs = g.segs.size() * sizeof(Seg);
+  size_t bw = g.waits.size() * sizeof(Wait), bg = g.sigs.size() * sizeof(int32_t);
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  size_t total = up(bt) + up(bs) + up(bw) + up(bg) + 256;
+  if (cudaMalloc(&dg.blob, total) != cudaSuccess) return SERINV_ERR_CUDA;
+  char *base = (char *)dg.blob;
+  size_t o = 0;
+  auto put = [&](const void *src, size_t n) {
+    char *dst = base + o;
+    if (n) cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
+    o += up(n);
+    return (const void *)dst;
+  };
+  dg.d_tasks = (const Task *)put(g.tasks.data(), bt);
+  dg.d_segs = (const Seg *)put(g.segs.data(), bs);
+  dg.d_waits = (const Wait *)put(g.waits.data(), bw);
+  dg.d_sigs = (const int32_t *)put(g.sigs.data(), bg);
+  if (cudaMalloc(&dg.ctr, (size_t)(g.nctr + 1) * sizeof(int32_t)) != cudaSuccess) return SERINV_ERR_CUDA;
+  dg.ntasks = (int64_t)g.tasks.size();
+  if (cudaGetLastError() != cudaSuccess) return SERINV_ERR_CUDA;
+  // keep stats, drop the big host arrays
+  std::vector<Task>().swap(g.tasks);
+  std::vector<Seg>().swap(g.segs);
+  std::vector<Wait>().swap(g.waits);
+  std::vector<int32_t>().swap(g.sigs);
+  return SERINV_OK;
+}
+
+int get_graph(serinv_handle_t h, const GKey &key, DevGraph **out) {
+  std::lock_guard<std::mutex> lk(h->mu);
+  auto it = h->cache.find(key);
+  if (it != h->cache.end()) {
+    *out = it->second.get();
+    return SERINV_OK;
+  }
+  int kind = std::get<0>(key);
+  int64_t n = std::get<1>(key), b = std::get<2>(key), a = std::get<3>(key);
+  BuildOptions opt;
+  opt.grid = h->grid;
+  std::unique_ptr<DevGraph> dg(new DevGraph());
+  if (kind <= 2) {
+    dg->g = build_sequential(kind, n, b, a, opt);
+  } else if (kind == 3) {
+    int P = std::get<4>(key);
+    double r;
+    int64_t rb = std::get<5>(key);
+    memcpy(&r, &rb, 8);
+    dg->g = build_pselinv(n, b, a, P, r, opt);
+  } else {
+    int P = std::get<4>(key);
+    int rank = std::get<6>(key);
+    int64_t start = std::get<7>(key), count = std::get<8>(key);
+    dg->g = build_distributed(kind - 4, P, rank, n, start, count, b, a, opt);
+  }
+  if (!dg->g.error.empty()) {
+    fprintf(stderr, "serinv: graph build failed: %s\n", dg->g.error.c_str());
+    return SERINV_ERR_SHAPE;
+  }
+  int rc = upload(*dg);
+  if (rc) return rc;
+  *out = dg.get();
+  h->cache[key] = std::move(dg);
+  return SERINV_OK;
+}
+
+int launch(serinv_handle_t h, DevGraph &dg, double *bufs[BUF_COUNT], int *d_info, cudaStream_t st) {
+  if (cudaMemsetAsync(dg.ctr, 0, (size_t)(dg.g.nctr + 1) * sizeof(int32_t), st) != cudaSuccess)
+    return SERINV_ERR_CUDA;
+  if (cudaMemsetAsync(d_info, 0, sizeof(int), st) != cudaSuccess) return SERINV_ERR_CUDA;
+  dev::Params p;
+  p.tasks = dg.d_tasks;
+  p.segs = dg.d_segs;
+  p.waits = dg.d_waits;
+  p.sigs = dg.d_sigs;
+  p.ctr = dg.ctr;
+  p.claim = dg.ctr + dg.g.nctr;
+  p.ntasks = (int)dg.ntasks;
+  for (int i = 0; i < BUF_COUNT; ++i) p.bufs[i] = bufs[i];
+  p.info = d_info;
+  serinv_exec_kernel<<<h->grid, 256, h->smem, st>>>(p);
+  h->last_launches = 1;
+  return cudaGetLastError() == cudaSuccess ? SERINV_OK : SERINV_ERR_CUDA;
+}
+
+int check_bta(const serinv_bta_t *A) {
+  if (!A) return -2;
+  if (A->n < 1 || A->b < 1 || A->a < 0) return SERINV_ERR_SHAPE;
+  if (A->b > 64 * 4000 || A->a > 64 * 4000 || A->n >= (1 << 19)) return SERINV_ERR_SHAPE;
+  if (!A->diag) return -2;
+  if (A->n > 1 && !A->lower) return -2;
+  if (A->a > 0 && (!A->arrow || !A->tip)) return -2;
+  if (!aligned16(A->diag) || (A->lower && !aligned16(A->lower)) || (A->arrow && !aligned16(A->arrow)) ||
+      (A->tip && !aligned16(A->tip)))
+    return SERINV_ERR_ALIGN;
+  return SERINV_OK;
+}
+
+int run_seq(serinv_handle_t h, int kind, const serinv_bta_t *A, void *ws, size_t ws_bytes, int *d_info,
+            double *d_logdet, void *stream) {
+  if (!h) return SERINV_ERR_HANDLE;
+  int rc = check_bta(A);
+  if (rc) return rc;
+  if (!d_info) return -5;
+  if (!ws || !aligned16(ws)) return SERINV_ERR_WS;
+  if (cudaSetDevice(h->device) != cudaSuccess) return SERINV_ERR_CUDA;
+  DevGraph *dg = nullptr;
+  rc = get_graph(h, GKey(kind, A->n, A->b, A->a, 1, 0, 0, 0, 0), &dg);
+  if (rc) return rc;
+  if ((int64_t)ws_bytes < dg->g.ws_doubles * 8) return SERINV_ERR_WS;
+  double *bufs[BUF_COUNT] = {A->diag, A->lower, A->arrow, A->tip, (double *)ws, nullptr, nullptr,
+                             d_logdet ? d_logdet : h->dummy};
+  return launch(h, *dg, bufs, d_info, (cudaStream_t)stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *serinv_version(void) { return "serinv-b200 0.1.0 sm_100a"; }
+
+const char *serinv_status_string(int s) {
+  switch (s) {
+    case SERINV_OK: return "ok";
+    case SERINV_ERR_CUDA: return "CUDA error";
+    case SERINV_ERR_WS: return "workspace too small or misaligned";
+    case SERINV_ERR_NCCL: return "NCCL error";
+    case SERINV_ERR_HANDLE: return "invalid handle";
+    case SERINV_ERR_SHAPE: return "unsupported shape";
+    case SERINV_ERR_ALIGN: return "base pointer not 16-byte aligned";
+    case SERINV_ERR_PLAN: return "infeasible partition plan";
+    default: return s < 0 ? "invalid argument" : "unknown status";
+  }
+}
+
+int serinv_create(serinv_handle_t *h, int cuda_device) {
+  if (!h) return -1;
+  *h = nullptr;
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return SERINV_ERR_CUDA;
+  std::unique_ptr<serinv_ctx> c(new serinv_ctx());
+  c->device = cuda_device;
+  if (cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, cuda_device) != cudaSuccess)
+    return SERINV_ERR_CUDA;
+  c->smem = exec_smem_bytes();
+  if (cudaFuncSetAttribute(serinv_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem) !=
+      cudaSuccess)
+    return SERINV_ERR_CUDA;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, serinv_exec_kernel, 256, c->smem) != cudaSuccess ||
+      per_sm < 1)
+    return SERINV_ERR_CUDA;
+  c->grid = c->sms * per_sm;
+  if (cudaMalloc(&c->dummy, 256) != cudaSuccess) return SERINV_ERR_CUDA;
+  *h = c.release();
+  return SERINV_OK;
+}
+
+int serinv_destroy(serinv_handle_t h) {
+  if (!h) return SERINV_ERR_HANDLE;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  h->cache.clear();
+  if (h->dummy) cudaFree(h->dummy);
+  delete h;
+  return SERINV_OK;
+}
+
+int serinv_pobtaf_ws(int64_t n, int64_t b, int64_t a, size_t *bytes) {
+  if (!bytes) return -4;
+  if (n < 1 || b < 1 || a < 0) return SERINV_ERR_SHAPE;
+  *bytes = (size_t)sequential_ws_bytes(0, n, b, a);
+  return SERINV_OK;
+}
+int serinv_pobtasi_ws(int64_t n, int64_t b, int64_t a, size_t *bytes) {
+  if (!bytes) return -4;
+  if (n < 1 || b < 1 || a < 0) return SERINV_ERR_SHAPE;
+  *bytes = (size_t)sequential_ws_bytes(1, n, b, a);
+  return SERINV_OK;
+}
+int serinv_selinv_ws(int64_t n, int64_t b, int64_t a, size_t *bytes) {
+  if (!bytes) return -4;
+  if (n < 1 || b < 1 || a < 0) return SERINV_ERR_SHAPE;
+  *bytes = (size_t)sequential_ws_bytes(2, n, b, a);
+  return SERINV_OK;
+}
+
+int serinv_prepare(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_t a) {
+  if (!h) return SERINV_ERR_HANDLE;
+  if (kind < 0 || kind > 2) return -2;
+  if (n < 1 || b < 1 || a < 0) return SERINV_ERR_SHAPE;
+  cudaSetDevice(h->device);
+  DevGraph *dg;
+  return get_graph(h, GKey(kind, n, b, a, 1, 0, 0, 0, 0), &dg);
+}
+
+int serinv_pobtaf(serinv_handle_t h, const serinv_bta_t *A, void *d_ws, size_t ws_bytes, int *d_info,
+                  double *d_logdet, void *stream) {
+  return run_seq(h, 0, A, d_ws, ws_bytes, d_info, d_logdet, stream);
+}
+
+int serinv_pobtasi(serinv_handle_t h, const serinv_bta_t *L, void *d_ws, size_t ws_bytes, int *d_info,
+                   void *stream) {
+  return run_seq(h, 1, L, d_ws, ws_bytes, d_info, nullptr, stream);
+}
+
+int serinv_selinv(serinv_handle_t h, const serinv_bta_t *A, void *d_ws, size_t ws_bytes, int *d_info,
+                  double *d_logdet, void *stream) {
+  return run_seq(h, 2, A, d_ws, ws_bytes, d_info, d_logdet, stream);
+}
+
+int serinv_plan(int64_t n, int P, double r, int64_t *starts) {
+  if (!starts) return -4;
+  if (!(r > 0.0) || !std::isfinite(r)) return -3;
+  std::vector<int64_t> s;
+  if (!plan_partitions(n, P, r, s)) return SERINV_ERR_PLAN;
+  for (size_t i = 0; i < s.size(); ++i) starts[i] = s[i];
+  return SERINV_OK;
+}
+
+int serinv_pselinv_ws(int64_t n, int64_t b, int64_t a, int P, double r, size_t *bytes) {
+  if (!bytes) return -6;
+  std::vector<int64_t> s;
+  if (!plan_partitions(n, P, r, s)) return SERINV_ERR_PLAN;
+  *bytes = (size_t)pselinv_ws_bytes(n, b, a, P, r);
+  return SERINV_OK;
+}
+
+int serinv_pselinv(serinv_handle_t h, const serinv_bta_t *A, int P, double r, void *d_ws, size_t ws_bytes,
+                   int *d_info, double *d_logdet, void *stream) {
+  if (!h) return SERINV_ERR_HANDLE;
+  int rc = check_bta(A);
+  if (rc) return rc;
+  if (!d_info) return -7;
+  if (!d_ws || !aligned16(d_ws)) return SERINV_ERR_WS;
+  std::vector<int64_t> s;
+  if (!plan_partitions(A->n, P, r, s)) return SERINV_ERR_PLAN;
+  if (P == 1) return run_seq(h, 2, A, d_ws, ws_bytes, d_info, d_logdet, stream);
+  if (cudaSetDevice(h->device) != cudaSuccess) return SERINV_ERR_CUDA;
+  int64_t rb;
+  memcpy(&rb, &r, 8);
+  DevGraph *dg = nullptr;
+  rc = get_graph(h, GKey(3, A->n, A->b, A->a, P, rb, 0, 0, 0), &dg);
+  if (rc) return rc;
+  if ((int64_t)ws_bytes < dg->g.ws_doubles * 8) return SERINV_ERR_WS;
+  double *bufs[BUF_COUNT] = {A->diag, A->lower, A->arrow, A->tip, (double *)d_ws, nullptr, nullptr,
+                             d_logdet ? d_logdet : h->dummy};
+  return launch(h, *dg, bufs, d_info, (cudaStream_t)stream);
+}
+
+int serinv_exchange_bytes(int64_t b, int64_t a, size_t *bytes) {
+  if (!bytes) return -3;
+  if (b < 1 || a < 0) return SERINV_ERR_SHAPE;
+  *bytes = (size_t)exchange_doubles(b, a) * 8;
+  return SERINV_OK;
+}
+
+static int check_part(const serinv_part_t *pt) {
+  if (!pt) return -1;
+  if (pt->P < 1 || pt->rank < 0 || pt->rank >= pt->P || pt->count < 1 || pt->start < 0 ||
+      pt->start + pt->count > pt->n_global)
+    return SERINV_ERR_PLAN;
+  if (pt->P > 1 && pt->rank > 0 && pt->count < 2) return SERINV_ERR_PLAN;
+  return SERINV_OK;
+}
+
+int serinv_ppobtaf_ws(const serinv_part_t *part, int64_t b, int64_t a, size_t *bytes) {
+  int rc = check_part(part);
+  if (rc) return rc;
+  if (!bytes) return -4;
+  *bytes = (size_t)distributed_ws_bytes(part->P, part->rank, part->n_global, part->start, part->count, b, a);
+  return SERINV_OK;
+}
+
+static int run_dist(serinv_handle_t h, int phase, const serinv_part_t *part, const serinv_bta_t *A, void *d_ws,
+                    size_t ws_bytes, void *ext0, const void *ext1, int *d_info, double *d_logdet, void *stream) {
+  if (!h) return SERINV_ERR_HANDLE;
+  int rc = check_part(part);
+  if (rc) return rc;
+  if (!A || !A->diag || A->b < 1 || A->a < 0) return -3;
+  if (A->n != part->count) return -3;
+  if (A->a > 0 && (!A->arrow || !A->tip)) return -3;
+  if (part->count > 1 && !A->lower) return -3;
+  if (!d_ws || !aligned16(d_ws)) return SERINV_ERR_WS;
+  if (!d_info) return -8;
+  if (cudaSetDevice(h->device) != cudaSuccess) return SERINV_ERR_CUDA;
+  DevGraph *dg = nullptr;
+  rc = get_graph(h, GKey(4 + phase, part->n_global, A->b, A->a, part->P, 0, part->rank, part->start, part->count),
+                 &dg);
+  if (rc) return rc;
+  if ((int64_t)ws_bytes < dg->g.ws_doubles * 8) return SERINV_ERR_WS;
+  double *bufs[BUF_COUNT] = {A->diag, A->lower, A->arrow, A->tip, (double *)d_ws, (double *)ext0,
+                             (double *)ext1, d_logdet ? d_logdet : h->dummy};
+  return launch(h, *dg, bufs, d_info, (cudaStream_t)stream);
+}
+
+int serinv_ppobtaf(serinv_handle_t h, const serinv_part_t *part, const serinv_bta_t *A_local, void *d_ws,
+                   size_t ws_bytes, void *d_sendbuf, int *d_info, void *stream) {
+  if (!d_sendbuf) return -6;
+  return run_dist(h, 0, part, A_local, d_ws, ws_bytes, d_sendbuf, nullptr, d_info, nullptr, stream);
+}
+
+int serinv_ppobtasi(serinv_handle_t h, const serinv_part_t *part, const serinv_bta_t *L_local, void *d_ws,
+                    size_t ws_bytes, const void *d_recvbuf, int *d_info, double *d_logdet, void *stream) {
+  if (!d_recvbuf) return -6;
+  return run_dist(h, 1, part, L_local, d_ws, ws_bytes, nullptr, d_recvbuf, d_info, d_logdet, stream);
+}
+
+int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_t a, int P, double r,
+                       serinv_graph_stats_t *out) {
+  if (!h) return SERINV_ERR_HANDLE;
+  if (!out) return -8;
+  if (kind < 0 || kind > 3) return -2;
+  int64_t rb = 0;
+  if (kind == 3) memcpy(&rb, &r, 8);
+  cudaSetDevice(h->device);
+  DevGraph *dg = nullptr;
+  int rc = get_graph(h, GKey(kind, n, b, a, kind == 3 ? P : 1, rb, 0, 0, 0), &dg);
+  if (rc) return rc;
+  out->tasks = dg->ntasks;
+  out->counters = dg->g.nctr;
+  out->flops = dg->g.flops;
+  out->grid = h->grid;
+  out->tile = SERINV_TILE;
+  return SERINV_OK;
+}
+
+int serinv_last_launches(serinv_handle_t h, int *launches) {
+  if (!h || !launches) return SERINV_ERR_HANDLE;
+  *launches = h->last_launches;
+  return SERINV_OK;
+}
+
+}  // extern "C"

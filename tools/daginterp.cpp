@@ -1,0 +1,227 @@
+// daginterp.cpp -- TEST TOOL: executes a serinv task graph on the host, task by
+// task in emission order, with plain loops.  Used only by tests/test_graph_host.py
+// to validate the graph builder (dependencies, locations, task semantics) on a
+// machine without a GPU.  It is not linked into libserinv.so and is never on
+// the product path.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../paper_2503_17528_b200/csrc/graph.h"
+
+using namespace serinv;
+
+namespace {
+
+struct Ctx {
+  double *bufs[BUF_COUNT];
+  std::vector<int32_t> ctr;
+  int info = 0;
+};
+
+inline double *ptr(Ctx &c, const Loc &l) { return c.bufs[l.buf] + l.off; }
+inline double get(Ctx &c, const Loc &l, int r, int k) { return ptr(c, l)[(int64_t)r * l.ld + k]; }
+// op(X)[i][j]
+inline double opget(Ctx &c, const Loc &l, int trans, int i, int j) {
+  return trans ? get(c, l, j, i) : get(c, l, i, j);
+}
+
+int run(const Graph &g, Ctx &c) {
+  c.ctr.assign(g.nctr, 0);
+  std::vector<double> acc(SERINV_TILE * SERINV_TILE), tmp(SERINV_TILE * SERINV_TILE);
+  for (size_t t = 0; t < g.tasks.size(); ++t) {
+    const Task &T = g.tasks[t];
+    for (int w = 0; w < T.nwait; ++w) {
+      const Wait &W = g.waits[T.wait0 + w];
+      if (c.ctr[W.ctr] < W.target) {
+        fprintf(stderr, "task %zu (type %d): wait on counter %d not satisfied (%d < %d)\n", t, T.type, W.ctr,
+                c.ctr[W.ctr], W.target);
+        return -1;
+      }
+    }
+    const int m = T.m, n = T.n;
+    auto A_ = [&](int i, int j) -> double & { return acc[i * SERINV_TILE + j]; };
+    if (T.type == TK_GEMM || T.type == TK_POTRF) {
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < n; ++j) {
+          double s = 0;
+          for (int si = 0; si < T.nseg; ++si) {
+            const Seg &S = g.segs[T.seg0 + si];
+            for (int k = 0; k < S.k; ++k) s += opget(c, S.A, S.ta, i, k) * opget(c, S.B, S.tb, k, j);
+          }
+          double v = T.alpha * s;
+          if (T.beta != 0.0) v += T.beta * get(c, T.c0, i, j);
+          A_(i, j) = v;
+        }
+    }
+    if (T.type == TK_GEMM) {
+      if (T.flags & TF_POST) {
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < n; ++j) {
+            double s = 0;
+            for (int k = 0; k < n; ++k) s += A_(i, k) * opget(c, T.r, (T.flags & TF_POST_T) ? 1 : 0, k, j);
+            tmp[i * SERINV_TILE + j] = s;
+          }
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < n; ++j) A_(i, j) = tmp[i * SERINV_TILE + j];
+      }
+      double *o = ptr(c, T.out);
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < n; ++j) o[(int64_t)i * T.out.ld + j] = A_(i, j);
+      if (T.flags & TF_MIRROR) {
+        double *o2 = ptr(c, T.out2);
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < n; ++j) o2[(int64_t)j * T.out2.ld + i] = A_(i, j);
+      }
+      if (T.flags & TF_ZERO_MIRROR) {
+        double *o2 = ptr(c, T.out2);
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < n; ++j) o2[(int64_t)j * T.out2.ld + i] = 0.0;
+      }
+    } else if (T.type == TK_POTRF || T.type == TK_TRTRI) {
+      if (T.type == TK_TRTRI) {
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < m; ++j) A_(i, j) = j <= i ? get(c, T.c0, i, j) : 0.0;
+      } else {
+        // Cholesky (lower) of acc
+        double ls = 0;
+        for (int j = 0; j < m; ++j) {
+          double d = A_(j, j);
+          for (int k = 0; k < j; ++k) d -= A_(j, k) * A_(j, k);
+          if (!(d > 0.0)) {
+            if (!c.info || T.aux1 + j + 1 < c.info) c.info = T.aux1 + j + 1;
+            d = NAN;
+          }
+          d = std::sqrt(d);
+          A_(j, j) = d;
+          for (int i = j + 1; i < m; ++i) {
+            double s = A_(i, j);
+            for (int k = 0; k < j; ++k) s -= A_(i, k) * A_(j, k);
+            A_(i, j) = s / d;
+          }
+          ls += std::log(d);
+        }
+        for (int i = 0; i < m; ++i)
+          for (int j = i + 1; j < m; ++j) A_(i, j) = 0.0;
+        if (T.r.buf >= 0 && T.aux0 >= 0) *ptr(c, T.r) = ls;
+        double *o = ptr(c, T.out);
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < m; ++j) o[(int64_t)i * T.out.ld + j] = A_(i, j);
+      }
+      // W = L^{-1}
+      std::vector<double> W(m * m, 0.0);
+      for (int j = 0; j < m; ++j) {
+        W[j * m + j] = 1.0 / A_(j, j);
+        for (int i = j + 1; i < m; ++i) {
+          double s = 0;
+          for (int k = j; k < i; ++k) s += A_(i, k) * W[k * m + j];
+          W[i * m + j] = -s / A_(i, i);
+        }
+      }
+      Loc wl = (T.type == TK_TRTRI) ? T.out : T.out2;
+      if (T.type == TK_TRTRI || (T.flags & TF_W_OUT)) {
+        double *o = ptr(c, wl);
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < m; ++j) o[(int64_t)i * wl.ld + j] = W[i * m + j];
+      }
+      if (T.type == TK_TRTRI) {
+        for (int j = 0; j < m; ++j)
+          if (!(A_(j, j) != 0.0) || !std::isfinite(A_(j, j)))
+            if (!c.info || T.aux1 + j + 1 < c.info) c.info = T.aux1 + j + 1;
+      }
+    } else if (T.type == TK_REDUCE) {
+      double *o = ptr(c, T.out);
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < n; ++j) {
+          double s = 0;
+          for (int p = 0; p < T.aux0; ++p) s += ptr(c, T.r)[T.aux2 * p + (int64_t)i * T.r.ld + j];
+          double v = T.alpha * s;
+          if (T.beta != 0.0) v += T.beta * get(c, T.c0, i, j);
+          o[(int64_t)i * T.out.ld + j] = v;
+        }
+    } else if (T.type == TK_COPY) {
+      double *o = ptr(c, T.out);
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < n; ++j)
+          o[(int64_t)i * T.out.ld + j] = T.alpha * ((T.flags & TF_TRANS_C0) ? get(c, T.c0, j, i) : get(c, T.c0, i, j));
+    } else if (T.type == TK_LOGDET) {
+      double s = 0;
+      for (int i = 0; i < T.aux0; ++i) s += ptr(c, T.r)[i];
+      *ptr(c, T.out) = c.info ? NAN : 2.0 * s;
+    }
+    for (int s = 0; s < T.nsig; ++s) c.ctr[g.sigs[T.sig0 + s]]++;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+// kind: 0 pobtaf, 1 pobtasi, 2 selinv.  Returns 0 on success; *info as serinv.
+int dag_run_sequential(int kind, int64_t n, int64_t b, int64_t a, double *diag, double *lower, double *arrow,
+                       double *tip, double *logdet, int *info, int grid, int update_group, int64_t *ntasks) {
+  BuildOptions opt;
+  opt.grid = grid;
+  opt.update_group = update_group;
+  Graph g = build_sequential(kind, n, b, a, opt);
+  if (!g.error.empty()) {
+    fprintf(stderr, "graph error: %s\n", g.error.c_str());
+    return -2;
+  }
+  std::vector<double> ws(g.ws_doubles + 64, 0.0);
+  double ld = 0;
+  Ctx c;
+  memset(c.bufs, 0, sizeof(c.bufs));
+  c.bufs[BUF_DIAG] = diag;
+  c.bufs[BUF_LOWER] = lower;
+  c.bufs[BUF_ARROW] = arrow;
+  c.bufs[BUF_TIP] = tip;
+  c.bufs[BUF_WS] = ws.data();
+  c.bufs[BUF_LOGDET] = &ld;
+  int rc = run(g, c);
+  *info = c.info;
+  if (logdet) *logdet = ld;
+  if (ntasks) *ntasks = (int64_t)g.tasks.size();
+  return rc;
+}
+
+int dag_run_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, double *diag, double *lower, double *arrow,
+                    double *tip, double *logdet, int *info, int grid, int64_t *ntasks) {
+  BuildOptions opt;
+  opt.grid = grid;
+  Graph g = build_pselinv(n, b, a, P, r, opt);
+  if (!g.error.empty()) {
+    fprintf(stderr, "graph error: %s\n", g.error.c_str());
+    return -2;
+  }
+  std::vector<double> ws(g.ws_doubles + 64, 0.0);
+  double ld = 0;
+  Ctx c;
+  memset(c.bufs, 0, sizeof(c.bufs));
+  c.bufs[BUF_DIAG] = diag;
+  c.bufs[BUF_LOWER] = lower;
+  c.bufs[BUF_ARROW] = arrow;
+  c.bufs[BUF_TIP] = tip;
+  c.bufs[BUF_WS] = ws.data();
+  c.bufs[BUF_LOGDET] = &ld;
+  int rc = run(g, c);
+  *info = c.info;
+  if (logdet) *logdet = ld;
+  if (ntasks) *ntasks = (int64_t)g.tasks.size();
+  return rc;
+}
+
+int dag_stats_sequential(int kind, int64_t n, int64_t b, int64_t a, int grid, int64_t *ntasks, double *flops,
+                         int64_t *nctr) {
+  BuildOptions opt;
+  opt.grid = grid;
+  Graph g = build_sequential(kind, n, b, a, opt);
+  if (!g.error.empty()) return -2;
+  *ntasks = (int64_t)g.tasks.size();
+  *flops = g.flops;
+  *nctr = g.nctr;
+  return 0;
+}
+}
