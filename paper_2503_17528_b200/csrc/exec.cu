@@ -492,6 +492,7 @@ __device__ void run_copy(const Params &p, const Task &T) {
 }
 
 __device__ void run_logdet(const Params &p, const Task &T, double *smem) {
+  // *out = 2 * sum slots (fixed per-thread strides + fixed tree) + sum extras (rank order)
   const double *slots = lptr(p, T.r);
   double s = 0.0;
   for (int j = threadIdx.x; j < T.aux0; j += NT) s += __ldcg(slots + j);
@@ -502,8 +503,13 @@ __device__ void run_logdet(const Params &p, const Task &T, double *smem) {
     __syncthreads();
   }
   if (threadIdx.x == 0) {
+    double v = 2.0 * smem[0];
+    if (T.aux1 > 0) {
+      const double *ex = lptr(p, T.c0);
+      for (int j = 0; j < T.aux1; ++j) v += __ldcg(ex + T.aux2 * j);
+    }
     int inf = *(volatile int *)p.info;
-    *lptr(p, T.out) = inf ? __longlong_as_double(0x7ff8000000000000ULL) : 2.0 * smem[0];
+    *lptr(p, T.out) = inf ? __longlong_as_double(0x7ff8000000000000ULL) : v;
   }
 }
 

@@ -1,12 +1,28 @@
 // graph.cpp -- lowering of PAPER.md Alg. 1-6 to a tile-task DAG + scheduler.
 // See graph.h for the overview and task.h for the task semantics.
+//
+// Structure
+//   Ctx      the graph under construction (tasks, counters, workspace bump
+//            allocator, logdet slots, location-keyed "final X" counters) and
+//            the scheduler (finalize).
+//   Problem  one elimination problem: nodes (blocks) in elimination order and
+//            the storage of every structurally non-zero block (Y, X).
+//   Builder  lowers one Problem: factor_node (tile right-looking Cholesky,
+//            Alg. 1 / Alg. 4 lines 3-12), precompute_node (W = L^{-1},
+//            L W, W^T W: "invert L_ii once"), invert_node
+//            (Takahashi step, Alg. 2 lines 7-12 / Alg. 6 lines 2-12).
+//   build_*  assemble the problems of POBTAF / POBTASI / selinv (sequential),
+//            the in-process partitioned pipeline (Alg. 3-6 + Sec. 3.3) and the
+//            per-rank distributed graphs.
 #include "graph.h"
 
 #include <algorithm>
 #include <cassert>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <queue>
 #include <unordered_map>
 
@@ -23,34 +39,18 @@ inline Loc at(const Loc &base, int64_t r, int64_t c) {
   return l;
 }
 inline Loc tileloc(const Loc &base, int q, int c) { return at(base, (int64_t)q * TILE, (int64_t)c * TILE); }
+inline Loc wsloc(int64_t off, int64_t ld) { return Loc{BUF_WS, (int32_t)ld, off}; }
 
 // ---------------------------------------------------------------------------
-// Raw graph under construction (tasks in creation order = a topological order).
+// Graph under construction.
 // ---------------------------------------------------------------------------
 struct RawTask {
   Task t{};
   std::vector<Seg> segs;
-  std::vector<int32_t> waits;   // counters (target = #producers, fixed at finalize)
-  std::vector<int32_t> sigs;    // counters signalled (own counter first)
-  double cost = 0.0;            // ns (scheduler model)
+  std::vector<int32_t> waits;  // counters (target = #producers, fixed at finalize)
+  std::vector<int32_t> sigs;   // counters signalled (own counter first)
+  double cost = 0.0;           // ns (scheduler model)
   double flops = 0.0;
-};
-
-struct Raw {
-  std::vector<RawTask> tasks;
-  int32_t nctr = 0;
-  int32_t new_ctr() { return nctr++; }
-  // returns task id; the task's own completion counter == its id counter
-  int add(RawTask &&rt) {
-    int id = (int)tasks.size();
-    int32_t own = new_ctr();
-    rt.sigs.insert(rt.sigs.begin(), own);
-    own_ctr.push_back(own);
-    tasks.push_back(std::move(rt));
-    return id;
-  }
-  int32_t ctr_of(int task) const { return own_ctr[task]; }
-  std::vector<int32_t> own_ctr;
 };
 
 double gemm_flops(int m, int n, const std::vector<Seg> &segs) {
@@ -59,9 +59,9 @@ double gemm_flops(int m, int n, const std::vector<Seg> &segs) {
   return 2.0 * m * n * k;
 }
 
-// Scheduler cost model (ns): one CTA of a 2-CTA/SM persistent grid.
+// Scheduler cost model (ns) for one CTA of a 2-CTA/SM persistent grid.
 double task_cost(const RawTask &rt) {
-  const double ns_per_flop = 1.0 / 110.0;  // ~110 GFLOP/s per CTA
+  const double ns_per_flop = 1.0 / 110.0;
   switch (rt.t.type) {
     case TK_POTRF: return 5000.0 + rt.flops * ns_per_flop;
     case TK_TRTRI: return 2500.0;
@@ -70,37 +70,147 @@ double task_cost(const RawTask &rt) {
   }
 }
 
+Seg mkseg(Loc A, int ta, Loc Bm, int tb, int k) {
+  Seg s{};
+  s.A = A;
+  s.B = Bm;
+  s.k = k;
+  s.ta = (int8_t)ta;
+  s.tb = (int8_t)tb;
+  return s;
+}
+
+struct Ctx {
+  BuildOptions opt;
+  std::vector<RawTask> tasks;
+  std::vector<int32_t> own;
+  int32_t nctr = 0;
+  int64_t ws_top = 0;
+  int64_t slot_region = 0, slot_cap = 0, slot_count = 0;
+  std::map<std::tuple<int32_t, int64_t, int, int>, int32_t> xrc;  // final-X row/col tile counters by location
+  std::vector<int32_t> potrf_ctrs;                                  // every factor-done counter (LOGDET waits)
+
+  int32_t new_ctr() { return nctr++; }
+  int64_t alloc(int64_t doubles) {
+    int64_t o = ws_top;
+    ws_top += (std::max<int64_t>(doubles, 1) + 31) / 32 * 32;
+    return o;
+  }
+  int64_t slots(int64_t k) {
+    int64_t s = slot_count;
+    slot_count += k;
+    if (slot_count > slot_cap) fprintf(stderr, "serinv graph: slot overflow\n");
+    return s;
+  }
+  int32_t ctr_of(int task) const { return own[task]; }
+  int32_t XRC(const Loc &base, int tile, int rc) {
+    auto k = std::make_tuple(base.buf, base.off, tile, rc);
+    auto it = xrc.find(k);
+    if (it != xrc.end()) return it->second;
+    int32_t c = new_ctr();
+    xrc[k] = c;
+    return c;
+  }
+  int emit(RawTask &&rt) {
+    if (rt.t.type == TK_GEMM)
+      rt.flops = gemm_flops(rt.t.m, rt.t.n, rt.segs) + ((rt.t.flags & TF_POST) ? 2.0 * rt.t.m * rt.t.n * rt.t.n : 0.0);
+    if (rt.t.type == TK_POTRF) rt.flops = gemm_flops(rt.t.m, rt.t.n, rt.segs) + 2.0 * rt.t.m * rt.t.m * rt.t.m / 3.0;
+    if (rt.t.type == TK_TRTRI) rt.flops = rt.t.m * (double)rt.t.m * rt.t.m / 3.0;
+    rt.cost = task_cost(rt);
+    std::sort(rt.waits.begin(), rt.waits.end());
+    rt.waits.erase(std::unique(rt.waits.begin(), rt.waits.end()), rt.waits.end());
+    int id = (int)tasks.size();
+    int32_t o = new_ctr();
+    rt.sigs.insert(rt.sigs.begin(), o);
+    own.push_back(o);
+    tasks.push_back(std::move(rt));
+    return id;
+  }
+
+  // ---- data-movement tasks ---------------------------------------------
+  // out (rows x cols, row-major) = op(src), tiles of 64 x 64; src is cols x rows if trans
+  void copy_block(Loc out, Loc src, int rows, int cols, bool trans, const std::vector<int32_t> &waits,
+                  const std::vector<int32_t> &sigs_all, std::function<void(RawTask &, int, int)> tile_sigs = nullptr) {
+    for (int q = 0; q < ntiles(rows); ++q)
+      for (int c = 0; c < ntiles(cols); ++c) {
+        RawTask rt;
+        rt.t.type = TK_COPY;
+        rt.t.m = (int16_t)tdim(rows, q);
+        rt.t.n = (int16_t)tdim(cols, c);
+        rt.t.out = tileloc(out, q, c);
+        rt.t.c0 = trans ? tileloc(src, c, q) : tileloc(src, q, c);
+        rt.t.alpha = 1.0;
+        if (trans) rt.t.flags = TF_TRANS_C0;
+        rt.waits = waits;
+        rt.sigs = sigs_all;
+        if (tile_sigs) tile_sigs(rt, q, c);
+        emit(std::move(rt));
+      }
+  }
+  void sig_xblock(RawTask &rt, const Loc &base, int q, int c) {
+    rt.sigs.push_back(XRC(base, q, 0));
+    rt.sigs.push_back(XRC(base, c, 1));
+  }
+  // out = beta * C0 + alpha * sum_{j<cnt} P_j (P_j at src + j*stride), tiled
+  void reduce_block(Loc out, Loc c0, double beta, Loc src, int64_t stride, int cnt, double alpha, int rows, int cols,
+                    const std::vector<int32_t> &waits, const std::vector<int32_t> &sigs) {
+    for (int q = 0; q < ntiles(rows); ++q)
+      for (int c = 0; c < ntiles(cols); ++c) {
+        RawTask rt;
+        rt.t.type = TK_REDUCE;
+        rt.t.m = (int16_t)tdim(rows, q);
+        rt.t.n = (int16_t)tdim(cols, c);
+        rt.t.out = tileloc(out, q, c);
+        rt.t.c0 = tileloc(c0, q, c);
+        rt.t.beta = beta;
+        rt.t.r = tileloc(src, q, c);
+        rt.t.aux2 = stride;
+        rt.t.aux0 = cnt;
+        rt.t.alpha = alpha;
+        rt.waits = waits;
+        rt.sigs = sigs;
+        emit(std::move(rt));
+      }
+  }
+  // *out = 2 * sum slots[slot0 .. slot0+ns) + sum_{j<ne} extra[j*stride]  (fixed order; NaN if info)
+  int logdet(Loc out, int64_t slot0, int64_t ns, Loc extra, int ne, int64_t stride, const std::vector<int32_t> &waits) {
+    RawTask rt;
+    rt.t.type = TK_LOGDET;
+    rt.t.r = wsloc(slot_region + slot0, 0);
+    rt.t.aux0 = (int32_t)ns;
+    rt.t.c0 = extra;
+    rt.t.aux1 = ne;
+    rt.t.aux2 = stride;
+    rt.t.out = out;
+    rt.waits = waits;
+    for (int32_t c : potrf_ctrs) rt.waits.push_back(c);
+    return emit(std::move(rt));
+  }
+
+  Graph finalize();
+};
+
 // ---------------------------------------------------------------------------
-// Builder over a Problem.
+// Lowering of one elimination problem.
 // ---------------------------------------------------------------------------
 struct Builder {
-  Raw raw;
+  Ctx &cx;
   Problem &P;
-  BuildOptions opt;
-  int64_t ws_top = 0;           // next free workspace double
-  int64_t slot_top = 0;         // next logdet slot (in the slot region)
-  int64_t slot_region = -1;     // WS offset of the slot region
-
-  // L tile producers: key (Y, q, X, c) -> task
-  std::unordered_map<uint64_t, int> Lprod;
-  // per target tile chain state
+  std::unordered_map<uint64_t, int> Lprod;  // L tile producers
   struct TileState {
     std::vector<std::pair<int, int>> pending;  // columns (X, c) not yet applied
-    int last = -1;                             // last task that wrote the tile
+    int last = -1;
     bool written = false;
   };
   std::unordered_map<uint64_t, TileState> tstate;
-  // group counters
-  std::map<int, int32_t> factordone;   // node -> counter (all final L tiles of column-node X)
-  std::map<int, int32_t> predone;      // node -> counter (precompute of node X done)
-  std::map<std::tuple<int, int, int, int>, int32_t> xr, xc;  // (Y,X,tile, kind) final-X row/col
-  std::map<std::tuple<int, int>, int32_t> wcol;               // (X, c) W column complete
-  std::map<std::tuple<int, int, int>, int32_t> lcol;          // (Z, X, c) Lchk column complete
-  std::map<int, int> wdiag_task;       // (X*4096 + c) -> task producing W(c,c)
+  std::map<int, int32_t> factordone, predone;
+  std::map<std::tuple<int, int, int>, int32_t> lcol;
+  std::map<int64_t, int> wdiag_task;
+  std::map<std::tuple<int, int, int>, int> lam_task;
+  std::vector<int32_t> input_waits;  // extra waits for tasks reading the problem's inputs
 
-  Builder(Problem &p, const BuildOptions &o) : P(p), opt(o) {}
+  Builder(Ctx &c, Problem &p) : cx(c), P(p) {}
 
-  // key of tile (row node Y, row tile q) x (column node X, column tile c)
   static uint64_t key4(int Y, int q, int X, int c) {
     return ((uint64_t)(uint32_t)Y << 44) | ((uint64_t)(uint32_t)q << 32) | ((uint64_t)(uint32_t)X << 12) |
            (uint64_t)(uint32_t)c;
@@ -111,29 +221,21 @@ struct Builder {
     X = (int)((k >> 12) & 0xFFFFF);
     c = (int)(k & 0xFFF);
   }
-
-  int64_t alloc(int64_t doubles) {
-    int64_t off = ws_top;
-    ws_top += (doubles + 31) / 32 * 32;  // 256-byte granules
-    return off;
-  }
-
-  int32_t group_ctr(std::map<int, int32_t> &m, int k) {
+  int32_t gctr(std::map<int, int32_t> &m, int k) {
     auto it = m.find(k);
     if (it != m.end()) return it->second;
-    int32_t c = raw.new_ctr();
+    int32_t c = cx.new_ctr();
     m[k] = c;
     return c;
   }
-  template <class K>
-  int32_t gctr(std::map<K, int32_t> &m, const K &k) {
-    auto it = m.find(k);
-    if (it != m.end()) return it->second;
-    int32_t c = raw.new_ctr();
-    m[k] = c;
-    return c;
+  int32_t lcol_ctr(int Z, int X, int c) {
+    auto k = std::make_tuple(Z, X, c);
+    auto it = lcol.find(k);
+    if (it != lcol.end()) return it->second;
+    int32_t v = cx.new_ctr();
+    lcol[k] = v;
+    return v;
   }
-
   const BlkRef &B(int Y, int X) const {
     auto it = P.blk.find({Y, X});
     if (it == P.blk.end() || !it->second.valid) {
@@ -147,40 +249,32 @@ struct Builder {
     auto it = P.blk.find({Y, X});
     return it != P.blk.end() && it->second.valid;
   }
+  int32_t XR(int Y, int X, int q) { return cx.XRC(B(Y, X).base, q, 0); }
+  int32_t XC(int Y, int X, int c) { return cx.XRC(B(Y, X).base, c, 1); }
 
-  // ------------------------------------------------------------------ helpers
-  static Seg seg(Loc A, int ta, Loc Bm, int tb, int k) {
-    Seg s{};
-    s.A = A;
-    s.B = Bm;
-    s.k = k;
-    s.ta = (int8_t)ta;
-    s.tb = (int8_t)tb;
-    return s;
+  // workspace for W, Lambda, Lchk of every eliminated node; logdet slots
+  void allocate(bool inverse) {
+    int nn = (int)P.size.size();
+    P.W.assign(nn, Loc{});
+    P.Lam.assign(nn, Loc{});
+    P.slot.assign(nn, -1);
+    for (int X = 0; X < nn; ++X) {
+      if (!P.elim[X]) continue;
+      int64_t s = P.size[X];
+      P.W[X] = wsloc(cx.alloc(s * s), s);
+      P.slot[X] = cx.slots(ntiles(s));
+      if (inverse) {
+        P.Lam[X] = wsloc(cx.alloc(s * s), s);
+        for (int Z : P.rows[X]) P.Lchk[{Z, X}] = wsloc(cx.alloc((int64_t)P.size[Z] * s), s);
+      }
+    }
   }
 
-  int emit(RawTask &&rt) {
-    if (rt.t.type == TK_GEMM) rt.flops = gemm_flops(rt.t.m, rt.t.n, rt.segs) +
-                                        ((rt.t.flags & TF_POST) ? 2.0 * rt.t.m * rt.t.n * rt.t.n : 0.0);
-    if (rt.t.type == TK_POTRF)
-      rt.flops = gemm_flops(rt.t.m, rt.t.n, rt.segs) + 2.0 * rt.t.m * rt.t.m * rt.t.m / 3.0;
-    if (rt.t.type == TK_TRTRI) rt.flops = rt.t.m * (double)rt.t.m * rt.t.m / 3.0;
-    rt.cost = task_cost(rt);
-    // dedupe waits
-    std::sort(rt.waits.begin(), rt.waits.end());
-    rt.waits.erase(std::unique(rt.waits.begin(), rt.waits.end()), rt.waits.end());
-    return raw.add(std::move(rt));
-  }
-
-  // ===================================================================
-  // Factorisation (Alg. 1 / Alg. 4, tile-level right-looking)
-  // ===================================================================
+  // =================================================================== factor
   struct RT {
     int Y, q, h;
-    Loc loc;  // L(Y q, X c) tile
+    Loc loc;
   };
-
-  // column row-tiles of tile column (X, c)
   std::vector<RT> column_rows(int X, int c) {
     std::vector<RT> v;
     const BlkRef &d = B(X, X);
@@ -193,42 +287,7 @@ struct Builder {
     }
     return v;
   }
-
-  // target tile storage for update pair (Yi qi) >= (Yj qj) from column node X
-  BlkRef target_blk(int Yi, int Yj, int X, bool &ok) {
-    ok = true;
-    if (Yj == X) return B(Yi, X);
-    if (!has(Yi, Yj)) {
-      ok = false;
-      return BlkRef{};
-    }
-    return B(Yi, Yj);
-  }
-
   uint64_t tkey(int Yi, int Yj, int qi, int qj) { return key4(Yi, qi, Yj, qj); }
-
-  // Flush pending columns of a target tile into one chained update task.
-  // cols: list of (X, c) columns; all L tiles of rows (Yi qi) and (Yj qj) at those
-  // columns are final.  The group may span two nodes -> two segments.
-  int update_task(int Yi, int qi, int Yj, int qj, const BlkRef &tb, TileState &st,
-                  const std::vector<std::pair<int, int>> &cols) {
-    RawTask rt;
-    rt.t.type = TK_GEMM;
-    int m = tdim(P.size[Yi], qi), n = tdim(P.size[Yj], qj);
-    rt.t.m = (int16_t)m;
-    rt.t.n = (int16_t)n;
-    rt.t.out = tileloc(tb.base, qi, qj);
-    rt.t.alpha = -1.0;
-    bool first = !st.written;
-    rt.t.beta = (first && tb.zero_init) ? 0.0 : 1.0;
-    rt.t.c0 = rt.t.out;
-    add_update_segs(rt, Yi, qi, Yj, qj, cols);
-    if (st.last >= 0) rt.waits.push_back(raw.ctr_of(st.last));
-    int id = emit(std::move(rt));
-    st.last = id;
-    st.written = true;
-    return id;
-  }
 
   void add_update_segs(RawTask &rt, int Yi, int qi, int Yj, int qj, const std::vector<std::pair<int, int>> &cols) {
     size_t s = 0;
@@ -237,53 +296,61 @@ struct Builder {
       size_t e = s + 1;
       while (e < cols.size() && cols[e].first == X && cols[e].second == cols[e - 1].second + 1) ++e;
       int c1 = cols[e - 1].second;
-      // L(Yi qi, X c0..c1) and L(Yj qj, X c0..c1) are contiguous row strips
       const BlkRef &bi = (Yi == X) ? B(X, X) : B(Yi, X);
       const BlkRef &bj = (Yj == X) ? B(X, X) : B(Yj, X);
       int k = (int)(std::min<int64_t>((int64_t)(c1 + 1) * TILE, P.size[X]) - (int64_t)c0 * TILE);
-      rt.segs.push_back(seg(tileloc(bi.base, qi, c0), 0, tileloc(bj.base, qj, c0), 1, k));
+      rt.segs.push_back(mkseg(tileloc(bi.base, qi, c0), 0, tileloc(bj.base, qj, c0), 1, k));
       for (size_t u = s; u < e; ++u) {
         int c = cols[u].second;
-        rt.waits.push_back(raw.ctr_of(Lprod.at(key4(Yi, qi, X, c))));
-        rt.waits.push_back(raw.ctr_of(Lprod.at(key4(Yj, qj, X, c))));
+        rt.waits.push_back(cx.ctr_of(Lprod.at(key4(Yi, qi, X, c))));
+        rt.waits.push_back(cx.ctr_of(Lprod.at(key4(Yj, qj, X, c))));
       }
       s = e;
     }
   }
 
+  void update_task(int Yi, int qi, int Yj, int qj, const BlkRef &tb, TileState &st,
+                   const std::vector<std::pair<int, int>> &cols) {
+    RawTask rt;
+    rt.t.type = TK_GEMM;
+    rt.t.m = (int16_t)tdim(P.size[Yi], qi);
+    rt.t.n = (int16_t)tdim(P.size[Yj], qj);
+    rt.t.out = tileloc(tb.base, qi, qj);
+    rt.t.c0 = rt.t.out;
+    rt.t.alpha = -1.0;
+    rt.t.beta = (!st.written && tb.zero_init) ? 0.0 : 1.0;
+    add_update_segs(rt, Yi, qi, Yj, qj, cols);
+    if (st.last >= 0) rt.waits.push_back(cx.ctr_of(st.last));
+    for (int32_t w : input_waits) rt.waits.push_back(w);
+    st.last = cx.emit(std::move(rt));
+    st.written = true;
+  }
+
   void flush(int Yi, int qi, int Yj, int qj, const BlkRef &tb, TileState &st, size_t keep_last) {
-    // flush all pending columns except the last `keep_last`, in groups
     size_t upto = st.pending.size() - std::min(keep_last, st.pending.size());
     size_t s = 0;
+    const int G = cx.opt.update_group;
+    const bool whole = P.accum[Yj] != 0;
     while (s < upto) {
-      int G = opt.update_group;
-      bool whole_node = P.accum[Yj];
       std::vector<std::pair<int, int>> g;
       int X0 = st.pending[s].first;
       size_t e = s;
-      while (e < upto && st.pending[e].first == X0 && (whole_node || (int)g.size() < G)) {
-        g.push_back(st.pending[e]);
-        ++e;
-      }
+      while (e < upto && st.pending[e].first == X0 && (whole || (int)g.size() < G)) g.push_back(st.pending[e++]);
       update_task(Yi, qi, Yj, qj, tb, st, g);
       s = e;
     }
     st.pending.erase(st.pending.begin(), st.pending.begin() + upto);
   }
 
-  // logdet slot for a diagonal tile
-  int64_t next_slot() { return slot_top++; }
-
-  void factor_node(int X, bool fuse_w) {
+  void factor_node(int X) {
     int nt = ntiles(P.size[X]);
     const BlkRef &d = B(X, X);
-    int32_t fd = group_ctr(factordone, X);
+    int32_t fd = gctr(factordone, X);
+    cx.potrf_ctrs.push_back(fd);
     for (int c = 0; c < nt; ++c) {
       int w = tdim(P.size[X], c);
-      // ---- POTRF of the diagonal tile (X c, X c)
-      {
-        uint64_t k = tkey(X, X, c, c);
-        TileState &st = tstate[k];
+      {  // POTRF of the diagonal tile with the last update fused in
+        TileState &st = tstate[tkey(X, X, c, c)];
         flush(X, c, X, c, d, st, 1);
         RawTask rt;
         rt.t.type = TK_POTRF;
@@ -293,25 +360,25 @@ struct Builder {
         rt.t.alpha = -1.0;
         rt.t.beta = 1.0;
         if (!st.pending.empty()) add_update_segs(rt, X, c, X, c, st.pending);
-        if (st.last >= 0) rt.waits.push_back(raw.ctr_of(st.last));
+        if (st.last >= 0) rt.waits.push_back(cx.ctr_of(st.last));
+        for (int32_t iw : input_waits) rt.waits.push_back(iw);
         rt.t.flags = TF_W_OUT;
         rt.t.out2 = tileloc(P.W[X], c, c);
         rt.t.aux0 = (int32_t)(P.slot[X] + c);
-        rt.t.r = Loc{BUF_WS, 0, slot_region + P.slot[X] + c};
+        rt.t.r = wsloc(cx.slot_region + P.slot[X] + c, 0);
         rt.t.aux1 = (int32_t)(P.rowbase[X] + (int64_t)c * TILE);
         rt.sigs.push_back(fd);
-        int id = emit(std::move(rt));
+        int id = cx.emit(std::move(rt));
         st.pending.clear();
         st.last = id;
+        st.written = true;
         Lprod[key4(X, c, X, c)] = id;
-        wdiag_task[X * 4096 + c] = id;
+        wdiag_task[(int64_t)X * 4096 + c] = id;
       }
-      // ---- TRSM of every row tile below: L = (A - last update) W(c,c)^T
       std::vector<RT> rts = column_rows(X, c);
-      for (auto &r : rts) {
+      for (auto &r : rts) {  // TRSM = (A - last update) W(c,c)^T
         const BlkRef &tb = (r.Y == X) ? d : B(r.Y, X);
-        uint64_t k = tkey(r.Y, X, r.q, c);
-        TileState &st = tstate[k];
+        TileState &st = tstate[tkey(r.Y, X, r.q, c)];
         flush(r.Y, r.q, X, c, tb, st, 1);
         RawTask rt;
         rt.t.type = TK_GEMM;
@@ -321,46 +388,39 @@ struct Builder {
         rt.t.c0 = r.loc;
         rt.t.alpha = -1.0;
         rt.t.beta = (!st.written && tb.zero_init) ? 0.0 : 1.0;
-        if (!st.pending.empty()) {
+        if (!st.pending.empty())
           add_update_segs(rt, r.Y, r.q, X, c, st.pending);
-        } else {
-          rt.t.alpha = 0.0;  // no update: out = C0 * W^T
-        }
-        if (st.last >= 0) rt.waits.push_back(raw.ctr_of(st.last));
-        rt.waits.push_back(raw.ctr_of(Lprod.at(key4(X, c, X, c))));
+        else
+          rt.t.alpha = 0.0;
+        if (st.last >= 0) rt.waits.push_back(cx.ctr_of(st.last));
+        for (int32_t iw : input_waits) rt.waits.push_back(iw);
+        rt.waits.push_back(cx.ctr_of(Lprod.at(key4(X, c, X, c))));
         rt.t.flags = TF_POST | TF_POST_T;
         rt.t.r = tileloc(P.W[X], c, c);
-        if (r.Y == X) {  // strict-upper tile (c, r.q) of the diagonal block: zero it
+        if (r.Y == X) {
           rt.t.flags |= TF_ZERO_MIRROR;
           rt.t.out2 = tileloc(d.base, c, r.q);
         }
         rt.sigs.push_back(fd);
-        int id = emit(std::move(rt));
+        int id = cx.emit(std::move(rt));
         st.pending.clear();
         st.last = id;
         st.written = true;
         Lprod[key4(r.Y, r.q, X, c)] = id;
       }
-      // ---- register this column's contributions to every later target tile
-      // pairs (i >= j) of the row tiles; j must be a later column than (X, c)
-      for (size_t j = 0; j < rts.size(); ++j) {
+      for (size_t j = 0; j < rts.size(); ++j)
         for (size_t i = j; i < rts.size(); ++i) {
           const RT &ri = rts[i], &rj = rts[j];
-          bool ok;
-          BlkRef tb = target_blk(ri.Y, rj.Y, X, ok);
-          if (!ok) continue;
           if (ri.Y == rj.Y && ri.q < rj.q) continue;
-          uint64_t k = tkey(ri.Y, rj.Y, ri.q, rj.q);
-          tstate[k].pending.push_back({X, c});
+          if (rj.Y != X && ri.Y != rj.Y && !has(ri.Y, rj.Y)) continue;
+          tstate[tkey(ri.Y, rj.Y, ri.q, rj.q)].pending.push_back({X, c});
         }
-      }
-      (void)fuse_w;
     }
   }
 
-  // Flush all pending updates onto non-eliminated (boundary) targets.
-  void flush_boundary() {
-    // deterministic order: iterate sorted keys
+  // all pending updates of non-eliminated (boundary) targets become tasks;
+  // their last writers are appended to `done`
+  void flush_boundary(std::vector<int32_t> &done) {
     std::vector<uint64_t> keys;
     for (auto &kv : tstate)
       if (!kv.second.pending.empty()) keys.push_back(kv.first);
@@ -371,37 +431,33 @@ struct Builder {
       TileState &st = tstate[k];
       flush(Yi, qi, Yj, qj, B(Yi, Yj), st, 0);
     }
+    for (uint64_t k : keys) done.push_back(cx.ctr_of(tstate[k].last));
   }
 
-  // ===================================================================
-  // Selected inversion (Alg. 2 / Alg. 6 with L^{-1} precompute)
-  // ===================================================================
-  // W_X = L_XX^{-1}: diagonal tiles from POTRF (fused) or TRTRI, then
-  // W(r,c) = -(sum_{k=c+1..r} W(r,k) L(k,c)) W(c,c)   (from W L = I).
+  // ========================================================= inverse precompute
   void precompute_node(int X, bool have_wdiag) {
     int nt = ntiles(P.size[X]);
     const BlkRef &d = B(X, X);
-    // in a pobtasi-only graph L is an input: no factor-done counter to wait on
-    int32_t fd = have_wdiag ? group_ctr(factordone, X) : -1;
-    int32_t pre = group_ctr(predone, X);
+    int32_t fd = have_wdiag ? gctr(factordone, X) : -1;
+    int32_t pre = gctr(predone, X);
     std::vector<std::vector<int>> Wt(nt, std::vector<int>(nt, -1));
     for (int c = 0; c < nt; ++c) {
-      int w = tdim(P.size[X], c);
       if (have_wdiag) {
-        Wt[c][c] = wdiag_task.at(X * 4096 + c);
+        Wt[c][c] = wdiag_task.at((int64_t)X * 4096 + c);
       } else {
         RawTask rt;
         rt.t.type = TK_TRTRI;
-        rt.t.m = rt.t.n = (int16_t)w;
+        rt.t.m = rt.t.n = (int16_t)tdim(P.size[X], c);
         rt.t.c0 = tileloc(d.base, c, c);
         rt.t.out = tileloc(P.W[X], c, c);
         rt.t.aux1 = (int32_t)(P.rowbase[X] + (int64_t)c * TILE);
-        if (fd >= 0) rt.waits.push_back(fd);
+        for (int32_t iw : input_waits) rt.waits.push_back(iw);
         rt.sigs.push_back(pre);
-        Wt[c][c] = emit(std::move(rt));
+        Wt[c][c] = cx.emit(std::move(rt));
       }
     }
-    for (int r = 1; r < nt; ++r) {
+    // W(r,c) = -(sum_{k=c+1..r} W(r,k) L(k,c)) W(c,c)     (from W L = I)
+    for (int r = 1; r < nt; ++r)
       for (int c = r - 1; c >= 0; --c) {
         RawTask rt;
         rt.t.type = TK_GEMM;
@@ -411,27 +467,26 @@ struct Builder {
         rt.t.alpha = -1.0;
         rt.t.beta = 0.0;
         int k = (int)(std::min<int64_t>((int64_t)(r + 1) * TILE, P.size[X]) - (int64_t)(c + 1) * TILE);
-        rt.segs.push_back(seg(tileloc(P.W[X], r, c + 1), 0, tileloc(d.base, c + 1, c), 0, k));
-        rt.t.flags = TF_POST;  // * W(c,c)
+        rt.segs.push_back(mkseg(tileloc(P.W[X], r, c + 1), 0, tileloc(d.base, c + 1, c), 0, k));
+        rt.t.flags = TF_POST;
         rt.t.r = tileloc(P.W[X], c, c);
-        for (int kk = c + 1; kk <= r; ++kk) rt.waits.push_back(raw.ctr_of(Wt[r][kk]));
-        rt.waits.push_back(raw.ctr_of(Wt[c][c]));
+        for (int kk = c + 1; kk <= r; ++kk) rt.waits.push_back(cx.ctr_of(Wt[r][kk]));
+        rt.waits.push_back(cx.ctr_of(Wt[c][c]));
         if (fd >= 0) rt.waits.push_back(fd);
+        for (int32_t iw : input_waits) rt.waits.push_back(iw);
         rt.sigs.push_back(pre);
-        Wt[r][c] = emit(std::move(rt));
+        Wt[r][c] = cx.emit(std::move(rt));
       }
-    }
     auto wcol_wait = [&](RawTask &rt, int c) {
-      for (int r = c; r < nt; ++r) rt.waits.push_back(raw.ctr_of(Wt[r][c]));
+      for (int r = c; r < nt; ++r) rt.waits.push_back(cx.ctr_of(Wt[r][c]));
     };
-    // Lchk(Z, X)(q, c) = sum_{k >= c} L_{Z,X}(q, k) W(k, c)
+    // Lchk(Z,X)(q,c) = sum_{k >= c} L_{Z,X}(q,k) W(k,c)
     for (int Z : P.rows[X]) {
       const BlkRef &bz = B(Z, X);
       Loc lc = P.Lchk.at({Z, X});
-      int nq = ntiles(P.size[Z]);
       for (int c = 0; c < nt; ++c) {
-        int32_t lcc = gctr(lcol, std::make_tuple(Z, X, c));
-        for (int q = 0; q < nq; ++q) {
+        int32_t lcc = lcol_ctr(Z, X, c);
+        for (int q = 0; q < ntiles(P.size[Z]); ++q) {
           RawTask rt;
           rt.t.type = TK_GEMM;
           rt.t.m = (int16_t)tdim(P.size[Z], q);
@@ -439,18 +494,19 @@ struct Builder {
           rt.t.out = tileloc(lc, q, c);
           rt.t.alpha = 1.0;
           rt.t.beta = 0.0;
-          int k = (int)(P.size[X] - (int64_t)c * TILE);
-          rt.segs.push_back(seg(tileloc(bz.base, q, c), 0, tileloc(P.W[X], c, c), 0, k));
+          rt.segs.push_back(mkseg(tileloc(bz.base, q, c), 0, tileloc(P.W[X], c, c), 0,
+                                  (int)(P.size[X] - (int64_t)c * TILE)));
           wcol_wait(rt, c);
           if (fd >= 0) rt.waits.push_back(fd);
+          for (int32_t iw : input_waits) rt.waits.push_back(iw);
           rt.sigs.push_back(pre);
           rt.sigs.push_back(lcc);
-          emit(std::move(rt));
+          cx.emit(std::move(rt));
         }
       }
     }
-    // Lambda_X(r, c) = sum_{k >= r} W(k,r)^T W(k,c), r >= c
-    for (int r = 0; r < nt; ++r) {
+    // Lambda(r,c) = sum_{k >= r} W(k,r)^T W(k,c),  r >= c
+    for (int r = 0; r < nt; ++r)
       for (int c = 0; c <= r; ++c) {
         RawTask rt;
         rt.t.type = TK_GEMM;
@@ -459,32 +515,16 @@ struct Builder {
         rt.t.out = tileloc(P.Lam[X], r, c);
         rt.t.alpha = 1.0;
         rt.t.beta = 0.0;
-        int k = (int)(P.size[X] - (int64_t)r * TILE);
-        rt.segs.push_back(seg(tileloc(P.W[X], r, r), 1, tileloc(P.W[X], r, c), 0, k));
+        rt.segs.push_back(
+            mkseg(tileloc(P.W[X], r, r), 1, tileloc(P.W[X], r, c), 0, (int)(P.size[X] - (int64_t)r * TILE)));
         wcol_wait(rt, r);
         wcol_wait(rt, c);
         rt.sigs.push_back(pre);
-        lam_task[std::make_tuple(X, r, c)] = emit(std::move(rt));
+        lam_task[std::make_tuple(X, r, c)] = cx.emit(std::move(rt));
       }
-    }
-  }
-  std::map<std::tuple<int, int, int>, int> lam_task;
-
-  // counters for final-X rows / columns of storage block (Y, X)
-  int32_t XR(int Y, int X, int q) { return gctr(xr, std::make_tuple(Y, X, q, 0)); }
-  int32_t XC(int Y, int X, int c) { return gctr(xc, std::make_tuple(Y, X, c, 0)); }
-
-  // Register external producers of final X blocks (e.g. copies of X_r): a task
-  // that writes the whole block (Y, X) signals all its row/col counters.
-  void signal_whole_block(RawTask &rt, int Y, int X) {
-    int nr = ntiles(P.size[Y]), nc = ntiles(P.size[X]);
-    for (int q = 0; q < nr; ++q) rt.sigs.push_back(XR(Y, X, q));
-    for (int c = 0; c < nc; ++c) rt.sigs.push_back(XC(Y, X, c));
   }
 
-  // Read X_{Y,Z} row tile q (Y, Z in rows[X] U diag): location + transpose + waits
-  // X_{Y,Z}: if Y >= Z stored at blk(Y,Z) (row tile q, op N); else at blk(Z,Y)^T
-  // (column tile q, op T).
+  // X_{Y,Z} row tile q: Y >= Z at blk(Y,Z) (row tile, op N), else blk(Z,Y)^T (col tile, op T)
   void xrow(RawTask &rt, int Y, int Z, int q, Loc &loc, int &trans, int &k) {
     if (Y >= Z) {
       loc = tileloc(B(Y, Z).base, q, 0);
@@ -498,16 +538,14 @@ struct Builder {
     k = P.size[Z];
   }
 
-  // Takahashi step for node X (all Y in rows[X] already hold final X values).
+  // ================================================================ Takahashi
   void invert_node(int X) {
     int nt = ntiles(P.size[X]);
-    int32_t pre = group_ctr(predone, X);
+    int32_t pre = gctr(predone, X);
     const auto &R = P.rows[X];
-    // X_{Y,X}(q, c) = - sum_Z X_{Y,Z}(q, :) Lchk(Z,X)(:, c)
-    for (int Y : R) {
+    for (int Y : R) {  // X_{Y,X}(q,c) = -sum_Z X_{Y,Z}(q,:) Lchk(Z,X)(:,c)
       const BlkRef &by = B(Y, X);
-      int nq = ntiles(P.size[Y]);
-      for (int q = 0; q < nq; ++q) {
+      for (int q = 0; q < ntiles(P.size[Y]); ++q)
         for (int c = 0; c < nt; ++c) {
           RawTask rt;
           rt.t.type = TK_GEMM;
@@ -520,19 +558,18 @@ struct Builder {
             Loc a;
             int tr, k;
             xrow(rt, Y, Z, q, a, tr, k);
-            rt.segs.push_back(seg(a, tr, tileloc(P.Lchk.at({Z, X}), 0, c), 0, k));
-            rt.waits.push_back(gctr(lcol, std::make_tuple(Z, X, c)));
+            rt.segs.push_back(mkseg(a, tr, tileloc(P.Lchk.at({Z, X}), 0, c), 0, k));
+            rt.waits.push_back(lcol_ctr(Z, X, c));
           }
           rt.waits.push_back(pre);  // WAR: L_{Y,X} consumed by the precompute
           rt.sigs.push_back(XR(Y, X, q));
           rt.sigs.push_back(XC(Y, X, c));
-          emit(std::move(rt));
+          cx.emit(std::move(rt));
         }
-      }
     }
-    // X_{X,X}(r, c) = Lambda(r,c) - sum_Y X_{Y,X}(:, r)^T Lchk(Y,X)(:, c), r >= c, mirrored
+    // X_{X,X}(r,c) = Lambda(r,c) - sum_Y X_{Y,X}(:,r)^T Lchk(Y,X)(:,c), r >= c, mirrored
     const BlkRef &d = B(X, X);
-    for (int r = 0; r < nt; ++r) {
+    for (int r = 0; r < nt; ++r)
       for (int c = 0; c <= r; ++c) {
         RawTask rt;
         rt.t.type = TK_GEMM;
@@ -540,15 +577,14 @@ struct Builder {
         rt.t.n = (int16_t)tdim(P.size[X], c);
         rt.t.out = tileloc(d.base, r, c);
         rt.t.c0 = tileloc(P.Lam[X], r, c);
-        rt.t.alpha = -1.0;
+        rt.t.alpha = R.empty() ? 0.0 : -1.0;
         rt.t.beta = 1.0;
         for (int Y : R) {
-          rt.segs.push_back(seg(tileloc(B(Y, X).base, 0, r), 1, tileloc(P.Lchk.at({Y, X}), 0, c), 0, P.size[Y]));
+          rt.segs.push_back(mkseg(tileloc(B(Y, X).base, 0, r), 1, tileloc(P.Lchk.at({Y, X}), 0, c), 0, P.size[Y]));
           rt.waits.push_back(XC(Y, X, r));
-          rt.waits.push_back(gctr(lcol, std::make_tuple(Y, X, c)));
+          rt.waits.push_back(lcol_ctr(Y, X, c));
         }
-        if (R.empty()) rt.t.alpha = 0.0;
-        rt.waits.push_back(raw.ctr_of(lam_task.at(std::make_tuple(X, r, c))));
+        rt.waits.push_back(cx.ctr_of(lam_task.at(std::make_tuple(X, r, c))));
         rt.waits.push_back(pre);
         if (r != c) {
           rt.t.flags = TF_MIRROR;
@@ -560,262 +596,478 @@ struct Builder {
           rt.sigs.push_back(XR(X, X, c));
           rt.sigs.push_back(XC(X, X, r));
         }
-        emit(std::move(rt));
+        cx.emit(std::move(rt));
       }
-    }
   }
+};
 
-  // LOGDET over slots [0, nslots) of the slot region
-  void logdet_task(int64_t nslots) {
-    RawTask rt;
-    rt.t.type = TK_LOGDET;
-    rt.t.r = Loc{BUF_WS, 0, slot_region};
-    rt.t.aux0 = (int32_t)nslots;
-    rt.t.out = Loc{BUF_LOGDET, 0, 0};
-    // waits on every POTRF (all factordone counters)
-    for (auto &kv : factordone) rt.waits.push_back(kv.second);
-    emit(std::move(rt));
+// ---------------------------------------------------------------------------
+// Scheduler: bipartite DAG (tasks -> counters -> tasks), bottom-level
+// priorities, list-scheduling simulation on opt.grid workers.
+// ---------------------------------------------------------------------------
+Graph Ctx::finalize() {
+  Graph g;
+  const int N = (int)tasks.size();
+  const int C = nctr;
+  std::vector<int32_t> nprod(C, 0), nwaiter(C, 0);
+  for (auto &t : tasks) {
+    for (int32_t s : t.sigs) nprod[s]++;
+    for (int32_t w : t.waits) nwaiter[w]++;
   }
-
-  // ------------------------------------------------------------------ finalize
-  Graph finalize() {
-    Graph g;
-    const int N = (int)raw.tasks.size();
-    const int C = raw.nctr;
-    // Bipartite DAG: task -> counters it signals -> tasks waiting on them.
-    std::vector<int32_t> nprod(C, 0), nwaiter(C, 0);
-    for (auto &t : raw.tasks) {
-      for (int32_t s : t.sigs) nprod[s]++;
-      for (int32_t w : t.waits) nwaiter[w]++;
-    }
-    // CSR of waiters per counter
-    std::vector<int64_t> wptr(C + 1, 0);
-    for (int c = 0; c < C; ++c) wptr[c + 1] = wptr[c] + nwaiter[c];
-    std::vector<int32_t> wlist(wptr[C]);
-    {
-      std::vector<int64_t> fill(wptr.begin(), wptr.end() - 1);
-      for (int i = 0; i < N; ++i)
-        for (int32_t w : raw.tasks[i].waits) wlist[fill[w]++] = i;
-    }
+  std::vector<int64_t> wptr(C + 1, 0);
+  for (int c = 0; c < C; ++c) wptr[c + 1] = wptr[c] + nwaiter[c];
+  std::vector<int32_t> wlist(wptr[C]);
+  {
+    std::vector<int64_t> fill(wptr.begin(), wptr.end() - 1);
     for (int i = 0; i < N; ++i)
-      for (int32_t w : raw.tasks[i].waits)
-        if (nprod[w] == 0) {
-          g.error = "counter with no producer";
-          return g;
-        }
-    // topological order of tasks (Kahn over the bipartite graph, creation order ties)
-    std::vector<int32_t> tdeg(N), cdeg(nprod);
-    for (int i = 0; i < N; ++i) tdeg[i] = (int32_t)raw.tasks[i].waits.size();
-    std::vector<int> topo;
-    topo.reserve(N);
-    {
-      std::priority_queue<int, std::vector<int>, std::greater<int>> q;
-      for (int i = 0; i < N; ++i)
-        if (!tdeg[i]) q.push(i);
-      while (!q.empty()) {
-        int t = q.top();
-        q.pop();
-        topo.push_back(t);
-        for (int32_t s : raw.tasks[t].sigs)
-          if (--cdeg[s] == 0)
-            for (int64_t k = wptr[s]; k < wptr[s + 1]; ++k)
-              if (--tdeg[wlist[k]] == 0) q.push(wlist[k]);
-      }
-      if ((int)topo.size() != N) {
-        g.error = "dependency cycle";
-        return g;
-      }
-    }
-    // bottom levels: bl(task) = cost + max over signalled counters of max waiter bl
-    std::vector<double> bl(N, 0.0), cbl(C, 0.0);
-    for (int k = N - 1; k >= 0; --k) {
-      int t = topo[k];
-      double m = 0;
-      for (int32_t s : raw.tasks[t].sigs) m = std::max(m, cbl[s]);
-      bl[t] = raw.tasks[t].cost + m;
-      for (int32_t w : raw.tasks[t].waits) cbl[w] = std::max(cbl[w], bl[t]);
-    }
-    // list scheduling simulation
-    std::vector<int> order;
-    order.reserve(N);
-    if (opt.schedule) {
-      auto cmp = [&](int x, int y) {
-        if (bl[x] != bl[y]) return bl[x] < bl[y];
-        return x > y;
-      };
-      std::priority_queue<int, std::vector<int>, decltype(cmp)> ready(cmp);
-      typedef std::pair<double, int> Ev;
-      std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> ev;
-      for (int i = 0; i < N; ++i) tdeg[i] = (int32_t)raw.tasks[i].waits.size();
-      cdeg = nprod;
-      for (int i = 0; i < N; ++i)
-        if (!tdeg[i]) ready.push(i);
-      int free_w = std::max(1, opt.grid);
-      double now = 0;
-      while ((int)order.size() < N) {
-        while (free_w > 0 && !ready.empty()) {
-          int t = ready.top();
-          ready.pop();
-          order.push_back(t);
-          ev.push({now + raw.tasks[t].cost, t});
-          --free_w;
-        }
-        if (ev.empty()) break;
-        Ev e = ev.top();
-        ev.pop();
-        now = e.first;
-        ++free_w;
-        for (int32_t s : raw.tasks[e.second].sigs)
-          if (--cdeg[s] == 0)
-            for (int64_t k = wptr[s]; k < wptr[s + 1]; ++k)
-              if (--tdeg[wlist[k]] == 0) ready.push(wlist[k]);
-      }
-      if ((int)order.size() != N) {
-        g.error = "schedule incomplete";
-        return g;
-      }
-      g.sim_ns = now;
-    } else {
-      order = topo;
-    }
-    // emit flat arrays
-    g.tasks.reserve(N);
-    for (int t : order) {
-      RawTask &rt = raw.tasks[t];
-      Task task = rt.t;
-      task.seg0 = (int32_t)g.segs.size();
-      task.nseg = (int32_t)rt.segs.size();
-      for (auto &s : rt.segs) g.segs.push_back(s);
-      task.wait0 = (int32_t)g.waits.size();
-      task.nwait = (int32_t)rt.waits.size();
-      for (int32_t w : rt.waits) g.waits.push_back(Wait{w, nprod[w]});
-      task.sig0 = (int32_t)g.sigs.size();
-      task.nsig = (int32_t)rt.sigs.size();
-      for (int32_t s : rt.sigs) g.sigs.push_back(s);
-      g.tasks.push_back(task);
-      g.flops += rt.flops;
-    }
-    g.nctr = raw.nctr;
-    g.grid = opt.grid;
-    g.ws_doubles = ws_top;
-    g.nslots = slot_top;
-    return g;
+      for (int32_t w : tasks[i].waits) wlist[fill[w]++] = i;
   }
-};
-
-// ---------------------------------------------------------------------------
-// Sequential problem: nodes 0..n-1 (blocks) and n (the arrow tip, if a > 0).
-// ---------------------------------------------------------------------------
-struct SeqLayout {
-  int64_t n, b, a;
-  int64_t W, Wtip, Lchk, Lnchk, Lam, Lamtip, slots, total;
-};
-
-SeqLayout seq_layout(int kind, int64_t n, int64_t b, int64_t a) {
-  SeqLayout L{};
-  L.n = n;
-  L.b = b;
-  L.a = a;
-  int64_t top = 0;
-  auto take = [&](int64_t d) {
-    int64_t o = top;
-    top += (d + 31) / 32 * 32;
-    return o;
-  };
-  L.W = take(n * b * b);
-  L.Wtip = take(a * a);
-  bool inv = kind != 0;
-  L.Lchk = inv ? take(std::max<int64_t>(n - 1, 0) * b * b) : -1;
-  L.Lnchk = inv ? take(n * a * b) : -1;
-  L.Lam = inv ? take(n * b * b) : -1;
-  L.Lamtip = inv ? take(a * a) : -1;
-  L.slots = take(n * ntiles(b) + ntiles(a) + 1);
-  L.total = top;
-  return L;
+  for (int i = 0; i < N; ++i)
+    for (int32_t w : tasks[i].waits)
+      if (nprod[w] == 0) {
+        g.error = "counter with no producer";
+        return g;
+      }
+  std::vector<int32_t> tdeg(N), cdeg(nprod);
+  for (int i = 0; i < N; ++i) tdeg[i] = (int32_t)tasks[i].waits.size();
+  std::vector<int> topo;
+  topo.reserve(N);
+  {
+    std::priority_queue<int, std::vector<int>, std::greater<int>> q;
+    for (int i = 0; i < N; ++i)
+      if (!tdeg[i]) q.push(i);
+    while (!q.empty()) {
+      int t = q.top();
+      q.pop();
+      topo.push_back(t);
+      for (int32_t s : tasks[t].sigs)
+        if (--cdeg[s] == 0)
+          for (int64_t k = wptr[s]; k < wptr[s + 1]; ++k)
+            if (--tdeg[wlist[k]] == 0) q.push(wlist[k]);
+    }
+    if ((int)topo.size() != N) {
+      g.error = "dependency cycle";
+      return g;
+    }
+  }
+  std::vector<double> bl(N, 0.0), cbl(C, 0.0);
+  for (int k = N - 1; k >= 0; --k) {
+    int t = topo[k];
+    double m = 0;
+    for (int32_t s : tasks[t].sigs) m = std::max(m, cbl[s]);
+    bl[t] = tasks[t].cost + m;
+    for (int32_t w : tasks[t].waits) cbl[w] = std::max(cbl[w], bl[t]);
+  }
+  std::vector<int> order;
+  order.reserve(N);
+  if (opt.schedule) {
+    auto cmp = [&](int x, int y) {
+      if (bl[x] != bl[y]) return bl[x] < bl[y];
+      return x > y;
+    };
+    std::priority_queue<int, std::vector<int>, decltype(cmp)> ready(cmp);
+    typedef std::pair<double, int> Ev;
+    std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> ev;
+    for (int i = 0; i < N; ++i) tdeg[i] = (int32_t)tasks[i].waits.size();
+    cdeg = nprod;
+    for (int i = 0; i < N; ++i)
+      if (!tdeg[i]) ready.push(i);
+    int free_w = std::max(1, opt.grid);
+    double now = 0;
+    while ((int)order.size() < N) {
+      while (free_w > 0 && !ready.empty()) {
+        int t = ready.top();
+        ready.pop();
+        order.push_back(t);
+        ev.push({now + tasks[t].cost, t});
+        --free_w;
+      }
+      if (ev.empty()) break;
+      Ev e = ev.top();
+      ev.pop();
+      now = e.first;
+      ++free_w;
+      for (int32_t s : tasks[e.second].sigs)
+        if (--cdeg[s] == 0)
+          for (int64_t k = wptr[s]; k < wptr[s + 1]; ++k)
+            if (--tdeg[wlist[k]] == 0) ready.push(wlist[k]);
+    }
+    if ((int)order.size() != N) {
+      g.error = "schedule incomplete";
+      return g;
+    }
+    g.sim_ns = now;
+  } else {
+    order = topo;
+  }
+  g.tasks.reserve(N);
+  for (int t : order) {
+    RawTask &rt = tasks[t];
+    Task task = rt.t;
+    task.seg0 = (int32_t)g.segs.size();
+    task.nseg = (int32_t)rt.segs.size();
+    for (auto &s : rt.segs) g.segs.push_back(s);
+    task.wait0 = (int32_t)g.waits.size();
+    task.nwait = (int32_t)rt.waits.size();
+    for (int32_t w : rt.waits) g.waits.push_back(Wait{w, nprod[w]});
+    task.sig0 = (int32_t)g.sigs.size();
+    task.nsig = (int32_t)rt.sigs.size();
+    for (int32_t s : rt.sigs) g.sigs.push_back(s);
+    g.tasks.push_back(task);
+    g.flops += rt.flops;
+  }
+  g.nctr = nctr;
+  g.grid = opt.grid;
+  g.ws_doubles = ws_top;
+  g.nslots = slot_count;
+  return g;
 }
 
-void seq_problem(Problem &P, const SeqLayout &L) {
-  int64_t n = L.n, b = L.b, a = L.a;
-  int nn = (int)n + (a > 0 ? 1 : 0);
-  int A = (int)n;  // arrow node id
+// ---------------------------------------------------------------------------
+// Problem constructors
+// ---------------------------------------------------------------------------
+BlkRef blkref(Loc base, int rows, int cols, bool zero_init = false) {
+  BlkRef r;
+  r.base = base;
+  r.rows = rows;
+  r.cols = cols;
+  r.zero_init = zero_init;
+  r.valid = true;
+  return r;
+}
+
+// Block families: block i of a family at off + i * stride.
+struct Fam {
+  int32_t buf;
+  int64_t off, stride;
+  int32_t ld;
+  Loc at(int64_t i) const { return Loc{buf, ld, off + i * stride}; }
+};
+Fam famD(int64_t b) { return Fam{BUF_DIAG, 0, b * b, (int32_t)b}; }
+Fam famL(int64_t b) { return Fam{BUF_LOWER, 0, b * b, (int32_t)b}; }
+Fam famA(int64_t b, int64_t a) { return Fam{BUF_ARROW, 0, a * b, (int32_t)b}; }
+
+// A BT(A) chain problem: nodes 0..m-1 of size b (diag D(i), lower Lo(i) = (i+1,i),
+// arrow Ar(i)), then the arrow node m (size a, storage tip) if a > 0.  Nodes
+// [0, elim_upto) are eliminated; the arrow node iff elim_tip.
+void chain_problem(Problem &P, int m, int64_t b, int64_t a, std::function<Loc(int)> D, std::function<Loc(int)> Lo,
+                   std::function<Loc(int)> Ar, Loc tip, bool tip_zero, int elim_upto, bool elim_tip,
+                   std::function<int64_t(int)> rowbase, int64_t tip_rowbase) {
+  int nn = m + (a > 0 ? 1 : 0);
+  int A = m;
   P.size.assign(nn, (int)b);
   if (a > 0) P.size[A] = (int)a;
-  P.elim.assign(nn, 1);
+  P.elim.assign(nn, 0);
+  for (int i = 0; i < elim_upto; ++i) P.elim[i] = 1;
+  if (a > 0) P.elim[A] = elim_tip;
   P.accum.assign(nn, 0);
   if (a > 0) P.accum[A] = 1;
   P.rowbase.resize(nn);
-  for (int i = 0; i < nn; ++i) P.rowbase[i] = (int64_t)i * b;
   P.rows.assign(nn, {});
-  P.W.resize(nn);
-  P.Lam.resize(nn);
-  P.slot.resize(nn);
-  for (int i = 0; i < (int)n; ++i) {
-    BlkRef d;
-    d.base = Loc{BUF_DIAG, (int32_t)b, (int64_t)i * b * b};
-    d.rows = d.cols = (int)b;
-    d.valid = true;
-    P.blk[{i, i}] = d;
-    if (i + 1 < (int)n) {
-      BlkRef l;
-      l.base = Loc{BUF_LOWER, (int32_t)b, (int64_t)i * b * b};
-      l.rows = l.cols = (int)b;
-      l.valid = true;
-      P.blk[{i + 1, i}] = l;
-      P.rows[i].push_back(i + 1);
+  for (int i = 0; i < m; ++i) {
+    P.rowbase[i] = rowbase(i);
+    P.blk[{i, i}] = blkref(D(i), (int)b, (int)b);
+    if (i + 1 < m) {
+      P.blk[{i + 1, i}] = blkref(Lo(i), (int)b, (int)b);
+      if (i < elim_upto) P.rows[i].push_back(i + 1);
     }
     if (a > 0) {
-      BlkRef ar;
-      ar.base = Loc{BUF_ARROW, (int32_t)b, (int64_t)i * a * b};
-      ar.rows = (int)a;
-      ar.cols = (int)b;
-      ar.valid = true;
-      P.blk[{A, i}] = ar;
-      P.rows[i].push_back(A);
+      P.blk[{A, i}] = blkref(Ar(i), (int)a, (int)b);
+      if (i < elim_upto) P.rows[i].push_back(A);
     }
-    P.W[i] = Loc{BUF_WS, (int32_t)b, L.W + (int64_t)i * b * b};
-    P.Lam[i] = Loc{BUF_WS, (int32_t)b, L.Lam >= 0 ? L.Lam + (int64_t)i * b * b : 0};
-    if (L.Lchk >= 0 && i + 1 < (int)n) P.Lchk[{i + 1, i}] = Loc{BUF_WS, (int32_t)b, L.Lchk + (int64_t)i * b * b};
-    if (L.Lnchk >= 0 && a > 0) P.Lchk[{A, i}] = Loc{BUF_WS, (int32_t)b, L.Lnchk + (int64_t)i * a * b};
-    P.slot[i] = (int64_t)i * ntiles(b);
   }
   if (a > 0) {
-    BlkRef t;
-    t.base = Loc{BUF_TIP, (int32_t)a, 0};
-    t.rows = t.cols = (int)a;
-    t.valid = true;
-    P.blk[{A, A}] = t;
-    P.W[A] = Loc{BUF_WS, (int32_t)a, L.Wtip};
-    P.Lam[A] = Loc{BUF_WS, (int32_t)a, L.Lamtip >= 0 ? L.Lamtip : 0};
-    P.slot[A] = n * ntiles(b);
+    P.rowbase[A] = tip_rowbase;
+    P.blk[{A, A}] = blkref(tip, (int)a, (int)a, tip_zero);
+  }
+}
+
+// Middle partition (Alg. 4) on buffers whose block s is at local index ls:
+// nodes 0..k-1 = blocks s+1..e-1 (k = e-s-1; node k-1 is the boundary l),
+// F = k (block s, moved last by the implicit shifting permutation),
+// arrow = k+1.  Bbuf(j) stores the fill-in block (F, node j): rows f, columns j.
+void middle_problem(Problem &P, int64_t ls, int64_t cnt, int64_t b, int64_t a, Loc U, const Fam &Bbuf,
+                    int64_t glob_s) {
+  int k = (int)(cnt - 1);
+  int F = k, A = k + 1;
+  int nn = k + 1 + (a > 0 ? 1 : 0);
+  P.size.assign(nn, (int)b);
+  if (a > 0) P.size[A] = (int)a;
+  P.elim.assign(nn, 0);
+  for (int j = 0; j + 1 < k; ++j) P.elim[j] = 1;  // interior s+1..e-2
+  P.accum.assign(nn, 0);
+  P.accum[F] = 1;
+  if (a > 0) P.accum[A] = 1;
+  P.rowbase.resize(nn);
+  P.rows.assign(nn, {});
+  for (int j = 0; j < k; ++j) {
+    int64_t li = ls + 1 + j;
+    P.rowbase[j] = (glob_s + 1 + j) * b;
+    P.blk[{j, j}] = blkref(famD(b).at(li), (int)b, (int)b);
+    bool el = j + 1 < k;
+    if (el) {
+      P.blk[{j + 1, j}] = blkref(famL(b).at(li), (int)b, (int)b);
+      P.rows[j].push_back(j + 1);
+    }
+    // B_{s+1} = A_{s+1,s}^T is copied in; later B_j start as fill-in zeros
+    P.blk[{F, j}] = blkref(Bbuf.at(j), (int)b, (int)b, j > 0);
+    if (el) P.rows[j].push_back(F);
+    if (a > 0) {
+      P.blk[{A, j}] = blkref(famA(b, a).at(li), (int)a, (int)b);
+      if (el) P.rows[j].push_back(A);
+    }
+  }
+  P.rowbase[F] = glob_s * b;
+  P.blk[{F, F}] = blkref(famD(b).at(ls), (int)b, (int)b);
+  if (a > 0) {
+    P.rowbase[A] = -1;
+    P.blk[{A, F}] = blkref(famA(b, a).at(ls), (int)a, (int)b);
+    P.blk[{A, A}] = blkref(U, (int)a, (int)a, true);
+  }
+}
+
+int64_t slot_bound(int64_t nblocks, int64_t b, int64_t a) { return nblocks * ntiles(b) + ntiles(a) + 8; }
+
+Graph build_seq_ctx(Ctx &cx, int kind, int64_t n, int64_t b, int64_t a) {
+  bool fact = kind != 1, inv = kind != 0;
+  cx.slot_cap = slot_bound(n, b, a);
+  cx.slot_region = cx.alloc(cx.slot_cap);
+  Problem P;
+  chain_problem(
+      P, (int)n, b, a, [&](int i) { return famD(b).at(i); }, [&](int i) { return famL(b).at(i); },
+      [&](int i) { return famA(b, a).at(i); }, Loc{BUF_TIP, (int32_t)a, 0}, false, (int)n, true,
+      [&](int i) { return (int64_t)i * b; }, n * b);
+  Builder bld(cx, P);
+  bld.allocate(inv);
+  int nn = (int)P.size.size();
+  if (fact) {
+    for (int X = 0; X < nn; ++X) bld.factor_node(X);
+    cx.logdet(Loc{BUF_LOGDET, 0, 0}, 0, cx.slot_count, Loc{BUF_WS, 0, 0}, 0, 0, {});
+  }
+  if (inv) {
+    for (int X = 0; X < nn; ++X) bld.precompute_node(X, fact);
+    for (int X = nn - 1; X >= 0; --X) bld.invert_node(X);
+  }
+  return cx.finalize();
+}
+
+// ---------------------------------------------------------------------------
+// Partitioned pipeline (shared by the in-process graph and the per-rank graphs)
+// ---------------------------------------------------------------------------
+struct PartState {
+  int p = 0;
+  int64_t s = 0, e = 0;  // global block range
+  int64_t ls = 0;        // local index of block s in the buffers
+  Problem prob;
+  std::unique_ptr<Builder> bld;
+  Loc U{};                    // a x a tip accumulator
+  Fam Bbuf{};                 // fill-in chain (middle partitions)
+  std::vector<int32_t> done;  // counters: everything the factor phase wrote
+  int nelim = 0;
+};
+
+// PPOBTAF for one partition (Alg. 3 line 3 / line 5): factor the interior and
+// flush the Schur updates into the boundary blocks, U_p and (middle) B_{e-1}.
+void ppobtaf_part(Ctx &cx, PartState &ps, int64_t b, int64_t a) {
+  bool top = ps.p == 0;
+  int64_t cnt = ps.e - ps.s;
+  ps.U = wsloc(cx.alloc(std::max<int64_t>(a * a, 1)), std::max<int64_t>(a, 1));
+  if (top) {
+    int64_t ls = ps.ls;
+    chain_problem(
+        ps.prob, (int)cnt, b, a, [&](int i) { return famD(b).at(ls + i); }, [&](int i) { return famL(b).at(ls + i); },
+        [&](int i) { return famA(b, a).at(ls + i); }, ps.U, true, (int)cnt - 1, false,
+        [&](int i) { return (ps.s + i) * b; }, -1);
+  } else {
+    ps.Bbuf = Fam{BUF_WS, cx.alloc((cnt - 1) * b * b), b * b, (int32_t)b};
+    middle_problem(ps.prob, ps.ls, cnt, b, a, ps.U, ps.Bbuf, ps.s);
+  }
+  ps.bld.reset(new Builder(cx, ps.prob));
+  Builder &B = *ps.bld;
+  B.allocate(true);
+  if (!top) {  // B_{s+1} = A_{s+1,s}^T (Alg. 4 line 1, reading R7)
+    int32_t c = cx.new_ctr();
+    cx.copy_block(ps.Bbuf.at(0), famL(b).at(ps.ls), (int)b, (int)b, true, {}, {c});
+    B.input_waits.push_back(c);
+    ps.done.push_back(c);
+  }
+  for (size_t X = 0; X < ps.prob.size.size(); ++X)
+    if (ps.prob.elim[X]) {
+      B.factor_node((int)X);
+      ++ps.nelim;
+    }
+  B.flush_boundary(ps.done);
+  if (a > 0 && ps.nelim == 0) {  // U_p = 0 when nothing is eliminated
+    int32_t z = cx.new_ctr();
+    cx.reduce_block(ps.U, ps.U, 0.0, ps.U, 0, 0, 0.0, (int)a, (int)a, {}, {z});
+    ps.done.push_back(z);
+  }
+  for (auto &kv : B.factordone) ps.done.push_back(kv.second);
+}
+
+// one rank's exchange record (doubles): boundary blocks, couplings, U_p, log det
+struct XRec {
+  int64_t b, a;
+  int64_t bd0() const { return 0; }          // A_TT (top) or A_ff (middle)
+  int64_t bd1() const { return b * b; }      // A_ll (middle)
+  int64_t lw0() const { return 2 * b * b; }  // coupling A_{e,e-1} to the next rank (original)
+  int64_t lw1() const { return 3 * b * b; }  // B_{e-1} (rows f, columns l)
+  int64_t ar0() const { return 4 * b * b; }
+  int64_t ar1() const { return 4 * b * b + a * b; }
+  int64_t U() const { return 4 * b * b + 2 * a * b; }
+  int64_t ld() const { return 4 * b * b + 2 * a * b + a * a; }
+};
+
+// pack partition ps into record `rec` (buffer rbuf, offset r0)
+void pack_part(Ctx &cx, PartState &ps, int P, int64_t b, int64_t a, int32_t rbuf, int64_t r0, int32_t sig) {
+  XRec x{b, a};
+  auto rec = [&](int64_t off, int64_t ld) { return Loc{rbuf, (int32_t)ld, r0 + off}; };
+  int64_t cnt = ps.e - ps.s, ls = ps.ls;
+  const auto &w = ps.done;
+  if (ps.p == 0) {
+    cx.copy_block(rec(x.bd0(), b), famD(b).at(ls + cnt - 1), (int)b, (int)b, false, w, {sig});
+    if (a > 0) cx.copy_block(rec(x.ar0(), b), famA(b, a).at(ls + cnt - 1), (int)a, (int)b, false, w, {sig});
+  } else {
+    cx.copy_block(rec(x.bd0(), b), famD(b).at(ls), (int)b, (int)b, false, w, {sig});
+    cx.copy_block(rec(x.bd1(), b), famD(b).at(ls + cnt - 1), (int)b, (int)b, false, w, {sig});
+    cx.copy_block(rec(x.lw1(), b), ps.Bbuf.at(cnt - 2), (int)b, (int)b, false, w, {sig});
+    if (a > 0) {
+      cx.copy_block(rec(x.ar0(), b), famA(b, a).at(ls), (int)a, (int)b, false, w, {sig});
+      cx.copy_block(rec(x.ar1(), b), famA(b, a).at(ls + cnt - 1), (int)a, (int)b, false, w, {sig});
+    }
+  }
+  if (ps.p < P - 1) cx.copy_block(rec(x.lw0(), b), famL(b).at(ls + cnt - 1), (int)b, (int)b, false, {}, {sig});
+  if (a > 0) cx.copy_block(rec(x.U(), a), ps.U, (int)a, (int)a, false, w, {sig});
+}
+
+struct Reduced {
+  Fam D, Lo, Ar;
+  Loc tip;
+  Problem P;
+  std::unique_ptr<Builder> B;
+};
+
+// Assemble A_r (2P-1 blocks, reading R9) from the P records at (rbuf, rec0 +
+// p*recsz), then POBTARSSI = POBTAF + POBTASI on it (Sec. 3.3).  The reduced tip
+// A_nn + U_0 + ... + U_{P-1} (reading R8) is formed in place in BUF_TIP.
+void reduced_from_records(Ctx &cx, int P, int64_t n, int64_t b, int64_t a, int32_t rbuf, int64_t rec0, int64_t recsz,
+                          const std::vector<int64_t> &starts, const std::vector<int32_t> &inwaits, Reduced &R) {
+  XRec x{b, a};
+  int nr = 2 * P - 1;
+  R.D = Fam{BUF_WS, cx.alloc(nr * b * b), b * b, (int32_t)b};
+  R.Lo = Fam{BUF_WS, cx.alloc(std::max(nr - 1, 1) * b * b), b * b, (int32_t)b};
+  R.Ar = Fam{BUF_WS, cx.alloc(std::max<int64_t>(nr * a * b, 1)), a * b, (int32_t)b};
+  auto rec = [&](int p, int64_t off, int64_t ld) { return Loc{rbuf, (int32_t)ld, rec0 + p * recsz + off}; };
+  int32_t cr = cx.new_ctr();
+  std::vector<int32_t> ready{cr};
+  cx.copy_block(R.D.at(0), rec(0, x.bd0(), b), (int)b, (int)b, false, inwaits, {cr});
+  if (a > 0) cx.copy_block(R.Ar.at(0), rec(0, x.ar0(), b), (int)a, (int)b, false, inwaits, {cr});
+  for (int p = 1; p < P; ++p) {
+    cx.copy_block(R.D.at(2 * p - 1), rec(p, x.bd0(), b), (int)b, (int)b, false, inwaits, {cr});
+    cx.copy_block(R.D.at(2 * p), rec(p, x.bd1(), b), (int)b, (int)b, false, inwaits, {cr});
+    if (a > 0) {
+      cx.copy_block(R.Ar.at(2 * p - 1), rec(p, x.ar0(), b), (int)a, (int)b, false, inwaits, {cr});
+      cx.copy_block(R.Ar.at(2 * p), rec(p, x.ar1(), b), (int)a, (int)b, false, inwaits, {cr});
+    }
+    cx.copy_block(R.Lo.at(2 * p - 2), rec(p - 1, x.lw0(), b), (int)b, (int)b, false, inwaits, {cr});
+    cx.copy_block(R.Lo.at(2 * p - 1), rec(p, x.lw1(), b), (int)b, (int)b, true, inwaits, {cr});
+  }
+  R.tip = Loc{BUF_TIP, (int32_t)std::max<int64_t>(a, 1), 0};
+  if (a > 0) {
+    int32_t ct = cx.new_ctr();
+    cx.reduce_block(R.tip, R.tip, 1.0, rec(0, x.U(), a), recsz, P, 1.0, (int)a, (int)a, inwaits, {ct});
+    ready.push_back(ct);
+  }
+  auto rb = [&](int i) -> int64_t {
+    int64_t blk;
+    if (i == 0)
+      blk = starts[1] - 1;
+    else {
+      int p = (i + 1) / 2;
+      blk = (i & 1) ? starts[p] : starts[p + 1] - 1;
+    }
+    return blk >= 0 ? blk * b : n * b;
+  };
+  chain_problem(
+      R.P, nr, b, a, [&](int i) { return R.D.at(i); }, [&](int i) { return R.Lo.at(i); },
+      [&](int i) { return R.Ar.at(i); }, R.tip, false, nr, true, rb, n * b);
+  R.B.reset(new Builder(cx, R.P));
+  R.B->input_waits = ready;
+  R.B->allocate(true);
+  int nn = (int)R.P.size.size();
+  for (int X = 0; X < nn; ++X) R.B->factor_node(X);
+  for (int X = 0; X < nn; ++X) R.B->precompute_node(X, true);
+  for (int X = nn - 1; X >= 0; --X) R.B->invert_node(X);
+}
+
+// Copy the true-inverse boundary blocks of partition ps from X_r into its
+// storage and signal their final-X counters ("POBTARSSI's result is copied to
+// PPOBTASI's L and B"; reading R10).
+void scatter_xr(Ctx &cx, PartState &ps, int P, int64_t b, int64_t a, const Reduced &R) {
+  int p = ps.p;
+  Problem &Q = ps.prob;
+  auto cp = [&](Loc dst, Loc src, int rows, int cols, bool trans) {
+    std::vector<int32_t> w = ps.done;  // WAR on everything the factor phase read / wrote
+    int sr = trans ? cols : rows, sc = trans ? rows : cols;
+    for (int q = 0; q < ntiles(sr); ++q) w.push_back(cx.XRC(src, q, 0));
+    for (int c = 0; c < ntiles(sc); ++c) w.push_back(cx.XRC(src, c, 1));
+    cx.copy_block(dst, src, rows, cols, trans, w, {}, [&](RawTask &rt, int q, int c) { cx.sig_xblock(rt, dst, q, c); });
+  };
+  int nn = (int)Q.size.size();
+  if (p == 0) {
+    int T = (int)(ps.e - ps.s) - 1;
+    cp(Q.blk.at({T, T}).base, R.D.at(0), (int)b, (int)b, false);
+    if (a > 0) cp(Q.blk.at({nn - 1, T}).base, R.Ar.at(0), (int)a, (int)b, false);
+  } else {
+    int k = (int)(ps.e - ps.s) - 1, F = k, L = k - 1;
+    cp(Q.blk.at({F, F}).base, R.D.at(2 * p - 1), (int)b, (int)b, false);
+    cp(Q.blk.at({L, L}).base, R.D.at(2 * p), (int)b, (int)b, false);
+    if (a > 0) {
+      cp(Q.blk.at({F + 1, F}).base, R.Ar.at(2 * p - 1), (int)a, (int)b, false);
+      cp(Q.blk.at({F + 1, L}).base, R.Ar.at(2 * p), (int)a, (int)b, false);
+    }
+    cp(Q.blk.at({F, L}).base, R.Lo.at(2 * p - 1), (int)b, (int)b, true);  // Q_{e-1} = X_r(L_p,F_p)^T
+  }
+  if (p < P - 1)  // coupling to the next partition: X_r(F_{p+1}, L_p)
+    cp(famL(b).at(ps.ls + (ps.e - ps.s) - 1), R.Lo.at(2 * p), (int)b, (int)b, false);
+  // the tip node of the partition now stands for the true X_nn (in BUF_TIP)
+  if (a > 0) Q.blk[{nn - 1, nn - 1}] = blkref(R.tip, (int)a, (int)a);
+}
+
+// PPOBTASI for one partition (Alg. 5 line 3 / line 5).
+void ppobtasi_part(Ctx &cx, PartState &ps, int64_t b, bool have_wdiag) {
+  Builder &B = *ps.bld;
+  int nn = (int)ps.prob.size.size();
+  for (int X = 0; X < nn; ++X)
+    if (ps.prob.elim[X]) B.precompute_node(X, have_wdiag);
+  for (int X = nn - 1; X >= 0; --X)
+    if (ps.prob.elim[X]) B.invert_node(X);
+  if (ps.p > 0) {  // X_{s+1,s} = Q_{s+1}^T (reading R10)
+    std::vector<int32_t> w;
+    for (int q = 0; q < ntiles(b); ++q) w.push_back(cx.XRC(ps.Bbuf.at(0), q, 0));
+    cx.copy_block(famL(b).at(ps.ls), ps.Bbuf.at(0), (int)b, (int)b, true, w, {});
   }
 }
 
 }  // namespace
 
 int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a) {
-  return seq_layout(kind, n, b, a).total * 8;
+  // mirrors the allocation order of build_seq_ctx (checked in build_sequential)
+  auto up = [](int64_t d) { return (std::max<int64_t>(d, 1) + 31) / 32 * 32; };
+  bool inv = kind != 0;
+  int64_t tot = up(slot_bound(n, b, a));
+  tot += n * (up(b * b) + (inv ? up(b * b) : 0));
+  if (inv) tot += (n - 1) * up(b * b) + (a > 0 ? n * up(a * b) : 0);
+  if (a > 0) tot += up(a * a) + (inv ? up(a * a) : 0);
+  return tot * 8;
 }
 
 Graph build_sequential(int kind, int64_t n, int64_t b, int64_t a, const BuildOptions &opt) {
-  SeqLayout L = seq_layout(kind, n, b, a);
-  Problem P;
-  seq_problem(P, L);
-  Builder bld(P, opt);
-  bld.ws_top = L.total;
-  bld.slot_region = L.slots;
-  int nn = (int)P.size.size();
-  bool fact = kind != 1, inv = kind != 0;
-  if (fact) {
-    for (int X = 0; X < nn; ++X) bld.factor_node(X, true);
-    bld.slot_top = n * ntiles(b) + ntiles(a);
-    bld.logdet_task(bld.slot_top);
-  }
-  if (inv) {
-    for (int X = 0; X < nn; ++X) bld.precompute_node(X, fact);
-    for (int X = nn - 1; X >= 0; --X) bld.invert_node(X);
-  }
-  Graph g = bld.finalize();
-  g.ws_doubles = L.total;
+  Ctx cx;
+  cx.opt = opt;
+  Graph g = build_seq_ctx(cx, kind, n, b, a);
+  if (g.error.empty() && g.ws_doubles * 8 > sequential_ws_bytes(kind, n, b, a))
+    g.error = "workspace accounting mismatch";
   return g;
 }
 
@@ -840,20 +1092,109 @@ bool plan_partitions(int64_t n, int P, double r, std::vector<int64_t> &starts) {
   return s == n;
 }
 
-}  // namespace serinv
+int64_t exchange_doubles(int64_t b, int64_t a) { return (4 * b * b + 2 * a * b + a * a + 1 + 31) / 32 * 32; }
 
-namespace serinv {
-Graph build_pselinv(int64_t, int64_t, int64_t, int, double, const BuildOptions &) {
-  Graph g;
-  g.error = "pselinv not built yet";
-  return g;
+Graph build_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, const BuildOptions &opt) {
+  std::vector<int64_t> starts;
+  if (!plan_partitions(n, P, r, starts)) {
+    Graph bad;
+    bad.error = "infeasible plan";
+    return bad;
+  }
+  Ctx cx;
+  cx.opt = opt;
+  cx.slot_cap = slot_bound(n + 2 * P, b, a);
+  cx.slot_region = cx.alloc(cx.slot_cap);
+  int64_t recsz = exchange_doubles(b, a);
+  int64_t recs = cx.alloc(recsz * P);
+  std::vector<PartState> parts(P);
+  for (int p = 0; p < P; ++p) {
+    parts[p].p = p;
+    parts[p].s = starts[p];
+    parts[p].e = starts[p + 1];
+    parts[p].ls = starts[p];
+    ppobtaf_part(cx, parts[p], b, a);
+  }
+  int32_t packed = cx.new_ctr();
+  for (int p = 0; p < P; ++p) pack_part(cx, parts[p], P, b, a, BUF_WS, recs + p * recsz, packed);
+  Reduced R;
+  reduced_from_records(cx, P, n, b, a, BUF_WS, recs, recsz, starts, {packed}, R);
+  for (int p = 0; p < P; ++p) {
+    parts[p].done.push_back(packed);  // scatter overwrites what the pack copies read
+    scatter_xr(cx, parts[p], P, b, a, R);
+    ppobtasi_part(cx, parts[p], b, true);
+  }
+  cx.logdet(Loc{BUF_LOGDET, 0, 0}, 0, cx.slot_count, Loc{BUF_WS, 0, 0}, 0, 0, {});
+  return cx.finalize();
 }
-int64_t pselinv_ws_bytes(int64_t, int64_t, int64_t, int, double) { return 0; }
-Graph build_distributed(int, int, int, int64_t, int64_t, int64_t, int64_t, int64_t, const BuildOptions &) {
-  Graph g;
-  g.error = "distributed not built yet";
-  return g;
+
+int64_t pselinv_ws_bytes(int64_t n, int64_t b, int64_t a, int P, double r) {
+  BuildOptions opt;
+  opt.schedule = false;
+  Graph g = build_pselinv(n, b, a, P, r, opt);
+  return g.error.empty() ? g.ws_doubles * 8 : -1;
 }
-int64_t distributed_ws_bytes(int, int, int64_t, int64_t, int64_t, int64_t, int64_t) { return 0; }
-int64_t exchange_doubles(int64_t, int64_t) { return 0; }
+
+// Distributed per-rank graphs.  Phase 0 (ppobtaf): factor the local partition
+// and pack the exchange record into EXT0.  Phase 1 (ppobtasi): assemble A_r
+// from the all-gathered records in EXT1 (rank order, identical on every rank),
+// POBTARSSI redundantly, scatter this rank's X_r blocks, backward pass.  Both
+// phases lay the workspace out identically (phase 1 replays the factor-phase
+// allocations), so the fill-in factor blocks B_i survive between the calls.
+Graph build_distributed(int phase, int P, int rank, int64_t n, int64_t start, int64_t count, int64_t b, int64_t a,
+                        const BuildOptions &opt) {
+  Ctx cx;
+  cx.opt = opt;
+  cx.slot_cap = slot_bound(count + 2 * P + 2, b, a);
+  cx.slot_region = cx.alloc(cx.slot_cap);
+  int64_t recsz = exchange_doubles(b, a);
+  XRec x{b, a};
+  PartState ps;
+  ps.p = rank;
+  ps.s = start;
+  ps.e = start + count;
+  ps.ls = 0;
+  ppobtaf_part(cx, ps, b, a);
+  if (phase == 0) {
+    int32_t packed = cx.new_ctr();
+    pack_part(cx, ps, P, b, a, BUF_EXT0, 0, packed);
+    cx.logdet(Loc{BUF_EXT0, 0, x.ld()}, 0, cx.slot_count, Loc{BUF_WS, 0, 0}, 0, 0, {});
+    return cx.finalize();
+  }
+  // phase 1: the factor tasks ran in phase 0; keep their workspace layout only
+  cx.tasks.clear();
+  cx.own.clear();
+  cx.potrf_ctrs.clear();
+  cx.xrc.clear();
+  Builder &PB = *ps.bld;
+  PB.factordone.clear();
+  PB.Lprod.clear();
+  PB.tstate.clear();
+  PB.input_waits.clear();
+  PB.wdiag_task.clear();
+  ps.done.clear();
+  int64_t part_slots = cx.slot_count;
+  std::vector<int64_t> st(P + 1, -1);
+  st[rank] = start;
+  st[rank + 1] = start + count;
+  st[0] = 0;
+  st[P] = n;
+  Reduced R;
+  reduced_from_records(cx, P, n, b, a, BUF_EXT1, 0, recsz, st, {}, R);
+  scatter_xr(cx, ps, P, b, a, R);
+  ppobtasi_part(cx, ps, b, false);  // W tiles recomputed by TRTRI (no fused POTRF here)
+  // log det = sum of the ranks' partials (rank order) + 2 sum log diag of POBTAF(A_r)
+  cx.logdet(Loc{BUF_LOGDET, 0, 0}, part_slots, cx.slot_count - part_slots, Loc{BUF_EXT1, 0, x.ld()}, P, recsz, {});
+  return cx.finalize();
+}
+
+int64_t distributed_ws_bytes(int P, int rank, int64_t n, int64_t start, int64_t count, int64_t b, int64_t a) {
+  BuildOptions opt;
+  opt.schedule = false;
+  Graph g0 = build_distributed(0, P, rank, n, start, count, b, a, opt);
+  Graph g1 = build_distributed(1, P, rank, n, start, count, b, a, opt);
+  if (!g0.error.empty() || !g1.error.empty()) return -1;
+  return std::max(g0.ws_doubles, g1.ws_doubles) * 8;
+}
+
 }  // namespace serinv

@@ -1,0 +1,135 @@
+"""Host logic of the product: the task-graph builder and scheduler (graph.cpp),
+checked on CPU by executing the emitted task lists with the host interpreter
+test tool (tools/daginterp.cpp, plain loops).  The interpreter also asserts
+that every wait is satisfied at claim time, i.e. that the emission order is a
+valid topological order (the persistent executor's deadlock-freedom premise).
+
+This validates dependencies, block/tile locations, fusion and the partitioned
+assembly; the CUDA tile kernels themselves are covered by the -m gpu tests.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import btagen
+from oracle import invariants as inv, parallel as par, sequential as seq
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        from paper_2503_17528_b200.build import build_daginterp
+        _lib = ctypes.CDLL(build_daginterp())
+    return _lib
+
+
+P_ = ctypes.c_void_p
+KEYS = ("diag", "lower", "arrow", "tip")
+
+
+def prep(A):
+    A = {k: np.ascontiguousarray(np.array(A[k], dtype=np.float64)) for k in KEYS}
+    n, b, a = A["diag"].shape[0], A["diag"].shape[1], A["tip"].shape[0]
+    if A["lower"].size == 0:
+        A["lower"] = np.zeros((1, b, b))
+    if A["arrow"].size == 0:
+        A["arrow"] = np.zeros((1, 1, b))
+    if A["tip"].size == 0:
+        A["tip"] = np.zeros((1, 1))
+    return A, n, b, a
+
+
+def cut(R, X):
+    a = X["tip"].shape[0]
+    return {k: (R[k][:X[k].shape[0]] if k != "tip" else R[k][:a, :a]) for k in X}
+
+
+def ptrs(A):
+    return [A[k].ctypes.data_as(P_) for k in KEYS]
+
+
+def run_seq(kind, A0, grid=16, ug=4):
+    A, n, b, a = prep(A0)
+    ld, info, nt = ctypes.c_double(0), ctypes.c_int(0), ctypes.c_int64(0)
+    rc = lib().dag_run_sequential(kind, ctypes.c_int64(n), ctypes.c_int64(b), ctypes.c_int64(a), *ptrs(A),
+                                  ctypes.byref(ld), ctypes.byref(info), grid, ug, ctypes.byref(nt))
+    assert rc == 0
+    return A, ld.value, info.value
+
+
+SHAPES = [(8, 4, 2), (3, 70, 5), (4, 130, 70), (5, 64, 0), (2, 200, 3), (1, 100, 10), (6, 5, 3), (1, 1, 0),
+          (3, 129, 1)]
+
+
+@pytest.mark.parametrize("n,b,a", SHAPES)
+def test_sequential_graphs(n, b, a):
+    A0 = btagen.g2(1, n, b, a)
+    L, X, ld = seq.selinv(A0)
+    R, ldr, info = run_seq(2, A0)
+    assert info == 0
+    assert inv.max_block_err(cut(R, X), X)[0] < 1e-12
+    assert abs(ldr - ld) <= 1e-12 * max(1, abs(ld))
+    F, ldf, info = run_seq(0, A0)
+    assert inv.max_block_err(cut(F, L), L)[0] < 1e-12
+    assert abs(ldf - ld) <= 1e-12 * max(1, abs(ld))
+    S, _, info = run_seq(1, L)
+    assert inv.max_block_err(cut(S, X), X)[0] < 1e-12
+
+
+@pytest.mark.parametrize("ug", [1, 2, 7])
+@pytest.mark.parametrize("grid", [1, 3, 296])
+def test_schedule_options_do_not_change_results(ug, grid):
+    A0 = btagen.g1(4, 4, 150, 9)
+    L, X, ld = seq.selinv(A0)
+    R, ldr, info = run_seq(2, A0, grid=grid, ug=ug)
+    assert inv.max_block_err(cut(R, X), X)[0] < 1e-12
+
+
+def test_info_first_bad_pivot():
+    A0 = btagen.g1(5, 5, 70, 3)
+    A0["diag"][2][10, 10] = -1e7
+    _, ld, info = run_seq(0, A0)
+    assert info == 2 * 70 + 11
+    assert np.isnan(ld)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("n,b,a", [(17, 4, 2), (24, 70, 5), (30, 8, 0), (16, 65, 3)])
+def test_pselinv_and_distributed_graphs(P, n, b, a):
+    if n < 2 * P - 1:
+        pytest.skip("too few blocks")
+    A0 = btagen.g2(7, n, b, a)
+    L, X, ld = seq.selinv(A0)
+    for runner in ("dag_run_pselinv", "dag_run_distributed"):
+        A, n_, b_, a_ = prep(A0)
+        ldv, info = ctypes.c_double(0), ctypes.c_int(0)
+        if runner == "dag_run_pselinv":
+            nt = ctypes.c_int64(0)
+            rc = lib().dag_run_pselinv(ctypes.c_int64(n), ctypes.c_int64(b), ctypes.c_int64(a), P,
+                                       ctypes.c_double(1.0), *ptrs(A), ctypes.byref(ldv), ctypes.byref(info), 16,
+                                       ctypes.byref(nt))
+        else:
+            rc = lib().dag_run_distributed(ctypes.c_int64(n), ctypes.c_int64(b), ctypes.c_int64(a), P,
+                                           ctypes.c_double(1.0), *ptrs(A), ctypes.byref(ldv), ctypes.byref(info))
+        assert rc == 0 and info.value == 0
+        e, where = inv.max_block_err(cut(A, X), X)
+        assert e < 1e-11, (runner, e, where)
+        assert abs(ldv.value - ld) <= 1e-12 * max(1, abs(ld))
+
+
+def test_partition_plan_matches_oracle_reading():
+    import paper_2503_17528_b200._lib  # noqa: F401  (the product plan lives in libserinv)
+    # serinv_plan is exported by libserinv.so; compare with the oracle's reading R6 when available
+    try:
+        from paper_2503_17528_b200 import plan
+        for n in range(1, 40):
+            for P in range(1, 7):
+                for r in (0.5, 1.0, 1.8, 2.25):
+                    if n < 2 * P - 1:
+                        continue
+                    assert plan(n, P, r) == par.plan(n, P, r)
+    except ImportError:
+        pytest.skip("libserinv.so not built")

@@ -148,7 +148,9 @@ int run(const Graph &g, Ctx &c) {
     } else if (T.type == TK_LOGDET) {
       double s = 0;
       for (int i = 0; i < T.aux0; ++i) s += ptr(c, T.r)[i];
-      *ptr(c, T.out) = c.info ? NAN : 2.0 * s;
+      double v = 2.0 * s;
+      for (int j = 0; j < T.aux1; ++j) v += ptr(c, T.c0)[T.aux2 * j];
+      *ptr(c, T.out) = c.info ? NAN : v;
     }
     for (int s = 0; s < T.nsig; ++s) c.ctr[g.sigs[T.sig0 + s]]++;
   }
@@ -211,6 +213,75 @@ int dag_run_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, double *di
   if (logdet) *logdet = ld;
   if (ntasks) *ntasks = (int64_t)g.tasks.size();
   return rc;
+}
+
+// Simulate P ranks of the distributed path on the host.  Global arrays in, X out
+// (in place); each rank works on copies of its local blocks.
+int dag_run_distributed(int64_t n, int64_t b, int64_t a, int P, double r, double *diag, double *lower, double *arrow,
+                        double *tip, double *logdet, int *info) {
+  std::vector<int64_t> st;
+  if (!plan_partitions(n, P, r, st)) return -3;
+  int64_t rec = exchange_doubles(b, a);
+  std::vector<double> records(rec * P, 0.0);
+  struct Rank {
+    std::vector<double> D, L, A, T, ws;
+    int64_t cnt;
+    Ctx c;
+  };
+  std::vector<Rank> R(P);
+  BuildOptions opt;
+  opt.grid = 8;
+  for (int p = 0; p < P; ++p) {
+    Rank &k = R[p];
+    int64_t s = st[p], e = st[p + 1], cnt = e - s;
+    k.cnt = cnt;
+    k.D.assign(diag + s * b * b, diag + e * b * b);
+    int64_t nl = (p < P - 1) ? cnt : cnt - 1;
+    k.L.assign(std::max<int64_t>(nl, 1) * b * b, 0.0);
+    if (nl > 0) std::copy(lower + s * b * b, lower + (s + nl) * b * b, k.L.begin());
+    k.A.assign(std::max<int64_t>(cnt * a * b, 1), 0.0);
+    if (a) std::copy(arrow + s * a * b, arrow + e * a * b, k.A.begin());
+    k.T.assign(std::max<int64_t>(a * a, 1), 0.0);
+    if (a) std::copy(tip, tip + a * a, k.T.begin());
+    Graph g0 = build_distributed(0, P, p, n, s, cnt, b, a, opt);
+    Graph g1 = build_distributed(1, P, p, n, s, cnt, b, a, opt);
+    if (!g0.error.empty() || !g1.error.empty()) {
+      fprintf(stderr, "graph error: %s %s\n", g0.error.c_str(), g1.error.c_str());
+      return -2;
+    }
+    k.ws.assign(std::max(g0.ws_doubles, g1.ws_doubles) + 64, 0.0);
+    memset(k.c.bufs, 0, sizeof(k.c.bufs));
+    k.c.bufs[BUF_DIAG] = k.D.data();
+    k.c.bufs[BUF_LOWER] = k.L.data();
+    k.c.bufs[BUF_ARROW] = k.A.data();
+    k.c.bufs[BUF_TIP] = k.T.data();
+    k.c.bufs[BUF_WS] = k.ws.data();
+    k.c.bufs[BUF_EXT0] = records.data() + p * rec;
+    if (run(g0, k.c)) return -1;
+    if (k.c.info) *info = k.c.info;
+  }
+  double ld = 0;
+  for (int p = 0; p < P; ++p) {
+    Rank &k = R[p];
+    Graph g1 = build_distributed(1, P, p, n, st[p], k.cnt, b, a, opt);
+    double ldp = 0;
+    k.c.bufs[BUF_EXT0] = nullptr;
+    k.c.bufs[BUF_EXT1] = records.data();
+    k.c.bufs[BUF_LOGDET] = &ldp;
+    k.c.info = 0;
+    if (run(g1, k.c)) return -1;
+    if (k.c.info && !*info) *info = k.c.info;
+    if (p == 0) ld = ldp;
+    else if (!(ldp == ld) && !(std::isnan(ld) && std::isnan(ldp))) fprintf(stderr, "rank logdet mismatch\n");
+    int64_t s = st[p], e = st[p + 1], cnt = k.cnt;
+    std::copy(k.D.begin(), k.D.begin() + cnt * b * b, diag + s * b * b);
+    int64_t nl = (p < P - 1) ? cnt : cnt - 1;
+    if (nl > 0) std::copy(k.L.begin(), k.L.begin() + nl * b * b, lower + s * b * b);
+    if (a) std::copy(k.A.begin(), k.A.begin() + cnt * a * b, arrow + s * a * b);
+    if (a && p == 0) std::copy(k.T.begin(), k.T.begin() + a * a, tip);
+  }
+  *logdet = ld;
+  return 0;
 }
 
 int dag_stats_sequential(int kind, int64_t n, int64_t b, int64_t a, int grid, int64_t *ntasks, double *flops,
