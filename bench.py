@@ -1,0 +1,325 @@
+#!/usr/bin/env python3
+"""bench.py -- FP64 POBTAF + POBTASI (Serinv, arXiv 2503.17528) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One step = one pass of the whole hot path: POBTAF followed
+by POBTASI of a synthetic SPD BTA matrix (generator G1, seed 0) -- the fused
+`serinv_selinv` task graph at N = 1, the distributed PPOBTAF -> all-gather ->
+PPOBTASI at N > 1 (weak scaling: every rank owns the configured n blocks).
+Metric (BASELINE.json): FP64 TFLOP/s of POBTAF + POBTASI, algorithmic flop count
+(LAPACK conventions, sequential count for distributed runs),
+device-timed with CUDA events; fraction of the measured FP64 DMMA peak.
+
+--impl reference times the CPU oracle (oracle/, numpy/scipy FP64) on a bounded
+sample of the same workload (the paper's code does not exist).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {  # BASELINE.json configs
+    "C1": dict(n=8, b=4, a=2),
+    "C2": dict(n=128, b=1024, a=64),
+    "C3": dict(n=365, b=2048, a=4),
+    "C4": dict(n=256, b=512, a=16),
+    "C5": dict(n=16384, b=64, a=8),
+}
+METRIC = "FP64 seconds & TFLOP/s for POBTAF+POBTASI (1/2/4/8 B200), fraction of FP64 peak"
+FP64_PEAK_TFLOPS = 37.1   # measured DMMA peak, profiles/fp64_peaks_r01.json
+L2_BYTES = 126 * 2 ** 20
+
+
+def flops_pobtaf(n, b, a):
+    return (n - 1) * (7 / 3 * b ** 3 + 3 * a * b * b + a * a * b) + b ** 3 / 3 + a * b * b + a * a * b + a ** 3 / 3
+
+
+def flops_pobtasi(n, b, a):
+    return ((n - 1) * (14 / 3 * b ** 3 + 6 * a * b * b + 2 * a * a * b)
+            + 2 * b ** 3 / 3 + 2 * a * b * b + 2 * a * a * b + 2 * a ** 3 / 3)
+
+
+def bta_bytes(n, b, a):
+    return 8 * (n * b * b + (n - 1) * b * b + n * a * b + a * a)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--r", type=float, default=1.0, help="load-balance ratio for N > 1")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- CPU oracle
+def cpu_oracle_rate(cfg, budget_s=20.0, max_blocks=None):
+    """Time the oracle (as it stands) on a bounded sample: selinv on n' blocks of the
+    configured (b, a).  Returns (TFLOP/s, seconds, n', cores)."""
+    import numpy as np  # noqa: F401
+    import btagen
+    from oracle import sequential as seq
+    n, b, a = cfg["n"], cfg["b"], cfg["a"]
+    cores = len(os.sched_getaffinity(0))
+    nprime = 2
+    while True:
+        A = btagen.g1(0, nprime, b, a)
+        t0 = time.perf_counter()
+        seq.selinv(A)
+        dt = time.perf_counter() - t0
+        if dt * 2 > budget_s or nprime >= n or (max_blocks and nprime >= max_blocks):
+            break
+        nprime = min(n, nprime * 2)
+    fl = flops_pobtaf(nprime, b, a) + flops_pobtasi(nprime, b, a)
+    return fl / dt / 1e12, dt, nprime, cores
+
+
+def reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n, b, a = cfg["n"], cfg["b"], cfg["a"]
+    times = []
+    tf = None
+    nprime = None
+    cores = len(os.sched_getaffinity(0))
+    for it in range(args.warmup + args.steps):
+        rate, dt, nprime, cores = cpu_oracle_rate(cfg, budget_s=8.0)
+        if it >= args.warmup:
+            times.append(dt)
+            tf = rate if tf is None else min(tf, rate) if False else rate
+    fl = flops_pobtaf(nprime, b, a) + flops_pobtasi(nprime, b, a)
+    med = statistics.median(times)
+    value = fl / med / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(med * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} n={n} b={b} a={a}", "n": n, "b": b, "a": a,
+                   "generator": "g1 seed 0", "sample_blocks": nprime},
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": f"oracle selinv (numpy/scipy FP64) on n'={nprime} of the {n} blocks, same b, a"},
+        "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return reference_arm(args, cfg)
+    import torch
+    import torch.distributed as dist
+    import btagen
+    import paper_2503_17528_b200 as sb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    N = max(args.gpus, world)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n_loc, b, a = cfg["n"], cfg["b"], cfg["a"]
+    n = n_loc * world
+    fl = flops_pobtaf(n, b, a) + flops_pobtasi(n, b, a)
+    h = sb.default_handle(local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- inputs resident in HBM (pristine copy restored between steps, untimed)
+    if world == 1:
+        A = btagen.g1(0, n, b, a)
+        host = {k: torch.from_numpy(A[k]) for k in ("diag", "lower", "arrow", "tip")}
+        pristine = {k: v.cuda() for k, v in host.items()}
+        work = {k: v.clone() for k, v in pristine.items()}
+
+        def step(info=None, logdet=None):
+            return sb.selinv(work["diag"], work["lower"], work["arrow"], work["tip"], handle=h,
+                             check=False, info=info, logdet=logdet)
+    else:
+        from paper_2503_17528_b200 import distributed as sd
+        A = btagen.g1(0, n, b, a)
+        parts = sb.plan(n, world, args.r)
+        s, e = parts[rank]
+        host = sd.local_blocks(A, s, e, last=(rank == world - 1))
+        pristine = {k: torch.from_numpy(v).cuda() for k, v in host.items()}
+        work = {k: v.clone() for k, v in pristine.items()}
+        ctx = sd.DistContext(h, world, rank, n, s, e - s, b, a, device=local)
+
+        def step(info=None, logdet=None):
+            return sd.pselinv_step(ctx, work, check=False)
+
+    def restore():
+        for k in work:
+            work[k].copy_(pristine[k])
+
+    # ---- warmup
+    for _ in range(args.warmup):
+        restore()
+        step()
+    torch.cuda.synchronize()
+    info = h.scalars()[0]
+    if int(info.item()) != 0:
+        raise SystemExit(f"factorisation failed: info={int(info.item())}")
+
+    # ---- timed steps (device events on the library stream, max over ranks)
+    stream = torch.cuda.current_stream()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            restore()
+            barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    launches = h.last_launches()
+    t = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total = float(t.item())
+    sec_per_step = total / args.steps
+    value = fl / sec_per_step / 1e12
+
+    # ---- end to end through the public API with host buffers (pinned H2D, D2H of X + logdet)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        pinned = {k: v.pin_memory() for k, v in host.items()}
+        out = {k: torch.empty_like(v).pin_memory() for k, v in host.items()}
+        ld_host = torch.empty(1, dtype=torch.float64).pin_memory()
+        h2d = sum(v.numel() * 8 for v in pinned.values())
+        d2h = h2d + 8
+        et = []
+        for it in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for k in work:
+                work[k].copy_(pinned[k], non_blocking=True)
+            step()
+            for k in work:
+                out[k].copy_(work[k], non_blocking=True)
+            ld_host.copy_(h.scalars()[1], non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if it >= args.warmup:
+                et.append(e0.elapsed_time(e1) / 1e3)
+        e2e = {"value": round(fl / statistics.mean(et) / 1e12, 4), "unit": "TFLOP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": round(statistics.mean(et) * 1e3, 3)}
+
+    # ---- CPU baseline (oracle as it stands), rank 0, N = 1 only, bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, dt, nprime, cores = cpu_oracle_rate(cfg, budget_s=20.0)
+        cpu = {"value": round(rate, 6), "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+               "sample": f"oracle selinv (numpy/scipy FP64) on n'={nprime} of the {n} blocks (b={b}, a={a}), "
+                         f"{dt:.1f} s"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": N,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec_per_step * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{args.config} n={n_loc} b={b} a={a} per GPU", "n_global": n, "b": b, "a": a,
+                       "generator": "g1 seed 0", "parallelism": f"partitions{world}" if world > 1 else "single",
+                       "l2": f"inputs {bta_bytes(n_loc, b, a) / 1e9:.2f} GB per GPU > 126 MB L2",
+                       "step": "POBTAF+POBTASI (serinv_selinv)" if world == 1 else
+                               "PPOBTAF + NCCL all-gather + PPOBTASI"},
+            "seconds_per_step": round(sec_per_step, 6),
+            "tflops_pobtaf_plus_pobtasi": round(value, 4),
+            "fraction_of_fp64_peak": round(value / (FP64_PEAK_TFLOPS * N), 4),
+            "roofline": {"bound": "tensor", "achieved": round(value / N, 4), "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": round(value / N / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                         "kernel": "serinv_exec_kernel (persistent, 1 launch per step)",
+                         "peak_source": "measured DMMA f64 peak, profiles/fp64_peaks_r01.json"},
+            "clocks": clocks,
+            "gpu_launches": launches * args.steps,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -38,6 +38,8 @@
  *            (LAPACK dpotrf semantics): block (k-1)/b, or the tip if k > n*b.
  *            Outputs are then undefined and *d_logdet is NaN.
  *     k > 0  (pobtasi) zero / non-finite diagonal entry of L at global row k.
+ *     -1     internal watchdog fired (a dependency never completed within 20 s);
+ *            outputs undefined.  Indicates a library bug, never a property of A.
  * No host synchronisation happens inside any call (all work is enqueued on
  * `stream`, a cudaStream_t passed as void*).
  */
@@ -199,6 +201,14 @@ typedef struct {
 } serinv_graph_stats_t;
 int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_t a, int P,
                        double r, serinv_graph_stats_t *out);
+
+/* Tracing: while d_trace != NULL, every launch whose graph has at most
+ * bytes/96 tasks records 4 x uint64 per task (in emission order):
+ * {claim time, start time (inputs ready), end time, meta}, times from the GPU
+ * global timer (ns); meta = type | smid << 16 | m << 32 | n << 48; followed
+ * by 8 x uint64 per task of phase timestamps (POTRF / TRTRI tasks). 
+ * Pass NULL to disable. */
+int serinv_set_trace(serinv_handle_t h, void *d_trace, size_t bytes);
 
 /* Number of kernel launches enqueued by the last compute call of this handle. */
 int serinv_last_launches(serinv_handle_t h, int *launches);

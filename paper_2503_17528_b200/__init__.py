@@ -143,6 +143,8 @@ def _finish(h: Handle, info_t, logdet_t, check: bool, b: int, n: int):
     if not check:
         return None
     info = int(info_t.item())
+    if info < 0:
+        raise RuntimeError("serinv: internal watchdog fired (a task dependency never completed)")
     if info:
         raise NotPositiveDefinite(info, b, n)
     return float(logdet_t.item()) if logdet_t is not None else None
@@ -224,4 +226,5 @@ def graph_stats(kind: int, n: int, b: int, a: int, P: int = 1, r: float = 1.0, h
     return dict(tasks=st.tasks, counters=st.counters, flops=st.flops, grid=st.grid, tile=st.tile)
 
 
-from .distributed import ppobtaf, ppobtasi  # noqa: E402
+from .distributed import ppobtaf, ppobtasi  # noqa: E402,F401
+from . import distributed  # noqa: E402,F401

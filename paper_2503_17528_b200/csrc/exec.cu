@@ -58,6 +58,17 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+
 __device__ __forceinline__ double *lptr(const Params &p, const Loc &l) { return p.bufs[l.buf] + l.off; }
 
 __device__ void record_info(int *info, int v) {
@@ -136,16 +147,16 @@ __device__ __forceinline__ void mma_steps(const double *As, int sAr, int sAk, co
   }
 }
 
-// Main loop: acc = sum_s op(A_s) op(B_s) over all segments of task T.
-__device__ void gemm_mainloop(const Params &p, const Task &T, double *smem, double (&acc)[2][4][2]) {
+// Main loop: acc = sum_s op(A_s) op(B_s) over segments [s0, s0 + ns) (output m x n).
+__device__ void gemm_mainloop(const Params &p, int s0, int ns, int m, int n, double *smem, double (&acc)[2][4][2]) {
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  if (T.nseg == 0) return;
-  const Seg *segs = p.segs + T.seg0;
+  if (ns == 0) return;
+  const Seg *segs = p.segs + s0;
   int nchunks = 0;
-  for (int s = 0; s < T.nseg; ++s) nchunks += (segs[s].k + KC - 1) / KC;
+  for (int s = 0; s < ns; ++s) nchunks += (segs[s].k + KC - 1) / KC;
   // load-side cursor
   int ls = 0, lk = 0;
   auto issue = [&](int stage) {
@@ -154,8 +165,8 @@ __device__ void gemm_mainloop(const Params &p, const Task &T, double *smem, doub
     double *Bs = As + OPSZ;
     bool vecA = ((S.A.off | S.A.ld) & 1) == 0;
     bool vecB = ((S.B.off | S.B.ld) & 1) == 0;
-    load_operand(As, lptr(p, S.A), S.A.ld, S.ta != 0, T.m, S.k, lk, vecA);
-    load_operand(Bs, lptr(p, S.B), S.B.ld, S.tb == 0, T.n, S.k, lk, vecB);
+    load_operand(As, lptr(p, S.A), S.A.ld, S.ta != 0, m, S.k, lk, vecA);
+    load_operand(Bs, lptr(p, S.B), S.B.ld, S.tb == 0, n, S.k, lk, vecB);
     lk += KC;
     if (lk >= S.k) {
       lk = 0;
@@ -198,9 +209,10 @@ __device__ __forceinline__ void frag_rc(int mi, int ni, int h, int &r, int &c) {
   c = (warp & 1) * 32 + ni * 8 + 2 * (lane & 3) + h;
 }
 
-// acc = alpha * acc + beta * C0
-__device__ __forceinline__ void apply_c0(const Params &p, const Task &T, double (&acc)[2][4][2]) {
-  const double *c0 = (T.beta != 0.0) ? lptr(p, T.c0) : nullptr;
+// acc = alpha * acc + beta * C0   (C0: m x n at loc)
+__device__ __forceinline__ void apply_c0(const Params &p, double alpha, double beta, const Loc &loc, int m, int n,
+                                         double (&acc)[2][4][2]) {
+  const double *c0 = (beta != 0.0) ? lptr(p, loc) : nullptr;
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -209,8 +221,8 @@ __device__ __forceinline__ void apply_c0(const Params &p, const Task &T, double 
       for (int h = 0; h < 2; ++h) {
         int r, c;
         frag_rc(mi, ni, h, r, c);
-        double v = T.alpha * acc[mi][ni][h];
-        if (c0 && r < T.m && c < T.n) v += T.beta * __ldcg(c0 + (int64_t)r * T.c0.ld + c);
+        double v = alpha * acc[mi][ni][h];
+        if (c0 && r < m && c < n) v += beta * __ldcg(c0 + (int64_t)r * loc.ld + c);
         acc[mi][ni][h] = v;
       }
 }
@@ -234,6 +246,26 @@ __device__ __forceinline__ void tile_to_smem(double *St, const double *g, int ld
     int r = idx >> 6, c = idx & 63;
     St[r * LDT + c] = (r < m && c < n) ? __ldcg(g + (int64_t)r * ld + c) : 0.0;
   }
+}
+
+__device__ void store_tile(const Params &p, const Loc &loc, int m, int n, const double (&acc)[2][4][2]) {
+  double *o = lptr(p, loc);
+  const bool vec = ((loc.off | loc.ld) & 1) == 0;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      int r, c;
+      frag_rc(mi, ni, 0, r, c);
+      if (r >= m) continue;
+      double *dst = o + (int64_t)r * loc.ld + c;
+      if (vec && c + 1 < n) {
+        *reinterpret_cast<double2 *>(dst) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      } else {
+        if (c < n) dst[0] = acc[mi][ni][0];
+        if (c + 1 < n) dst[1] = acc[mi][ni][1];
+      }
+    }
 }
 
 __device__ void store_acc(const Params &p, const Task &T, const double (&acc)[2][4][2]) {
@@ -275,8 +307,8 @@ __device__ void store_acc(const Params &p, const Task &T, const double (&acc)[2]
 // ---------------------------------------------------------------------------
 __device__ void run_gemm(const Params &p, const Task &T, double *smem) {
   double acc[2][4][2];
-  gemm_mainloop(p, T, smem, acc);
-  apply_c0(p, T, acc);
+  gemm_mainloop(p, T.seg0, T.nseg, T.m, T.n, smem, acc);
+  apply_c0(p, T.alpha, T.beta, T.c0, T.m, T.n, acc);
   if (T.flags & TF_POST) {
     double *St = smem;
     double *Rt = smem + SERINV_TILE * LDT;
@@ -295,174 +327,225 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem) {
   store_acc(p, T, acc);
 }
 
-// 16 x 16 thread grid; thread (ty, tx) owns rows ty + 16 ii, cols tx + 16 kk.
-// Right-looking unscaled Cholesky (one barrier per pivot), then row-oriented
-// TRTRI W = L^{-1} (one barrier per row).
-__device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bool factor) {
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+__device__ __forceinline__ void phase_mark(const Params &p, int t, int k) {
+  if (p.trace && threadIdx.x == 0) p.trace[4 * (size_t)p.ntasks + 8 * (size_t)t + k] = globaltimer();
+}
+
+// select v[ii][kk] for runtime kk (keeps the arrays in registers)
+__device__ __forceinline__ double sel4(const double (&row)[4], int kk) {
+  double x = row[0];
+  x = (kk == 1) ? row[1] : x;
+  x = (kk == 2) ? row[2] : x;
+  x = (kk == 3) ? row[3] : x;
+  return x;
+}
+__device__ __forceinline__ void set4(double (&row)[4], int kk, double x) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (q == kk) row[q] = x;
+}
+
+// Tile Cholesky + inverse of the diagonal tile (64 x 64), fused into ONE pivot
+// loop with one CTA barrier per pivot:
+//   thread (r = tid & 15, c = tid >> 4) owns S[i][k], i = r + 16 ii, k = c + 16 kk,
+//   so the 16 owners of a column sit in one half-warp.  At step j the owners of
+//   column j+1 take the pivot by shuffle, scale their column by rsqrt(d) and
+//   publish it (L column j+1); everybody applies the rank-1 update of L column j.
+//   The inverse W = L^{-1} is built row by row in the same loop
+//   (W[j][:] = (e_j - sum_{s<j} L[j][s] W[s][:]) / L[j][j], right-looking),
+//   with multiplications by the published 1/L_jj only -- no divisions.
+__device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bool factor, int tsk) {
+  const int tid = threadIdx.x, r = tid & 15, c = tid >> 4;
+  const int lane = tid & 31;
   const int m = T.m;
-  double *St = smem;                          // [64][LDT]  the tile (L after factor)
-  double *cb = smem + SERINV_TILE * LDT;      // [2][64] column / row broadcast
-  double *dv = cb + 2 * SERINV_TILE;          // [64] pivots d_j (then L_jj)
-  double *lg = dv + SERINV_TILE;              // [64] log L_jj
+  double *St = smem;                      // [64][LDT] staging of the input tile
+  double *lb = smem + SERINV_TILE * LDT;  // [3][64] published L columns
+  double *wb = lb + 3 * SERINV_TILE;      // [2][64] published W rows
+  double *rsv = wb + 2 * SERINV_TILE;     // [64] 1 / L_jj
+  double *dv = rsv + SERINV_TILE;         // [64] pivots d_j (factor) / L_jj (trtri)
+  __shared__ int s_bad;
   if (factor) {
     double acc[2][4][2];
-    gemm_mainloop(p, T, smem, acc);
-    apply_c0(p, T, acc);
+    gemm_mainloop(p, T.seg0, T.nseg1, T.m, T.n, smem, acc);
+    apply_c0(p, T.alpha, T.beta, T.c0, T.m, T.n, acc);
     acc_to_smem(St, acc);
   } else {
     tile_to_smem(St, lptr(p, T.c0), T.c0.ld, m, m);
   }
+  if (tid == 0) s_bad = 1 << 30;
   __syncthreads();
-  double v[4][4];
+  phase_mark(p, tsk, 0);
+  double v[4][4], w[4][4];
 #pragma unroll
   for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) v[ii][kk] = St[(ty + 16 * ii) * LDT + tx + 16 * kk];
-  if (factor) {
-    for (int j = 0; j < m; ++j) {
-      double *buf = cb + (j & 1) * SERINV_TILE;
-      if (tx == (j & 15)) {
-        const int kk = j >> 4;
+    for (int kk = 0; kk < 4; ++kk) {
+      v[ii][kk] = St[(r + 16 * ii) * LDT + c + 16 * kk];
+      w[ii][kk] = 0.0;
+    }
+  // owners of column q publish it (factor: pivot + scaling; trtri: as given)
+  auto publish_col = [&](int q) {
+    const int kk = q >> 4;
+    const int src = (lane & 16) | (q & 15);
+    double mine = 0.0;  // S[q][q] if r == (q & 15)
 #pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
-          double x = v[0][0];
+    for (int ii = 0; ii < 4; ++ii)
+      if (ii == (q >> 4)) mine = sel4(v[ii], kk);
+    // only the 16 owner lanes (one half-warp) execute this: half-warp mask
+    const double d = __shfl_sync(0xFFFFu << (lane & 16), mine, src);
+    double rs;
+    if (factor) {
+      rs = rsqrt(d);
+      if (!(d > 0.0) && r == (q & 15)) atomicMin(&s_bad, q);
+    } else {
+      rs = 1.0 / d;
+      if ((!(d != 0.0) || !isfinite(d)) && r == (q & 15)) atomicMin(&s_bad, q);
+    }
+    double *col = lb + (q % 3) * SERINV_TILE;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q == kk) x = v[ii][q];
-          buf[ty + 16 * ii] = x;
-        }
-      }
-      __syncthreads();
-      const double d = buf[j];
-      const double dinv = 1.0 / d;
-      if (tid == 0) dv[j] = d;
+    for (int ii = 0; ii < 4; ++ii) {
+      const int i = r + 16 * ii;
+      double x = sel4(v[ii], kk);
+      if (factor)
+        x = (i > q) ? x * rs : (i == q ? d * rs : 0.0);
+      else
+        x = (i >= q) ? x : 0.0;
+      set4(v[ii], kk, x);
+      col[i] = x;
+    }
+    if (r == (q & 15)) {
+      rsv[q] = rs;
+      dv[q] = d;
+    }
+  };
+  if (c == 0) publish_col(0);
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    const double *lj = lb + (j % 3) * SERINV_TILE;
+    // (a) Cholesky: S[i][k] -= L[i][j] L[k][j], j < k <= i
+    if (factor) {
+      double lk[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) lk[kk] = lj[c + 16 * kk];
 #pragma unroll
       for (int ii = 0; ii < 4; ++ii) {
-        const int i = ty + 16 * ii;
-        const double li = buf[i] * dinv;
+        const int i = r + 16 * ii;
+        const double li = lj[i];
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const int k = tx + 16 * kk;
-          if (k > j && k <= i) v[ii][kk] = fma(-li, buf[k], v[ii][kk]);
+          const int k = c + 16 * kk;
+          if (k > j && k <= i) v[ii][kk] = fma(-li, lk[kk], v[ii][kk]);
         }
       }
     }
-    __syncthreads();
-    // scale: L[i][k] = v / sqrt(d_k) (i > k), L[k][k] = sqrt(d_k); zero upper
+    // (b) inverse: acc[i][c'] += L[i][j-1] W[j-1][c'], i > j-1, c' <= j-1
+    if (j > 0) {
+      const double *lp = lb + ((j - 1) % 3) * SERINV_TILE;
+      const double *wp = wb + ((j - 1) & 1) * SERINV_TILE;
+      double wk[4];
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      const int k = tx + 16 * kk;
-      const double dk = k < m ? dv[k] : 1.0;
-      const double sk = sqrt(dk);
-      const double rs = 1.0 / sk;
+      for (int kk = 0; kk < 4; ++kk) wk[kk] = wp[c + 16 * kk];
 #pragma unroll
       for (int ii = 0; ii < 4; ++ii) {
-        const int i = ty + 16 * ii;
-        double x = (i > k) ? v[ii][kk] * rs : (i == k ? sk : 0.0);
-        if (i >= m || k >= m) x = 0.0;
-        v[ii][kk] = x;
-        St[i * LDT + k] = x;
+        const int i = r + 16 * ii;
+        const double li = lp[i];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int k = c + 16 * kk;
+          if (i > j - 1 && k <= j - 1) w[ii][kk] = fma(li, wk[kk], w[ii][kk]);
+        }
       }
     }
-    if (tid < m) {
-      double d = dv[tid];
-      lg[tid] = 0.5 * log(d);
+    // (c) owners of column j+1 publish the next L column
+    if (j + 1 < m && c == ((j + 1) & 15)) publish_col(j + 1);
+    // (d) owners of row j finalise W row j = (e_j - acc[j][:]) / L_jj and publish it
+    if (r == (j & 15)) {
+      const double rj = rsv[j];
+      const int ii0 = j >> 4;
+      double *wr = wb + (j & 1) * SERINV_TILE;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = c + 16 * kk;
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == ii0) a = w[q][kk];
+        const double x = (k <= j) ? (((k == j) ? 1.0 : 0.0) - a) * rj : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == ii0) w[q][kk] = x;
+        wr[k] = x;
+      }
     }
     __syncthreads();
-    if (tid == 0) {
-      int bad = -1;
-      for (int j = 0; j < m; ++j)
-        if (!(dv[j] > 0.0)) {
-          bad = j;
-          break;
-        }
-      if (bad >= 0) record_info(p.info, T.aux1 + bad + 1);
-      if (T.aux0 >= 0) {
-        double s = 0.0;
-        for (int j = 0; j < m; ++j) s += lg[j];
-        *lptr(p, T.r) = s;
-      }
+  }
+  phase_mark(p, tsk, 1);
+  if (tid == 0 && s_bad < (1 << 30)) record_info(p.info, T.aux1 + s_bad + 1);
+  if (factor) {
+    // log det partial: sum_j 0.5 log d_j in a fixed order (tree over 64 values)
+    double *lg = wb;  // reuse
+    if (tid < 64) lg[tid] = (tid < m) ? 0.5 * log(dv[tid]) : 0.0;
+    __syncthreads();
+    for (int h = 32; h > 0; h >>= 1) {
+      if (tid < h) lg[tid] += lg[tid + h];
+      __syncthreads();
     }
-    // store L (full tile, zeros above the diagonal)
+    if (tid == 0 && T.aux0 >= 0) *lptr(p, T.r) = lg[0];
+    // store L (zeros above the diagonal)
     double *o = lptr(p, T.out);
-    for (int idx = tid; idx < m * m; idx += NT) {
-      int r = idx / m, c = idx - r * m;
-      o[(int64_t)r * T.out.ld + c] = St[r * LDT + c];
-    }
-  } else {
-    // TRTRI only: v holds L (lower); zero the strict upper part
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const int i = ty + 16 * ii, k = tx + 16 * kk;
-        if (k > i || i >= m || k >= m) {
-          v[ii][kk] = 0.0;
-          St[i * LDT + k] = 0.0;
-        }
+        const int i = r + 16 * ii, k = c + 16 * kk;
+        if (i < m && k < m) o[(int64_t)i * T.out.ld + k] = (k <= i) ? v[ii][kk] : 0.0;
       }
-    __syncthreads();
-    if (tid == 0) {
-      for (int j = 0; j < m; ++j) {
-        double d = St[j * LDT + j];
-        if (!(d != 0.0) || !isfinite(d)) {
-          record_info(p.info, T.aux1 + j + 1);
-          break;
-        }
-      }
-    }
   }
+  phase_mark(p, tsk, 2);
+  const Loc &wl = factor ? T.out2 : T.out;
   if (!factor || (T.flags & TF_W_OUT)) {
-    // W = L^{-1}, row by row: W[s][c] = (delta_sc - acc[s][c]) / L[s][s];
-    // acc[i][c] += L[i][s] W[s][c] for i > s.  acc kept in w[][] (registers).
-    double w[4][4];
-#pragma unroll
-    for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) w[ii][kk] = 0.0;
-    for (int s = 0; s < m; ++s) {
-      double *buf = cb + (s & 1) * SERINV_TILE;
-      const double lss = St[s * LDT + s];
-      if (ty == (s & 15)) {
-        const int ii = s >> 4;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int c = tx + 16 * kk;
-          double a = w[0][kk];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q == ii) a = w[q][kk];
-          double val = (c <= s) ? (((c == s) ? 1.0 : 0.0) - a) / lss : 0.0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q == ii) w[q][kk] = val;
-          buf[c] = val;
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int ii = 0; ii < 4; ++ii) {
-        const int i = ty + 16 * ii;
-        if (i > s && i < m) {
-          const double lis = St[i * LDT + s];
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const int c = tx + 16 * kk;
-            if (c <= s) w[ii][kk] = fma(lis, buf[c], w[ii][kk]);
-          }
-        }
-      }
-    }
-    const Loc &wl = factor ? T.out2 : T.out;
     double *wo = lptr(p, wl);
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const int i = ty + 16 * ii, c = tx + 16 * kk;
-        if (i < m && c < m) wo[(int64_t)i * wl.ld + c] = (c <= i) ? w[ii][kk] : 0.0;
+        const int i = r + 16 * ii, k = c + 16 * kk;
+        if (i < m && k < m) wo[(int64_t)i * wl.ld + k] = (k <= i) ? w[ii][kk] : 0.0;
       }
+  }
+  phase_mark(p, tsk, 3);
+  if (factor && (T.flags & TF_TRSM2)) {
+    // next link of the chain: L2 = (beta3 * C3 - sum_{s >= nseg1} ...) * W^T  (m3 x m);
+    // W stays in registers while the update runs through the staging buffers
+    double acc[2][4][2];
+    __syncthreads();
+    gemm_mainloop(p, T.seg0 + T.nseg1, T.nseg - T.nseg1, T.m3, m, smem, acc);
+    apply_c0(p, (T.nseg > T.nseg1) ? T.alpha : 0.0, T.beta3, T.out3, T.m3, m, acc);
+    double *S2 = smem;
+    double *Wt = smem + SERINV_TILE * LDT;
+    acc_to_smem(S2, acc);
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int i = r + 16 * ii, k = c + 16 * kk;
+        Wt[i * LDT + k] = (k <= i && i < m && k < m) ? w[ii][kk] : 0.0;
+      }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    mma_steps(S2, LDT, 1, Wt, LDT, 1, acc, (m + 3) / 4);
+    store_tile(p, T.out3, T.m3, m, acc);
+    phase_mark(p, tsk, 4);
+    if (T.flags & TF_ZERO_MIRROR) {  // strict-upper tile (c, c+1) of the diagonal block
+      double *z = lptr(p, T.out) + SERINV_TILE;
+      for (int idx = tid; idx < m * T.m3; idx += NT) {
+        int rr = idx / T.m3, cc = idx - rr * T.m3;
+        z[(int64_t)rr * T.out.ld + cc] = 0.0;
+      }
+    }
   }
 }
 
@@ -518,29 +601,80 @@ __device__ void run_logdet(const Params &p, const Task &T, double *smem) {
 extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev::Params p) {
   using namespace dev;
   extern __shared__ __align__(16) double smem[];
-  __shared__ int s_task;
+  __shared__ int s_task, s_q;
+  unsigned long long t_claim = 0, t_start = 0;
+  // ---- roles: the first nq-1 CTAs to arrive serve the critical queues and get
+  // their SM to themselves (co-resident siblings on those SMs exit); the rest
+  // serve the bulk queue.  All CTAs are co-resident, so the barrier is safe.
+  if (threadIdx.x == 0) {
+    int32_t *role = p.qclaim + p.nq;
+    const int rank = atomicAdd(role, 1);
+    const int me = (int)smid();
+    role[2 + rank] = me;
+    __threadfence();
+    atomicAdd(role + 1, 1);
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire(role + 1) < (int)gridDim.x) {
+      __nanosleep(64);
+      if (globaltimer() - t0 > 20000000000ULL) {  // watchdog (grid not co-resident)
+        atomicExch(p.info, -1);
+        break;
+      }
+    }
+    int q = 0;
+    const int ncrit = p.nq - 1;
+    if (rank < ncrit) {
+      q = 1 + rank;
+    } else {
+      for (int r = 0; r < ncrit && r < (int)gridDim.x; ++r)
+        if (ld_acquire(role + 2 + r) == me) q = -1;
+    }
+    s_q = q;
+  }
+  __syncthreads();
+  if (s_q < 0) return;
   for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(p.claim, 1);
+    if (threadIdx.x == 0) {
+      int q = s_q, t = -1;
+      for (;;) {
+        const int idx = atomicAdd(p.qclaim + q, 1);
+        if (idx < p.qoff[q + 1] - p.qoff[q]) {
+          t = p.qlist[p.qoff[q] + idx];
+          break;
+        }
+        if (q == 0) break;
+        q = 0;  // critical queue drained: help with the bulk queue
+      }
+      s_q = q;
+      s_task = t;
+    }
     __syncthreads();
     const int t = s_task;
-    if (t >= p.ntasks) break;
+    if (t < 0) break;
     const Task T = p.tasks[t];
+    if (p.trace && threadIdx.x == 0) t_claim = globaltimer();
     if (threadIdx.x == 0) {
       for (int w = 0; w < T.nwait; ++w) {
         const Wait W = p.waits[T.wait0 + w];
         if (ld_acquire(p.ctr + W.ctr) >= W.target) continue;
         int ns = 32;
+        const unsigned long long t0 = globaltimer();
         while (ld_acquire(p.ctr + W.ctr) < W.target) {
           __nanosleep(ns);
           ns = min(ns * 2, 256);
+          if (globaltimer() - t0 > 20000000000ULL) {  // 20 s watchdog: never hang the GPU
+            atomicExch(p.info, -1);
+            break;
+          }
         }
       }
     }
+    if (p.trace && threadIdx.x == 0) t_start = globaltimer();
     __syncthreads();
     switch (T.type) {
       case TK_GEMM: run_gemm(p, T, smem); break;
-      case TK_POTRF: run_potrf_trtri(p, T, smem, true); break;
-      case TK_TRTRI: run_potrf_trtri(p, T, smem, false); break;
+      case TK_POTRF: run_potrf_trtri(p, T, smem, true, t); break;
+      case TK_TRTRI: run_potrf_trtri(p, T, smem, false, t); break;
       case TK_REDUCE: run_reduce(p, T); break;
       case TK_COPY: run_copy(p, T); break;
       case TK_LOGDET: run_logdet(p, T, smem); break;
@@ -551,6 +685,14 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
     if (threadIdx.x == 0) {
       __threadfence();
       for (int s = 0; s < T.nsig; ++s) atomicAdd(p.ctr + p.sigs[T.sig0 + s], 1);
+      if (p.trace) {
+        unsigned long long *rec = p.trace + 4 * (size_t)t;
+        rec[0] = t_claim;
+        rec[1] = t_start;
+        rec[2] = globaltimer();
+        rec[3] = (unsigned long long)(unsigned)T.type | ((unsigned long long)smid() << 16) |
+                 ((unsigned long long)(unsigned)T.m << 32) | ((unsigned long long)(unsigned)T.n << 48);
+      }
     }
   }
 }

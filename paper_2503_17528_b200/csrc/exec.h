@@ -11,11 +11,15 @@ struct Params {
   const Seg *segs;
   const Wait *waits;
   const int32_t *sigs;
-  int32_t *ctr;    // dependency counters (zeroed before each launch)
-  int32_t *claim;  // next-task claim counter (zeroed before each launch)
+  int32_t *ctr;          // dependency counters (zeroed before each launch)
+  int32_t *qclaim;       // [nq] claim counters, then [2 + grid] role table (zeroed before each launch)
+  const int32_t *qlist;  // task indices per queue
+  const int32_t *qoff;   // [nq + 1]
+  int nq;                // queue 0 = bulk, 1..nq-1 = critical chains
   int ntasks;
   double *bufs[BUF_COUNT];
   int *info;
+  unsigned long long *trace;  // optional: 4 x u64 per task {claim, start, end, meta}
 };
 }  // namespace dev
 int exec_smem_bytes();

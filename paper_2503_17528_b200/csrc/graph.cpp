@@ -51,6 +51,7 @@ struct RawTask {
   std::vector<int32_t> sigs;   // counters signalled (own counter first)
   double cost = 0.0;           // ns (scheduler model)
   double flops = 0.0;
+  int queue = 0;               // claim queue (0 = bulk)
 };
 
 double gemm_flops(int m, int n, const std::vector<Seg> &segs) {
@@ -114,7 +115,9 @@ struct Ctx {
   int emit(RawTask &&rt) {
     if (rt.t.type == TK_GEMM)
       rt.flops = gemm_flops(rt.t.m, rt.t.n, rt.segs) + ((rt.t.flags & TF_POST) ? 2.0 * rt.t.m * rt.t.n * rt.t.n : 0.0);
-    if (rt.t.type == TK_POTRF) rt.flops = gemm_flops(rt.t.m, rt.t.n, rt.segs) + 2.0 * rt.t.m * rt.t.m * rt.t.m / 3.0;
+    if (rt.t.type == TK_POTRF)
+      rt.flops = 2.0 * rt.t.m * rt.t.n * [&] { double k = 0; for (auto &sg : rt.segs) k += sg.k; return k; }() +
+                 2.0 * rt.t.m * rt.t.m * rt.t.m / 3.0 + ((rt.t.flags & TF_TRSM2) ? 2.0 * rt.t.m3 * rt.t.m * rt.t.m : 0.0);
     if (rt.t.type == TK_TRTRI) rt.flops = rt.t.m * (double)rt.t.m * rt.t.m / 3.0;
     rt.cost = task_cost(rt);
     std::sort(rt.waits.begin(), rt.waits.end());
@@ -349,7 +352,9 @@ struct Builder {
     cx.potrf_ctrs.push_back(fd);
     for (int c = 0; c < nt; ++c) {
       int w = tdim(P.size[X], c);
-      {  // POTRF of the diagonal tile with the last update fused in
+      std::vector<RT> rts = column_rows(X, c);
+      size_t first_trsm = 0;
+      {  // POTRF of the diagonal tile with the last update fused in (+ the sub-diagonal TRSM)
         TileState &st = tstate[tkey(X, X, c, c)];
         flush(X, c, X, c, d, st, 1);
         RawTask rt;
@@ -360,6 +365,7 @@ struct Builder {
         rt.t.alpha = -1.0;
         rt.t.beta = 1.0;
         if (!st.pending.empty()) add_update_segs(rt, X, c, X, c, st.pending);
+        rt.t.nseg1 = (int32_t)rt.segs.size();
         if (st.last >= 0) rt.waits.push_back(cx.ctr_of(st.last));
         for (int32_t iw : input_waits) rt.waits.push_back(iw);
         rt.t.flags = TF_W_OUT;
@@ -368,15 +374,37 @@ struct Builder {
         rt.t.r = wsloc(cx.slot_region + P.slot[X] + c, 0);
         rt.t.aux1 = (int32_t)(P.rowbase[X] + (int64_t)c * TILE);
         rt.sigs.push_back(fd);
+        TileState *st0 = nullptr;
+        if (cx.opt.fuse_trsm && !rts.empty()) {
+          const RT &r0 = rts[0];
+          const BlkRef &tb0 = (r0.Y == X) ? d : B(r0.Y, X);
+          st0 = &tstate[tkey(r0.Y, X, r0.q, c)];
+          flush(r0.Y, r0.q, X, c, tb0, *st0, 1);
+          if (!st0->pending.empty()) add_update_segs(rt, r0.Y, r0.q, X, c, st0->pending);
+          if (st0->last >= 0) rt.waits.push_back(cx.ctr_of(st0->last));
+          rt.t.flags |= TF_TRSM2;
+          rt.t.out3 = r0.loc;
+          rt.t.m3 = r0.h;
+          rt.t.beta3 = (!st0->written && tb0.zero_init) ? 0.0 : 1.0;
+          if (r0.Y == X) rt.t.flags |= TF_ZERO_MIRROR;  // zero tile (c, c+1) = out + TILE columns
+          first_trsm = 1;
+        }
+        rt.queue = cx.opt.critical_queues ? P.queue : 0;
         int id = cx.emit(std::move(rt));
         st.pending.clear();
         st.last = id;
         st.written = true;
         Lprod[key4(X, c, X, c)] = id;
         wdiag_task[(int64_t)X * 4096 + c] = id;
+        if (st0) {
+          st0->pending.clear();
+          st0->last = id;
+          st0->written = true;
+          Lprod[key4(rts[0].Y, rts[0].q, X, c)] = id;
+        }
       }
-      std::vector<RT> rts = column_rows(X, c);
-      for (auto &r : rts) {  // TRSM = (A - last update) W(c,c)^T
+      for (size_t ri = first_trsm; ri < rts.size(); ++ri) {  // TRSM = (A - last update) W(c,c)^T
+        const RT &r = rts[ri];
         const BlkRef &tb = (r.Y == X) ? d : B(r.Y, X);
         TileState &st = tstate[tkey(r.Y, X, r.q, c)];
         flush(r.Y, r.q, X, c, tb, st, 1);
@@ -716,6 +744,16 @@ Graph Ctx::finalize() {
     g.tasks.push_back(task);
     g.flops += rt.flops;
   }
+  int nq = 1;
+  for (int t : order) nq = std::max(nq, tasks[t].queue + 1);
+  g.qoff.assign(nq + 1, 0);
+  for (int t : order) g.qoff[tasks[t].queue + 1]++;
+  for (int q = 0; q < nq; ++q) g.qoff[q + 1] += g.qoff[q];
+  g.qlist.assign(N, 0);
+  {
+    std::vector<int32_t> fill(g.qoff.begin(), g.qoff.end() - 1);
+    for (int i = 0; i < N; ++i) g.qlist[fill[tasks[order[i]].queue]++] = i;
+  }
   g.nctr = nctr;
   g.grid = opt.grid;
   g.ws_doubles = ws_top;
@@ -837,6 +875,7 @@ Graph build_seq_ctx(Ctx &cx, int kind, int64_t n, int64_t b, int64_t a) {
       P, (int)n, b, a, [&](int i) { return famD(b).at(i); }, [&](int i) { return famL(b).at(i); },
       [&](int i) { return famA(b, a).at(i); }, Loc{BUF_TIP, (int32_t)a, 0}, false, (int)n, true,
       [&](int i) { return (int64_t)i * b; }, n * b);
+  P.queue = 1;
   Builder bld(cx, P);
   bld.allocate(inv);
   int nn = (int)P.size.size();
@@ -864,6 +903,7 @@ struct PartState {
   Fam Bbuf{};                 // fill-in chain (middle partitions)
   std::vector<int32_t> done;  // counters: everything the factor phase wrote
   int nelim = 0;
+  int queue = 1;              // critical claim queue of this partition's chain
 };
 
 // PPOBTAF for one partition (Alg. 3 line 3 / line 5): factor the interior and
@@ -882,6 +922,7 @@ void ppobtaf_part(Ctx &cx, PartState &ps, int64_t b, int64_t a) {
     ps.Bbuf = Fam{BUF_WS, cx.alloc((cnt - 1) * b * b), b * b, (int32_t)b};
     middle_problem(ps.prob, ps.ls, cnt, b, a, ps.U, ps.Bbuf, ps.s);
   }
+  ps.prob.queue = ps.queue;
   ps.bld.reset(new Builder(cx, ps.prob));
   Builder &B = *ps.bld;
   B.allocate(true);
@@ -991,6 +1032,7 @@ void reduced_from_records(Ctx &cx, int P, int64_t n, int64_t b, int64_t a, int32
   chain_problem(
       R.P, nr, b, a, [&](int i) { return R.D.at(i); }, [&](int i) { return R.Lo.at(i); },
       [&](int i) { return R.Ar.at(i); }, R.tip, false, nr, true, rb, n * b);
+  R.P.queue = 1;
   R.B.reset(new Builder(cx, R.P));
   R.B->input_waits = ready;
   R.B->allocate(true);
@@ -1113,6 +1155,7 @@ Graph build_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, const Buil
     parts[p].s = starts[p];
     parts[p].e = starts[p + 1];
     parts[p].ls = starts[p];
+    parts[p].queue = p + 1;
     ppobtaf_part(cx, parts[p], b, a);
   }
   int32_t packed = cx.new_ctr();

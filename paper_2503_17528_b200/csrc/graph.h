@@ -37,6 +37,9 @@ struct Graph {
   int64_t ws_doubles = 0;    // workspace doubles used (excluding counters)
   int64_t nslots = 0;        // logdet slots
   double sim_ns = 0.0;       // simulated makespan of the schedule (ns)
+  // claim queues: queue 0 = bulk, queues 1..nq-1 = critical chains (one CTA each,
+  // alone on its SM).  qlist holds task indices, queue q = qlist[qoff[q] .. qoff[q+1]).
+  std::vector<int32_t> qlist, qoff;
   std::string error;         // non-empty if building failed
 };
 
@@ -63,12 +66,15 @@ struct Problem {
   std::vector<Loc> Lam;           // Lambda_X = W_X^T W_X
   std::map<std::pair<int, int>, Loc> Lchk;     // Lchk(Z,X) = L_{Z,X} W_X
   std::vector<int64_t> slot;      // logdet slot base per node (-1: none)
+  int queue = 0;                  // claim queue of this problem's POTRF chain (0 = bulk)
 };
 
 struct BuildOptions {
   int grid = 296;          // persistent CTAs (for the simulated schedule)
   int update_group = 4;    // tile columns per chained update task (regular targets)
   bool schedule = true;
+  bool critical_queues = true;  // dedicated CTAs for the POTRF chains
+  bool fuse_trsm = true;        // fuse the sub-diagonal TRSM into each POTRF task
 };
 
 // Sequential problems (whole matrix).  kind: 0 = pobtaf, 1 = pobtasi, 2 = selinv.

@@ -27,12 +27,16 @@ namespace {
 
 struct DevGraph {
   Graph g;                 // host copy (stats); task arrays freed after upload
-  void *blob = nullptr;    // tasks | segs | waits | sigs
-  int32_t *ctr = nullptr;  // nctr + 1 (claim counter last)
+  void *blob = nullptr;    // tasks | segs | waits | sigs | qlist | qoff
+  int32_t *ctr = nullptr;  // nctr counters, nq queue claims, 2 + grid role table
   const Task *d_tasks = nullptr;
   const Seg *d_segs = nullptr;
   const Wait *d_waits = nullptr;
   const int32_t *d_sigs = nullptr;
+  const int32_t *d_qlist = nullptr;
+  const int32_t *d_qoff = nullptr;
+  int nq = 1;
+  int64_t nctr_alloc = 0;
   int64_t ntasks = 0;
   ~DevGraph() {
     if (blob) cudaFree(blob);
@@ -51,6 +55,8 @@ struct serinv_ctx {
   int smem = 0;
   int last_launches = 0;
   double *dummy = nullptr;  // logdet sink when the caller passes NULL
+  unsigned long long *trace = nullptr;  // optional per-task trace buffer (device)
+  size_t trace_cap = 0;                 // records
   std::map<GKey, std::unique_ptr<DevGraph>> cache;
   std::mutex mu;
 };
@@ -59,12 +65,13 @@ namespace {
 
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
-int upload(DevGraph &dg) {
+int upload(DevGraph &dg, int grid) {
   Graph &g = dg.g;
   size_t bt = g.tasks.size() * sizeof(Task), bs = g.segs.size() * sizeof(Seg);
   size_t bw = g.waits.size() * sizeof(Wait), bg = g.sigs.size() * sizeof(int32_t);
+  size_t bq = g.qlist.size() * sizeof(int32_t), bo = g.qoff.size() * sizeof(int32_t);
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-  size_t total = up(bt) + up(bs) + up(bw) + up(bg) + 256;
+  size_t total = up(bt) + up(bs) + up(bw) + up(bg) + up(bq) + up(bo) + 256;
   if (cudaMalloc(&dg.blob, total) != cudaSuccess) return SERINV_ERR_CUDA;
   char *base = (char *)dg.blob;
   size_t o = 0;
@@ -78,7 +85,11 @@ int upload(DevGraph &dg) {
   dg.d_segs = (const Seg *)put(g.segs.data(), bs);
   dg.d_waits = (const Wait *)put(g.waits.data(), bw);
   dg.d_sigs = (const int32_t *)put(g.sigs.data(), bg);
-  if (cudaMalloc(&dg.ctr, (size_t)(g.nctr + 1) * sizeof(int32_t)) != cudaSuccess) return SERINV_ERR_CUDA;
+  dg.d_qlist = (const int32_t *)put(g.qlist.data(), bq);
+  dg.d_qoff = (const int32_t *)put(g.qoff.data(), bo);
+  dg.nq = (int)g.qoff.size() - 1;
+  dg.nctr_alloc = (int64_t)g.nctr + dg.nq + 2 + grid;
+  if (cudaMalloc(&dg.ctr, (size_t)dg.nctr_alloc * sizeof(int32_t)) != cudaSuccess) return SERINV_ERR_CUDA;
   dg.ntasks = (int64_t)g.tasks.size();
   if (cudaGetLastError() != cudaSuccess) return SERINV_ERR_CUDA;
   // keep stats, drop the big host arrays
@@ -86,6 +97,7 @@ int upload(DevGraph &dg) {
   std::vector<Seg>().swap(g.segs);
   std::vector<Wait>().swap(g.waits);
   std::vector<int32_t>().swap(g.sigs);
+  std::vector<int32_t>().swap(g.qlist);
   return SERINV_OK;
 }
 
@@ -119,7 +131,7 @@ int get_graph(serinv_handle_t h, const GKey &key, DevGraph **out) {
     fprintf(stderr, "serinv: graph build failed: %s\n", dg->g.error.c_str());
     return SERINV_ERR_SHAPE;
   }
-  int rc = upload(*dg);
+  int rc = upload(*dg, h->grid);
   if (rc) return rc;
   *out = dg.get();
   h->cache[key] = std::move(dg);
@@ -127,7 +139,7 @@ int get_graph(serinv_handle_t h, const GKey &key, DevGraph **out) {
 }
 
 int launch(serinv_handle_t h, DevGraph &dg, double *bufs[BUF_COUNT], int *d_info, cudaStream_t st) {
-  if (cudaMemsetAsync(dg.ctr, 0, (size_t)(dg.g.nctr + 1) * sizeof(int32_t), st) != cudaSuccess)
+  if (cudaMemsetAsync(dg.ctr, 0, (size_t)dg.nctr_alloc * sizeof(int32_t), st) != cudaSuccess)
     return SERINV_ERR_CUDA;
   if (cudaMemsetAsync(d_info, 0, sizeof(int), st) != cudaSuccess) return SERINV_ERR_CUDA;
   dev::Params p;
@@ -136,10 +148,14 @@ int launch(serinv_handle_t h, DevGraph &dg, double *bufs[BUF_COUNT], int *d_info
   p.waits = dg.d_waits;
   p.sigs = dg.d_sigs;
   p.ctr = dg.ctr;
-  p.claim = dg.ctr + dg.g.nctr;
+  p.qclaim = dg.ctr + dg.g.nctr;
+  p.qlist = dg.d_qlist;
+  p.qoff = dg.d_qoff;
+  p.nq = dg.nq;
   p.ntasks = (int)dg.ntasks;
   for (int i = 0; i < BUF_COUNT; ++i) p.bufs[i] = bufs[i];
   p.info = d_info;
+  p.trace = (h->trace && (size_t)dg.ntasks <= h->trace_cap) ? h->trace : nullptr;
   serinv_exec_kernel<<<h->grid, 256, h->smem, st>>>(p);
   h->last_launches = 1;
   return cudaGetLastError() == cudaSuccess ? SERINV_OK : SERINV_ERR_CUDA;
@@ -383,6 +399,14 @@ int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_
   out->flops = dg->g.flops;
   out->grid = h->grid;
   out->tile = SERINV_TILE;
+  return SERINV_OK;
+}
+
+int serinv_set_trace(serinv_handle_t h, void *d_trace, size_t bytes) {
+  if (!h) return SERINV_ERR_HANDLE;
+  if (d_trace && ((uintptr_t)d_trace & 7)) return SERINV_ERR_ALIGN;
+  h->trace = (unsigned long long *)d_trace;
+  h->trace_cap = d_trace ? bytes / 96 : 0;  // 4 + 8 u64 per task
   return SERINV_OK;
 }
 

@@ -41,6 +41,7 @@ enum TaskFlags : int16_t {
   TF_ZERO_MIRROR = 8, // store zeros at out2 (transposed footprint): strict-upper tiles of L
   TF_TRANS_C0 = 16,   // TK_COPY: out = alpha * C0^T
   TF_W_OUT = 32,      // TK_POTRF: store W = L^{-1} at out2
+  TF_TRSM2 = 64,      // TK_POTRF: fused TRSM of the sub-diagonal tile (out3)
 };
 
 // Buffer ids (kernel argument `bufs[]`, offsets in doubles).
@@ -83,8 +84,13 @@ struct Task {
   double alpha, beta;
   int32_t aux0, aux1;   // POTRF: aux0 = logdet slot (-1 none), aux1 = global row base (info)
   int64_t aux2;         // REDUCE: stride between partials (doubles); count in aux0
+  // TK_POTRF with TF_TRSM2: also L2 = (beta3 * C3 - sum_{s >= nseg1} ...) W^T for the
+  // sub-diagonal tile at out3 (m3 rows), i.e. the next link of the critical chain.
+  Loc out3;
+  double beta3;
+  int32_t m3, nseg1;
 };
 
 static_assert(sizeof(Loc) == 16, "Loc layout");
 static_assert(sizeof(Seg) == 40, "Seg layout");
-static_assert(sizeof(Task) == 128, "Task layout");
+static_assert(sizeof(Task) == 160, "Task layout");

@@ -1,12 +1,117 @@
-"""Distributed PPOBTAF / PPOBTASI (one process per GPU; Alg. 3-6).
+"""Distributed PPOBTAF / PPOBTASI: one process per GPU (Alg. 3-6, Sec. 3.3).
 
-Filled in by the distributed milestone; see include/serinv.h."""
+Rank p owns the global blocks [s, e) of `serinv_plan` and passes its LOCAL
+blocks (diag/arrow [count], lower [count] -- the last rank [count-1] -- and the
+replicated tip).  One step:
+
+    serinv_ppobtaf   local elimination (no communication) + pack of this rank's
+                     exchange record (boundary blocks, couplings, U_p, log det
+                     partial) into the send buffer
+    all-gather       of the P records (NCCL through torch.distributed; the only
+                     inter-GPU transfer: <= 4b^2 + 2ab + a^2 doubles per rank)
+    serinv_ppobtasi  every rank assembles A_r (2P-1 blocks) in rank order,
+                     solves it redundantly (bit-identical on all ranks), scatters
+                     its true-inverse boundary blocks and runs its backward pass
+
+Argument marshalling + the collective only; all arithmetic is in libserinv.
+"""
 from __future__ import annotations
 
+import ctypes
 
-def ppobtaf(*args, **kwargs):  # pragma: no cover - replaced by the distributed milestone
-    raise NotImplementedError("ppobtaf: distributed path not built yet")
+import numpy as np
+
+from . import _lib
+from ._lib import BTA, Part
+
+KEYS = ("diag", "lower", "arrow", "tip")
 
 
-def ppobtasi(*args, **kwargs):  # pragma: no cover
-    raise NotImplementedError("ppobtasi: distributed path not built yet")
+def local_blocks(A, s: int, e: int, last: bool):
+    """Slice rank-local blocks out of global host arrays (numpy), C-ABI layout."""
+    b = A["diag"].shape[1]
+    out = {"diag": np.ascontiguousarray(A["diag"][s:e]),
+           "lower": np.ascontiguousarray(A["lower"][s:e - 1] if last else A["lower"][s:e]),
+           "arrow": np.ascontiguousarray(A["arrow"][s:e]),
+           "tip": np.ascontiguousarray(A["tip"])}
+    if out["lower"].shape[0] == 0:
+        out["lower"] = np.zeros((1, b, b))
+    return out
+
+
+def exchange(send, recv, group=None):
+    """All-gather of the per-rank exchange records (rank order).  Works for NCCL
+    (CUDA tensors) and gloo (CPU tensors)."""
+    import torch.distributed as dist
+    dist.all_gather_into_tensor(recv, send, group=group)
+
+
+class DistContext:
+    """Per-rank state of the distributed routines (buffers persist between
+    ppobtaf and ppobtasi: the workspace keeps the fill-in factor blocks B_i)."""
+
+    def __init__(self, handle, P: int, rank: int, n_global: int, start: int, count: int, b: int, a: int,
+                 device: int = 0, group=None):
+        import torch
+        L = _lib.lib()
+        self.h = handle
+        self.part = Part(P, rank, n_global, start, count)
+        self.b, self.a = b, a
+        self.group = group
+        nb = ctypes.c_size_t(0)
+        rc = L.serinv_ppobtaf_ws(ctypes.byref(self.part), b, a, ctypes.byref(nb))
+        if rc:
+            raise RuntimeError(f"serinv_ppobtaf_ws failed: {rc}")
+        dev = f"cuda:{device}"
+        self.ws = torch.empty(max(nb.value, 256), dtype=torch.uint8, device=dev)
+        xb = ctypes.c_size_t(0)
+        L.serinv_exchange_bytes(b, a, ctypes.byref(xb))
+        self.rec_doubles = xb.value // 8
+        self.send = torch.zeros(self.rec_doubles, dtype=torch.float64, device=dev)
+        self.recv = torch.zeros(P * self.rec_doubles, dtype=torch.float64, device=dev)
+        self.info = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.logdet = torch.zeros(1, dtype=torch.float64, device=dev)
+
+
+def _bta_local(D, b, a, count):
+    def ptr(t):
+        return t.data_ptr() if (t is not None and t.numel() > 0) else None
+    return BTA(count, b, a, ptr(D["diag"]), ptr(D["lower"]), ptr(D["arrow"]) if a else None,
+               ptr(D["tip"]) if a else None)
+
+
+def _stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ppobtaf(ctx: DistContext, D):
+    """PARTIAL_/PERMUTED_POBTAF on the local blocks + pack of the exchange record."""
+    A = _bta_local(D, ctx.b, ctx.a, ctx.part.count)
+    rc = _lib.lib().serinv_ppobtaf(ctx.h._h, ctypes.byref(ctx.part), ctypes.byref(A), ctx.ws.data_ptr(),
+                                   ctx.ws.numel(), ctx.send.data_ptr(), ctx.info.data_ptr(), _stream())
+    if rc:
+        raise RuntimeError(f"serinv_ppobtaf failed: {rc}")
+
+
+def ppobtasi(ctx: DistContext, D):
+    """POBTARSSI (redundant) + PARTIAL_/PERMUTED_POBTASI on the local blocks."""
+    A = _bta_local(D, ctx.b, ctx.a, ctx.part.count)
+    rc = _lib.lib().serinv_ppobtasi(ctx.h._h, ctypes.byref(ctx.part), ctypes.byref(A), ctx.ws.data_ptr(),
+                                    ctx.ws.numel(), ctx.recv.data_ptr(), ctx.info.data_ptr(),
+                                    ctx.logdet.data_ptr(), _stream())
+    if rc:
+        raise RuntimeError(f"serinv_ppobtasi failed: {rc}")
+
+
+def pselinv_step(ctx: DistContext, D, check: bool = True):
+    """One distributed selected inversion: returns the global log det (check=True)."""
+    ppobtaf(ctx, D)
+    exchange(ctx.send, ctx.recv, ctx.group)
+    ppobtasi(ctx, D)
+    if check:
+        info = int(ctx.info.item())
+        if info:
+            raise ArithmeticError(f"not positive definite (global row {info})")
+        return float(ctx.logdet.item())
+    return None

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <vector>
 
 #include "../paper_2503_17528_b200/csrc/graph.h"
@@ -41,12 +42,17 @@ int run(const Graph &g, Ctx &c) {
       }
     }
     const int m = T.m, n = T.n;
+    if (getenv("DAG_DUMP"))
+      fprintf(stderr, "t%zu type %d m %d n %d out(%d,%lld) c0(%d,%lld) nseg %d nseg1 %d alpha %g beta %g flags %d out3(%d,%lld) m3 %d beta3 %g\n", t, T.type, m, n,
+              T.out.buf, (long long)T.out.off, T.c0.buf, (long long)T.c0.off, T.nseg, T.nseg1, T.alpha, T.beta, T.flags,
+              T.out3.buf, (long long)T.out3.off, T.m3, T.beta3);
     auto A_ = [&](int i, int j) -> double & { return acc[i * SERINV_TILE + j]; };
     if (T.type == TK_GEMM || T.type == TK_POTRF) {
+      int ns = (T.type == TK_POTRF) ? T.nseg1 : T.nseg;
       for (int i = 0; i < m; ++i)
         for (int j = 0; j < n; ++j) {
           double s = 0;
-          for (int si = 0; si < T.nseg; ++si) {
+          for (int si = 0; si < ns; ++si) {
             const Seg &S = g.segs[T.seg0 + si];
             for (int k = 0; k < S.k; ++k) s += opget(c, S.A, S.ta, i, k) * opget(c, S.B, S.tb, k, j);
           }
@@ -129,6 +135,34 @@ int run(const Graph &g, Ctx &c) {
         for (int j = 0; j < m; ++j)
           if (!(A_(j, j) != 0.0) || !std::isfinite(A_(j, j)))
             if (!c.info || T.aux1 + j + 1 < c.info) c.info = T.aux1 + j + 1;
+      }
+      if (T.type == TK_POTRF && (T.flags & TF_TRSM2)) {
+        // L2 = (beta3 * C3 + alpha * sum_{s >= nseg1} ...) W^T at out3 (m3 x m)
+        double alpha2 = (T.nseg > T.nseg1) ? T.alpha : 0.0;
+        std::vector<double> S2(T.m3 * m);
+        for (int i = 0; i < T.m3; ++i)
+          for (int j = 0; j < m; ++j) {
+            double s = 0;
+            for (int si = T.nseg1; si < T.nseg; ++si) {
+              const Seg &S = g.segs[T.seg0 + si];
+              for (int k = 0; k < S.k; ++k) s += opget(c, S.A, S.ta, i, k) * opget(c, S.B, S.tb, k, j);
+            }
+            double v = alpha2 * s;
+            if (T.beta3 != 0.0) v += T.beta3 * get(c, T.out3, i, j);
+            S2[i * m + j] = v;
+          }
+        double *o3 = ptr(c, T.out3);
+        for (int i = 0; i < T.m3; ++i)
+          for (int j = 0; j < m; ++j) {
+            double s = 0;
+            for (int k = 0; k < m; ++k) s += S2[i * m + k] * W[j * m + k];
+            o3[(int64_t)i * T.out3.ld + j] = s;
+          }
+        if (T.flags & TF_ZERO_MIRROR) {
+          double *z = ptr(c, T.out) + SERINV_TILE;
+          for (int i = 0; i < m; ++i)
+            for (int j = 0; j < T.m3; ++j) z[(int64_t)i * T.out.ld + j] = 0.0;
+        }
       }
     } else if (T.type == TK_REDUCE) {
       double *o = ptr(c, T.out);
@@ -282,6 +316,35 @@ int dag_run_distributed(int64_t n, int64_t b, int64_t a, int P, double r, double
   }
   *logdet = ld;
   return 0;
+}
+
+// One distributed phase on caller buffers (used by the gloo multi-process test).
+int64_t dag_dist_ws_doubles(int P, int rank, int64_t n, int64_t start, int64_t count, int64_t b, int64_t a) {
+  return distributed_ws_bytes(P, rank, n, start, count, b, a) / 8;
+}
+int64_t dag_exchange_doubles(int64_t b, int64_t a) { return exchange_doubles(b, a); }
+int dag_run_dist_phase(int phase, int P, int rank, int64_t n, int64_t start, int64_t count, int64_t b, int64_t a,
+                       double *diag, double *lower, double *arrow, double *tip, double *ws, double *ext0,
+                       double *ext1, double *logdet, int *info) {
+  BuildOptions opt;
+  opt.grid = 8;
+  Graph g = build_distributed(phase, P, rank, n, start, count, b, a, opt);
+  if (!g.error.empty()) return -2;
+  Ctx c;
+  memset(c.bufs, 0, sizeof(c.bufs));
+  double ld = 0;
+  c.bufs[BUF_DIAG] = diag;
+  c.bufs[BUF_LOWER] = lower;
+  c.bufs[BUF_ARROW] = arrow;
+  c.bufs[BUF_TIP] = tip;
+  c.bufs[BUF_WS] = ws;
+  c.bufs[BUF_EXT0] = ext0;
+  c.bufs[BUF_EXT1] = ext1;
+  c.bufs[BUF_LOGDET] = &ld;
+  int rc = run(g, c);
+  *info = c.info;
+  if (logdet) *logdet = ld;
+  return rc;
 }
 
 int dag_stats_sequential(int kind, int64_t n, int64_t b, int64_t a, int grid, int64_t *ntasks, double *flops,
