@@ -34,7 +34,7 @@ constexpr int OPSZ = SERINV_TILE * LD_MK;  // doubles per operand stage (2304 >=
 constexpr int LDT = SERINV_TILE + 4;     // full-tile stride in smem (68)
 constexpr int SMEM_DOUBLES = STAGES * 2 * OPSZ;  // 13824 doubles = 110592 bytes
 static_assert(KC * LD_KM <= OPSZ, "km layout fits the stage");
-static_assert(2 * SERINV_TILE * LDT + 4 * SERINV_TILE <= SMEM_DOUBLES, "post/potrf smem fits");
+static_assert(3 * SERINV_TILE * LDT + 5 * SERINV_TILE <= SMEM_DOUBLES, "post/potrf smem fits");
 
 __device__ __forceinline__ int ld_acquire(const int32_t *p) {
   int v;
@@ -147,30 +147,50 @@ __device__ __forceinline__ void mma_steps(const double *As, int sAr, int sAk, co
   }
 }
 
-// Main loop: acc = sum_s op(A_s) op(B_s) over segments [s0, s0 + ns) (output m x n).
-__device__ void gemm_mainloop(const Params &p, int s0, int ns, int m, int n, double *smem, double (&acc)[2][4][2]) {
+// Main loop over one or two segment lists sharing ONE cp.async pipeline:
+//   acc  = sum_{s in [s0, s0+ns)}  op(A_s) op(B_s)   (output m  x n)
+//   acc2 = sum_{s in [s0b, s0b+nsb)} op(A_s) op(B_s)  (output mb x n)   [if acc2 != nullptr]
+template <bool DUAL>
+__device__ __forceinline__ void gemm_mainloop2(const Params &p, int s0, int ns, int m, int s0b, int nsb, int mb,
+                                               int n, double *smem, double (&acc)[2][4][2],
+                                               double (&acc2)[2][4][2]) {
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  if (ns == 0) return;
-  const Seg *segs = p.segs + s0;
-  int nchunks = 0;
-  for (int s = 0; s < ns; ++s) nchunks += (segs[s].k + KC - 1) / KC;
-  // load-side cursor
-  int ls = 0, lk = 0;
+  if (DUAL) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc2[i][j][0] = acc2[i][j][1] = 0.0;
+  } else {
+    nsb = 0;
+  }
+  if (ns + nsb == 0) return;
+  const Seg *segsA = p.segs + s0;
+  const Seg *segsB = p.segs + s0b;
+  int nchA = 0, nchB = 0;
+  for (int s = 0; s < ns; ++s) nchA += (segsA[s].k + KC - 1) / KC;
+  for (int s = 0; s < nsb; ++s) nchB += (segsB[s].k + KC - 1) / KC;
+  const int nchunks = nchA + nchB;
+  // load-side cursor (list A, then list B)
+  int ls = 0, lk = 0, lj = 0;
   auto issue = [&](int stage) {
-    const Seg &S = segs[ls];
+    const bool inB = lj >= nchA;
+    const Seg &S = inB ? segsB[ls] : segsA[ls];
+    const int R = inB ? mb : m;
+    ++lj;
     double *As = smem + stage * 2 * OPSZ;
     double *Bs = As + OPSZ;
     bool vecA = ((S.A.off | S.A.ld) & 1) == 0;
     bool vecB = ((S.B.off | S.B.ld) & 1) == 0;
-    load_operand(As, lptr(p, S.A), S.A.ld, S.ta != 0, m, S.k, lk, vecA);
+    load_operand(As, lptr(p, S.A), S.A.ld, S.ta != 0, R, S.k, lk, vecA);
     load_operand(Bs, lptr(p, S.B), S.B.ld, S.tb == 0, n, S.k, lk, vecB);
     lk += KC;
     if (lk >= S.k) {
       lk = 0;
       ++ls;
+      if (lj == nchA) ls = 0;  // switch to list B
     }
   };
   // compute-side cursor (segment layouts)
@@ -185,21 +205,31 @@ __device__ void gemm_mainloop(const Params &p, int s0, int ns, int m, int n, dou
     __syncthreads();
     if (j + STAGES - 1 < nchunks) issue((j + STAGES - 1) % STAGES);
     cp_commit();
-    const Seg &S = segs[cs];
+    const bool inB = j >= nchA;
+    const Seg &S = inB ? segsB[cs] : segsA[cs];
     const double *As = smem + (j % STAGES) * 2 * OPSZ;
     const double *Bs = As + OPSZ;
     const bool akm = S.ta != 0, bkm = S.tb == 0;
     int kleft = S.k - ck;
     int ksteps = kleft >= KC ? KC / 4 : (kleft + 3) / 4;
-    mma_steps(As, akm ? 1 : LD_MK, akm ? LD_KM : 1, Bs, bkm ? 1 : LD_MK, bkm ? LD_KM : 1, acc, ksteps);
+    if (DUAL && inB)
+      mma_steps(As, akm ? 1 : LD_MK, akm ? LD_KM : 1, Bs, bkm ? 1 : LD_MK, bkm ? LD_KM : 1, acc2, ksteps);
+    else
+      mma_steps(As, akm ? 1 : LD_MK, akm ? LD_KM : 1, Bs, bkm ? 1 : LD_MK, bkm ? LD_KM : 1, acc, ksteps);
     ck += KC;
     if (ck >= S.k) {
       ck = 0;
       ++cs;
+      if (j + 1 == nchA) cs = 0;
     }
   }
   cp_wait<0>();
   __syncthreads();
+}
+
+__device__ __forceinline__ void gemm_mainloop(const Params &p, int s0, int ns, int m, int n, double *smem,
+                                              double (&acc)[2][4][2]) {
+  gemm_mainloop2<false>(p, s0, ns, m, 0, 0, 0, n, smem, acc, acc);
 }
 
 // Fragment element coordinates of acc[mi][ni][h].
@@ -331,7 +361,7 @@ __device__ __forceinline__ void phase_mark(const Params &p, int t, int k) {
   if (p.trace && threadIdx.x == 0) p.trace[4 * (size_t)p.ntasks + 8 * (size_t)t + k] = globaltimer();
 }
 
-// select v[ii][kk] for runtime kk (keeps the arrays in registers)
+// select row[kk] for runtime kk without dynamic register indexing
 __device__ __forceinline__ double sel4(const double (&row)[4], int kk) {
   double x = row[0];
   x = (kk == 1) ? row[1] : x;
@@ -340,150 +370,218 @@ __device__ __forceinline__ double sel4(const double (&row)[4], int kk) {
   return x;
 }
 __device__ __forceinline__ void set4(double (&row)[4], int kk, double x) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (q == kk) row[q] = x;
+  row[0] = (kk == 0) ? x : row[0];
+  row[1] = (kk == 1) ? x : row[1];
+  row[2] = (kk == 2) ? x : row[2];
+  row[3] = (kk == 3) ? x : row[3];
 }
 
-// Tile Cholesky + inverse of the diagonal tile (64 x 64), fused into ONE pivot
-// loop with one CTA barrier per pivot:
-//   thread (r = tid & 15, c = tid >> 4) owns S[i][k], i = r + 16 ii, k = c + 16 kk,
-//   so the 16 owners of a column sit in one half-warp.  At step j the owners of
-//   column j+1 take the pivot by shuffle, scale their column by rsqrt(d) and
-//   publish it (L column j+1); everybody applies the rank-1 update of L column j.
-//   The inverse W = L^{-1} is built row by row in the same loop
-//   (W[j][:] = (e_j - sum_{s<j} L[j][s] W[s][:]) / L[j][j], right-looking),
-//   with multiplications by the published 1/L_jj only -- no divisions.
+// 16x16 (x K) warp product on smem operands: acc(16 x 16, 2 x 2 m8n8 fragments) +=
+// A[r][k] * B[k][c],  A at As (row stride lda), B at Bs (row stride ldb).
+__device__ __forceinline__ void warp_mma16(const double *As, int lda, const double *Bs, int ldb, int K,
+                                           double (&acc)[2][2][2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  for (int k0 = 0; k0 < K; k0 += 4) {
+    double a0 = As[g * lda + k0 + q], a1 = As[(g + 8) * lda + k0 + q];
+    double b0 = Bs[(k0 + q) * ldb + g], b1 = Bs[(k0 + q) * ldb + g + 8];
+    dmma(acc[0][0], a0, b0);
+    dmma(acc[0][1], a0, b1);
+    dmma(acc[1][0], a1, b0);
+    dmma(acc[1][1], a1, b1);
+  }
+}
+
+// Diagonal-tile task: optional fused pre-update (GEMM), Cholesky (factor) of the
+// 64 x 64 tile, its inverse W = L^{-1}, log-det partial, info, and the fused TRSM
+// of the sub-diagonal tile (next link of the critical chain).
+//
+// Cholesky: thread (r = tid & 15, c = tid >> 4) owns S[i][k], i = r + 16 ii,
+// k = c + 16 kk, so the 16 owners of a column form one half-warp.  At step j the
+// owners of column j+1 (already updated) take the pivot by shuffle, scale the
+// column by rsqrt(d) and publish it; everybody applies the rank-1 update of L
+// column j (branch-free).  One CTA barrier per pivot.
+// Inverse: blocked on 16 x 16 blocks: the 4 diagonal blocks by right-looking
+// substitution in 4 warps, then the off-diagonal blocks level by level
+// W_ij = -W_ii (sum_k L_ik W_kj) with DMMA (one warp per block).
 __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bool factor, int tsk) {
   const int tid = threadIdx.x, r = tid & 15, c = tid >> 4;
-  const int lane = tid & 31;
+  const int lane = tid & 31, warp = tid >> 5;
   const int m = T.m;
-  double *St = smem;                      // [64][LDT] staging of the input tile
-  double *lb = smem + SERINV_TILE * LDT;  // [3][64] published L columns
-  double *wb = lb + 3 * SERINV_TILE;      // [2][64] published W rows
-  double *rsv = wb + 2 * SERINV_TILE;     // [64] 1 / L_jj
-  double *dv = rsv + SERINV_TILE;         // [64] pivots d_j (factor) / L_jj (trtri)
+  double *St = smem;                      // [64][LDT] L
+  double *Wt = St + SERINV_TILE * LDT;    // [64][LDT] W
+  double *S2 = Wt + SERINV_TILE * LDT;    // [64][LDT] TRSM2 staging / scratch
+  double *lb = S2 + SERINV_TILE * LDT;    // [3][64] published L columns
+  double *rsv = lb + 3 * SERINV_TILE;     // [64] 1 / L_jj
+  double *dv = rsv + SERINV_TILE;         // [64] pivots
   __shared__ int s_bad;
+  const bool trsm2 = factor && (T.flags & TF_TRSM2);
+  double acc2[2][4][2];
   if (factor) {
-    double acc[2][4][2];
-    gemm_mainloop(p, T.seg0, T.nseg1, T.m, T.n, smem, acc);
-    apply_c0(p, T.alpha, T.beta, T.c0, T.m, T.n, acc);
-    acc_to_smem(St, acc);
+    double acc1[2][4][2];
+    // both fused updates (diagonal tile, sub-diagonal tile) through one pipeline
+    if (trsm2)
+      gemm_mainloop2<true>(p, T.seg0, T.nseg1, T.m, T.seg0 + T.nseg1, T.nseg - T.nseg1, T.m3, T.n, smem, acc1, acc2);
+    else
+      gemm_mainloop2<false>(p, T.seg0, T.nseg1, T.m, 0, 0, 0, T.n, smem, acc1, acc1);
+    apply_c0(p, T.alpha, T.beta, T.c0, T.m, T.n, acc1);
+    if (trsm2) apply_c0(p, (T.nseg > T.nseg1) ? T.alpha : 0.0, T.beta3, T.out3, T.m3, m, acc2);
+    __syncthreads();
+    acc_to_smem(St, acc1);
   } else {
     tile_to_smem(St, lptr(p, T.c0), T.c0.ld, m, m);
   }
+  for (int idx = tid; idx < SERINV_TILE * LDT; idx += NT) Wt[idx] = 0.0;
+  if (tid < SERINV_TILE) rsv[tid] = 0.0;
   if (tid == 0) s_bad = 1 << 30;
   __syncthreads();
   phase_mark(p, tsk, 0);
-  double v[4][4], w[4][4];
+  if (factor) {
+    // Left-looking over 16-column blocks; inside a block one barrier per pivot.
+    // Thread (jj = tid & 15, rg = tid >> 4) owns A[i][16 cb + jj], i = 16 cb + rg + 16 t.
+    const int jj = tid & 15, rg = tid >> 4;
+    double *colb = lb;  // [2][64] unscaled pivot columns
+    for (int cb = 0; cb * 16 < m; ++cb) {
+      const int c0 = 16 * cb;
+      const int nrow = m - c0;  // rows c0..m-1
+      // (1) left-looking block update: A[c0:, c0:c0+16] -= L[c0:, :c0] L[c0:c0+16, :c0]^T
+      if (cb > 0) {
+        const int nrg = (nrow + 7) / 8;  // 8-row groups
+        for (int f = warp; f < nrg * 2; f += 8) {
+          const int r8 = c0 + 8 * (f >> 1), n8 = c0 + 8 * (f & 1);
+          const int g = lane >> 2, q = lane & 3;
+          double acc[2] = {0.0, 0.0};
+          for (int k0 = 0; k0 < c0; k0 += 4) {
+            const double av = St[(r8 + g) * LDT + k0 + q];
+            const double bv = St[(n8 + g) * LDT + k0 + q];
+            dmma(acc, av, bv);
+          }
+          St[(r8 + g) * LDT + n8 + 2 * q] -= acc[0];
+          St[(r8 + g) * LDT + n8 + 2 * q + 1] -= acc[1];
+        }
+        __syncthreads();
+      }
+      // (2) 16 pivots
+      double av[4];
 #pragma unroll
-  for (int ii = 0; ii < 4; ++ii)
+      for (int t = 0; t < 4; ++t) {
+        const int i = c0 + rg + 16 * t;
+        av[t] = (i < m) ? St[i * LDT + c0 + jj] : 0.0;
+      }
+      if (jj == 0) {
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      v[ii][kk] = St[(r + 16 * ii) * LDT + c + 16 * kk];
-      w[ii][kk] = 0.0;
+        for (int t = 0; t < 4; ++t) colb[rg + 16 * t] = av[t];  // local row index i - c0
+      }
+      __syncthreads();
+      const int ncol = min(16, nrow);
+      for (int q = 0; q < ncol; ++q) {
+        const double *cq = colb + (q & 1) * SERINV_TILE;
+        const double d = cq[q];
+        const double rs = rsqrt(d);
+        const double id = rs * rs;
+        const double lk = cq[jj] * id;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int il = rg + 16 * t;  // local row
+          const double f = (jj > q && jj <= il) ? cq[il] * lk : 0.0;
+          av[t] -= f;
+        }
+        if (jj == q + 1) {
+          double *cn = colb + ((q + 1) & 1) * SERINV_TILE;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) cn[rg + 16 * t] = av[t];
+        }
+        if (tid == 0) {
+          rsv[c0 + q] = rs;
+          dv[c0 + q] = d;
+          if (!(d > 0.0)) atomicMin(&s_bad, c0 + q);
+        }
+        __syncthreads();
+      }
+      // (3) scale the block's columns: L[i][k] = A[i][k] / sqrt(d_k) (i > k), sqrt(d_k) on the diagonal
+      {
+        const int k = c0 + jj;
+        const double rk = (k < m) ? rsv[k] : 0.0;
+        const double dk = (k < m) ? dv[k] : 0.0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int i = c0 + rg + 16 * t;
+          if (i < SERINV_TILE) {
+            const double x = (i > k) ? av[t] * rk : ((i == k) ? dk * rk : 0.0);
+            St[i * LDT + k] = (i < m && k < m) ? x : 0.0;
+          }
+        }
+        // rows above the block in these columns are the strict upper part: zero
+        for (int i = rg; i < c0; i += 16) St[i * LDT + k] = 0.0;
+      }
+      __syncthreads();
     }
-  // owners of column q publish it (factor: pivot + scaling; trtri: as given)
-  auto publish_col = [&](int q) {
-    const int kk = q >> 4;
-    const int src = (lane & 16) | (q & 15);
-    double mine = 0.0;  // S[q][q] if r == (q & 15)
+  } else {
+    // TRTRI-only: L given; zero its upper part, 1 / L_jj
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii)
-      if (ii == (q >> 4)) mine = sel4(v[ii], kk);
-    // only the 16 owner lanes (one half-warp) execute this: half-warp mask
-    const double d = __shfl_sync(0xFFFFu << (lane & 16), mine, src);
-    double rs;
-    if (factor) {
-      rs = rsqrt(d);
-      if (!(d > 0.0) && r == (q & 15)) atomicMin(&s_bad, q);
-    } else {
-      rs = 1.0 / d;
-      if ((!(d != 0.0) || !isfinite(d)) && r == (q & 15)) atomicMin(&s_bad, q);
-    }
-    double *col = lb + (q % 3) * SERINV_TILE;
-#pragma unroll
-    for (int ii = 0; ii < 4; ++ii) {
-      const int i = r + 16 * ii;
-      double x = sel4(v[ii], kk);
-      if (factor)
-        x = (i > q) ? x * rs : (i == q ? d * rs : 0.0);
-      else
-        x = (i >= q) ? x : 0.0;
-      set4(v[ii], kk, x);
-      col[i] = x;
-    }
-    if (r == (q & 15)) {
-      rsv[q] = rs;
-      dv[q] = d;
-    }
-  };
-  if (c == 0) publish_col(0);
-  __syncthreads();
-  for (int j = 0; j < m; ++j) {
-    const double *lj = lb + (j % 3) * SERINV_TILE;
-    // (a) Cholesky: S[i][k] -= L[i][j] L[k][j], j < k <= i
-    if (factor) {
-      double lk[4];
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) lk[kk] = lj[c + 16 * kk];
-#pragma unroll
-      for (int ii = 0; ii < 4; ++ii) {
-        const int i = r + 16 * ii;
-        const double li = lj[i];
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int k = c + 16 * kk;
-          if (k > j && k <= i) v[ii][kk] = fma(-li, lk[kk], v[ii][kk]);
-        }
-      }
-    }
-    // (b) inverse: acc[i][c'] += L[i][j-1] W[j-1][c'], i > j-1, c' <= j-1
-    if (j > 0) {
-      const double *lp = lb + ((j - 1) % 3) * SERINV_TILE;
-      const double *wp = wb + ((j - 1) & 1) * SERINV_TILE;
-      double wk[4];
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) wk[kk] = wp[c + 16 * kk];
-#pragma unroll
-      for (int ii = 0; ii < 4; ++ii) {
-        const int i = r + 16 * ii;
-        const double li = lp[i];
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int k = c + 16 * kk;
-          if (i > j - 1 && k <= j - 1) w[ii][kk] = fma(li, wk[kk], w[ii][kk]);
-        }
-      }
-    }
-    // (c) owners of column j+1 publish the next L column
-    if (j + 1 < m && c == ((j + 1) & 15)) publish_col(j + 1);
-    // (d) owners of row j finalise W row j = (e_j - acc[j][:]) / L_jj and publish it
-    if (r == (j & 15)) {
-      const double rj = rsv[j];
-      const int ii0 = j >> 4;
-      double *wr = wb + (j & 1) * SERINV_TILE;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const int k = c + 16 * kk;
-        double a = 0.0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q == ii0) a = w[q][kk];
-        const double x = (k <= j) ? (((k == j) ? 1.0 : 0.0) - a) * rj : 0.0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q == ii0) w[q][kk] = x;
-        wr[k] = x;
+        const int i = r + 16 * ii, k = c + 16 * kk;
+        if (k > i) St[i * LDT + k] = 0.0;
       }
+    if (tid < m) {
+      const double d = St[tid * LDT + tid];
+      rsv[tid] = 1.0 / d;
+      if (!(d != 0.0) || !isfinite(d)) atomicMin(&s_bad, tid);
+    }
+  }
+  __syncthreads();
+  phase_mark(p, tsk, 1);
+  // ---- inverse, diagonal 16 x 16 blocks: warp w < 4 inverts block w (lanes 0..15 = columns)
+  if (warp < 4 && 16 * warp < m && lane < 16) {
+    const int base = 16 * warp, cc = lane;
+    double w[16], a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const double x = (k >= cc) ? (((k == cc) ? 1.0 : 0.0) - a[k]) * rsv[base + k] : 0.0;
+      w[k] = x;
+#pragma unroll
+      for (int i = k + 1; i < 16; ++i) a[i] = fma(St[(base + i) * LDT + base + k], x, a[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) Wt[(base + i) * LDT + base + cc] = w[i];
+  }
+  __syncthreads();
+  // ---- off-diagonal blocks, level d = i - j
+  for (int d = 1; d < 4; ++d) {
+    const int bj = warp, bi = warp + d;
+    if (bi < 4 && 16 * bi < m) {
+      double acc[2][2][2] = {};
+      for (int k = bj; k < bi; ++k)
+        warp_mma16(St + (16 * bi) * LDT + 16 * k, LDT, Wt + (16 * k) * LDT + 16 * bj, LDT, 16, acc);
+      double *sc = S2 + warp * 16 * 17;  // per-warp 16 x 16 scratch (stride 17)
+      const int g = lane >> 2, q = lane & 3;
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) sc[(g + 8 * mi) * 17 + 8 * ni + 2 * q + h] = acc[mi][ni][h];
+      __syncwarp();
+      double acc2b[2][2][2] = {};
+      warp_mma16(Wt + (16 * bi) * LDT + 16 * bi, LDT, sc, 17, 16, acc2b);
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            Wt[(16 * bi + g + 8 * mi) * LDT + 16 * bj + 8 * ni + 2 * q + h] = -acc2b[mi][ni][h];
     }
     __syncthreads();
   }
-  phase_mark(p, tsk, 1);
+  phase_mark(p, tsk, 2);
   if (tid == 0 && s_bad < (1 << 30)) record_info(p.info, T.aux1 + s_bad + 1);
   if (factor) {
-    // log det partial: sum_j 0.5 log d_j in a fixed order (tree over 64 values)
-    double *lg = wb;  // reuse
+    // log det partial: sum_j 0.5 log d_j, fixed-order tree over 64 values
+    double *lg = lb;
     if (tid < 64) lg[tid] = (tid < m) ? 0.5 * log(dv[tid]) : 0.0;
     __syncthreads();
     for (int h = 32; h > 0; h >>= 1) {
@@ -491,62 +589,41 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
       __syncthreads();
     }
     if (tid == 0 && T.aux0 >= 0) *lptr(p, T.r) = lg[0];
-    // store L (zeros above the diagonal)
-    double *o = lptr(p, T.out);
-#pragma unroll
-    for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int i = r + 16 * ii, k = c + 16 * kk;
-        if (i < m && k < m) o[(int64_t)i * T.out.ld + k] = (k <= i) ? v[ii][kk] : 0.0;
-      }
   }
-  phase_mark(p, tsk, 2);
-  const Loc &wl = factor ? T.out2 : T.out;
-  if (!factor || (T.flags & TF_W_OUT)) {
-    double *wo = lptr(p, wl);
-#pragma unroll
-    for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int i = r + 16 * ii, k = c + 16 * kk;
-        if (i < m && k < m) wo[(int64_t)i * wl.ld + k] = (k <= i) ? w[ii][kk] : 0.0;
-      }
-  }
-  phase_mark(p, tsk, 3);
-  if (factor && (T.flags & TF_TRSM2)) {
-    // next link of the chain: L2 = (beta3 * C3 - sum_{s >= nseg1} ...) * W^T  (m3 x m);
-    // W stays in registers while the update runs through the staging buffers
-    double acc[2][4][2];
-    __syncthreads();
-    gemm_mainloop(p, T.seg0 + T.nseg1, T.nseg - T.nseg1, T.m3, m, smem, acc);
-    apply_c0(p, (T.nseg > T.nseg1) ? T.alpha : 0.0, T.beta3, T.out3, T.m3, m, acc);
-    double *S2 = smem;
-    double *Wt = smem + SERINV_TILE * LDT;
-    acc_to_smem(S2, acc);
-#pragma unroll
-    for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int i = r + 16 * ii, k = c + 16 * kk;
-        Wt[i * LDT + k] = (k <= i && i < m && k < m) ? w[ii][kk] : 0.0;
-      }
+  // ---- TRSM of the sub-diagonal tile: L2 = S2 * W^T (the update was applied up front)
+  if (trsm2) {
+    acc_to_smem(S2, acc2);
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
-    mma_steps(S2, LDT, 1, Wt, LDT, 1, acc, (m + 3) / 4);
-    store_tile(p, T.out3, T.m3, m, acc);
-    phase_mark(p, tsk, 4);
+      for (int jj = 0; jj < 4; ++jj) acc2[i][jj][0] = acc2[i][jj][1] = 0.0;
+    mma_steps(S2, LDT, 1, Wt, LDT, 1, acc2, (m + 3) / 4);
+    store_tile(p, T.out3, T.m3, m, acc2);
     if (T.flags & TF_ZERO_MIRROR) {  // strict-upper tile (c, c+1) of the diagonal block
       double *z = lptr(p, T.out) + SERINV_TILE;
       for (int idx = tid; idx < m * T.m3; idx += NT) {
-        int rr = idx / T.m3, cc = idx - rr * T.m3;
+        const int rr = idx / T.m3, cc = idx - rr * T.m3;
         z[(int64_t)rr * T.out.ld + cc] = 0.0;
       }
     }
   }
+  phase_mark(p, tsk, 3);
+  // ---- store L (factor) and W
+  {
+    const bool wout = !factor || (T.flags & TF_W_OUT);
+    const Loc &wl = factor ? T.out2 : T.out;
+    double *o = factor ? lptr(p, T.out) : nullptr;
+    double *wo = wout ? lptr(p, wl) : nullptr;
+    for (int idx = tid; idx < SERINV_TILE * SERINV_TILE; idx += NT) {
+      const int i = idx >> 6, k = idx & 63;
+      if (i < m && k < m) {
+        if (o) o[(int64_t)i * T.out.ld + k] = St[i * LDT + k];
+        if (wo) wo[(int64_t)i * wl.ld + k] = Wt[i * LDT + k];
+      }
+    }
+  }
+  phase_mark(p, tsk, 4);
 }
 
 __device__ void run_reduce(const Params &p, const Task &T) {

@@ -430,6 +430,9 @@ struct Builder {
           rt.t.out2 = tileloc(d.base, c, r.q);
         }
         rt.sigs.push_back(fd);
+        // the second row tile below the diagonal feeds the next chain task's fused
+        // update: keep it on the critical queue too
+        if (cx.opt.critical_queues && ri == first_trsm && first_trsm == 1) rt.queue = P.queue;
         int id = cx.emit(std::move(rt));
         st.pending.clear();
         st.last = id;

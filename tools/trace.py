@@ -65,7 +65,7 @@ def main():
         print(f"  POTRF duration mean {dur.mean()/1e3:.2f} us; claim->start {(start-claim)[pot].mean()/1e3:.2f} us")
         P_ = ph[pot] - t0
         st_ = start[pot]
-        names = ["gemm", "chol", "scale+store", "trtri", "trsm2"]
+        names = ["gemm(both)", "chol", "trtri", "trsm2", "store L,W"]
         prev = st_
         for k in range(5):
             cur = P_[:, k]
@@ -73,6 +73,7 @@ def main():
             if ok.any():
                 print(f"    phase {names[k]:12s} {np.mean((cur - prev)[ok])/1e3:8.2f} us")
                 prev = np.where(ok, cur, prev)
+
     # timeline utilisation in 10 buckets
     nb = 20
     edges = np.linspace(0, span, nb + 1)
