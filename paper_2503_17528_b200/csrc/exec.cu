@@ -34,7 +34,7 @@ constexpr int OPSZ = SERINV_TILE * LD_MK;  // doubles per operand stage (2304 >=
 constexpr int LDT = SERINV_TILE + 4;     // full-tile stride in smem (68)
 constexpr int SMEM_DOUBLES = STAGES * 2 * OPSZ;  // 13824 doubles = 110592 bytes
 static_assert(KC * LD_KM <= OPSZ, "km layout fits the stage");
-static_assert(3 * SERINV_TILE * LDT + 5 * SERINV_TILE <= SMEM_DOUBLES, "post/potrf smem fits");
+static_assert(3 * SERINV_TILE * LDT + 6 * SERINV_TILE <= SMEM_DOUBLES, "post/potrf smem fits");
 
 __device__ __forceinline__ int ld_acquire(const int32_t *p) {
   int v;
@@ -70,6 +70,31 @@ __device__ __forceinline__ unsigned smid() {
 }
 
 __device__ __forceinline__ double *lptr(const Params &p, const Loc &l) { return p.bufs[l.buf] + l.off; }
+
+// thread 0 spins until waits [w0, w1) of the task list are satisfied (20 s watchdog)
+__device__ void wait_range(const Params &p, int w0, int w1) {
+  for (int w = w0; w < w1; ++w) {
+    const Wait W = p.waits[w];
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.ctr + W.ctr) : "memory");
+    if (v >= W.target) continue;
+    int ns = 32;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.ctr + W.ctr) : "memory");
+      if (v >= W.target) break;
+      __nanosleep(ns);
+      ns = min(ns * 2, 256);
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > 20000000000ULL) {
+        atomicExch(p.info, -1);
+        break;
+      }
+    }
+  }
+}
 
 __device__ void record_info(int *info, int v) {
   int old = *(volatile int *)info;
@@ -227,6 +252,33 @@ __device__ __forceinline__ void gemm_mainloop2(const Params &p, int s0, int ns, 
   __syncthreads();
 }
 
+// Single-stage main loop (stage buffers at `stage`, 2 * OPSZ doubles): used
+// where the rest of shared memory holds live data (the late tile of a chain task).
+__device__ void gemm_onestage(const Params &p, int s0, int ns, int m, int n, double *stage, double (&acc)[2][4][2]) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const Seg *segs = p.segs + s0;
+  double *As = stage, *Bs = stage + OPSZ;
+  for (int s = 0; s < ns; ++s) {
+    const Seg &S = segs[s];
+    const bool vecA = ((S.A.off | S.A.ld) & 1) == 0, vecB = ((S.B.off | S.B.ld) & 1) == 0;
+    const bool akm = S.ta != 0, bkm = S.tb == 0;
+    for (int k0 = 0; k0 < S.k; k0 += KC) {
+      load_operand(As, lptr(p, S.A), S.A.ld, akm, m, S.k, k0, vecA);
+      load_operand(Bs, lptr(p, S.B), S.B.ld, bkm, n, S.k, k0, vecB);
+      cp_commit();
+      cp_wait<0>();
+      __syncthreads();
+      const int kleft = S.k - k0;
+      const int ksteps = kleft >= KC ? KC / 4 : (kleft + 3) / 4;
+      mma_steps(As, akm ? 1 : LD_MK, akm ? LD_KM : 1, Bs, bkm ? 1 : LD_MK, bkm ? LD_KM : 1, acc, ksteps);
+      __syncthreads();
+    }
+  }
+}
+
 __device__ __forceinline__ void gemm_mainloop(const Params &p, int s0, int ns, int m, int n, double *smem,
                                               double (&acc)[2][4][2]) {
   gemm_mainloop2<false>(p, s0, ns, m, 0, 0, 0, n, smem, acc, acc);
@@ -339,6 +391,10 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem) {
   double acc[2][4][2];
   gemm_mainloop(p, T.seg0, T.nseg, T.m, T.n, smem, acc);
   apply_c0(p, T.alpha, T.beta, T.c0, T.m, T.n, acc);
+  if (T.nlate > 0) {  // late inputs (the post-multiply tile, the SYRK target's updates)
+    if (threadIdx.x == 0) wait_range(p, T.wait0 + T.nwait - T.nlate, T.wait0 + T.nwait);
+    __syncthreads();
+  }
   if (T.flags & TF_POST) {
     double *St = smem;
     double *Rt = smem + SERINV_TILE * LDT;
@@ -355,6 +411,20 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem) {
     __syncthreads();
   }
   store_acc(p, T, acc);
+  if (T.flags & TF_SYRK3) {
+    // the next diagonal tile of the chain: out3 -= L L^T (L = this result, m x n)
+    double *Lt = smem;
+    acc_to_smem(Lt, acc);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    mma_steps(Lt, LDT, 1, Lt, LDT, 1, acc, (T.n + 3) / 4);
+    apply_c0(p, -1.0, 1.0, T.out3, T.m, T.m, acc);
+    store_tile(p, T.out3, T.m, T.m, acc);
+    __syncthreads();
+  }
 }
 
 __device__ __forceinline__ void phase_mark(const Params &p, int t, int k) {
@@ -410,8 +480,8 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   double *St = smem;                      // [64][LDT] L
   double *Wt = St + SERINV_TILE * LDT;    // [64][LDT] W
   double *S2 = Wt + SERINV_TILE * LDT;    // [64][LDT] TRSM2 staging / scratch
-  double *lb = S2 + SERINV_TILE * LDT;    // [3][64] published L columns
-  double *rsv = lb + 3 * SERINV_TILE;     // [64] 1 / L_jj
+  double *lb = S2 + SERINV_TILE * LDT;    // [4][64] published pivot columns
+  double *rsv = lb + 4 * SERINV_TILE;     // [64] 1 / L_jj
   double *dv = rsv + SERINV_TILE;         // [64] pivots
   __shared__ int s_bad;
   const bool trsm2 = factor && (T.flags & TF_TRSM2);
@@ -420,11 +490,11 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
     double acc1[2][4][2];
     // both fused updates (diagonal tile, sub-diagonal tile) through one pipeline
     if (trsm2)
-      gemm_mainloop2<true>(p, T.seg0, T.nseg1, T.m, T.seg0 + T.nseg1, T.nseg - T.nseg1, T.m3, T.n, smem, acc1, acc2);
+      gemm_mainloop2<true>(p, T.seg0, T.nseg1, T.m, T.seg0 + T.nseg1, T.nseg2 - T.nseg1, T.m3, T.n, smem, acc1, acc2);
     else
       gemm_mainloop2<false>(p, T.seg0, T.nseg1, T.m, 0, 0, 0, T.n, smem, acc1, acc1);
     apply_c0(p, T.alpha, T.beta, T.c0, T.m, T.n, acc1);
-    if (trsm2) apply_c0(p, (T.nseg > T.nseg1) ? T.alpha : 0.0, T.beta3, T.out3, T.m3, m, acc2);
+    if (trsm2) apply_c0(p, (T.nseg2 > T.nseg1) ? T.alpha : 0.0, T.beta3, T.out3, T.m3, m, acc2);
     __syncthreads();
     acc_to_smem(St, acc1);
   } else {
@@ -600,11 +670,35 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
       for (int jj = 0; jj < 4; ++jj) acc2[i][jj][0] = acc2[i][jj][1] = 0.0;
     mma_steps(S2, LDT, 1, Wt, LDT, 1, acc2, (m + 3) / 4);
     store_tile(p, T.out3, T.m3, m, acc2);
-    if (T.flags & TF_ZERO_MIRROR) {  // strict-upper tile (c, c+1) of the diagonal block
+    if (T.zmask & 1) {  // strict-upper tile (c, c+1) of the diagonal block
       double *z = lptr(p, T.out) + SERINV_TILE;
       for (int idx = tid; idx < m * T.m3; idx += NT) {
         const int rr = idx / T.m3, cc = idx - rr * T.m3;
         z[(int64_t)rr * T.out.ld + cc] = 0.0;
+      }
+    }
+    if (T.flags & TF_TRSM3) {
+      // second sub-diagonal tile: its inputs were produced by bulk tasks while this
+      // task factorised the diagonal tile -- await them now
+      if (tid == 0) wait_range(p, T.wait0 + T.nwait - T.nlate, T.wait0 + T.nwait);
+      __syncthreads();
+      double *stage = smem + 2 * SERINV_TILE * LDT;  // St (L) and Wt (W) stay live
+      gemm_onestage(p, T.seg0 + T.nseg2, T.nseg - T.nseg2, T.m4, m, stage, acc2);
+      apply_c0(p, (T.nseg > T.nseg2) ? T.alpha : 0.0, T.beta4, T.out4, T.m4, m, acc2);
+      acc_to_smem(S2, acc2);
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc2[i][jj][0] = acc2[i][jj][1] = 0.0;
+      mma_steps(S2, LDT, 1, Wt, LDT, 1, acc2, (m + 3) / 4);
+      store_tile(p, T.out4, T.m4, m, acc2);
+      if (T.zmask & 2) {  // strict-upper tile (c, c+2)
+        double *z = lptr(p, T.out) + 2 * SERINV_TILE;
+        for (int idx = tid; idx < m * T.m4; idx += NT) {
+          const int rr = idx / T.m4, cc = idx - rr * T.m4;
+          z[(int64_t)rr * T.out.ld + cc] = 0.0;
+        }
       }
     }
   }
@@ -637,6 +731,7 @@ __device__ void run_reduce(const Params &p, const Task &T) {
     double v = T.alpha * s;
     if (c0) v += T.beta * __ldcg(c0 + (int64_t)r * T.c0.ld + c);
     o[(int64_t)r * T.out.ld + c] = v;
+    if (T.flags & TF_MIRROR) lptr(p, T.out2)[(int64_t)c * T.out2.ld + r] = v;
   }
 }
 
@@ -698,13 +793,39 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
         break;
       }
     }
+    // The first ncrit DISTINCT SMs in arrival order become critical SMs; on each,
+    // the earliest-arrived CTA serves one critical queue and the others exit, so
+    // every critical chain owns a whole SM.
     int q = 0;
-    const int ncrit = p.nq - 1;
-    if (rank < ncrit) {
-      q = 1 + rank;
-    } else {
-      for (int r = 0; r < ncrit && r < (int)gridDim.x; ++r)
-        if (ld_acquire(role + 2 + r) == me) q = -1;
+    const int ncrit = p.ncrit;
+    int found = 0, last_crit_rank = -1;
+    for (int r = 0; r < (int)gridDim.x && found < ncrit; ++r) {
+      const int sr = ld_acquire(role + 2 + r);
+      bool seen = false;
+      for (int r2 = 0; r2 < r; ++r2)
+        if (ld_acquire(role + 2 + r2) == sr) {
+          seen = true;
+          break;
+        }
+      if (seen) continue;
+      ++found;  // sr is critical SM number `found`
+      last_crit_rank = r;
+      if (sr == me) q = (r == rank) ? found : -1;
+    }
+    // the urgent queue: the first nurgent CTAs (arrival order) not on a critical SM
+    if (q == 0 && p.nurgent > 0 && p.nq > ncrit + 1) {
+      int cnt = 0;
+      for (int r = 0; r < rank; ++r) {
+        const int sr = ld_acquire(role + 2 + r);
+        bool crit = false;
+        for (int r2 = 0; r2 <= last_crit_rank; ++r2)
+          if (ld_acquire(role + 2 + r2) == sr) {
+            crit = true;
+            break;
+          }
+        if (!crit) ++cnt;
+      }
+      if (cnt < p.nurgent) q = ncrit + 1;
     }
     s_q = q;
   }
@@ -731,7 +852,7 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
     const Task T = p.tasks[t];
     if (p.trace && threadIdx.x == 0) t_claim = globaltimer();
     if (threadIdx.x == 0) {
-      for (int w = 0; w < T.nwait; ++w) {
+      for (int w = 0; w < T.nwait - T.nlate; ++w) {
         const Wait W = p.waits[T.wait0 + w];
         if (ld_acquire(p.ctr + W.ctr) >= W.target) continue;
         int ns = 32;
@@ -757,7 +878,8 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
       case TK_LOGDET: run_logdet(p, T, smem); break;
       default: break;
     }
-    __threadfence();
+    // publish: barrier (CTA-scope ordering of every thread's stores) then one
+    // gpu-scope fence by the signalling thread (cumulative) and the increments
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();

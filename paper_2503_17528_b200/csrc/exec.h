@@ -15,7 +15,9 @@ struct Params {
   int32_t *qclaim;       // [nq] claim counters, then [2 + grid] role table (zeroed before each launch)
   const int32_t *qlist;  // task indices per queue
   const int32_t *qoff;   // [nq + 1]
-  int nq;                // queue 0 = bulk, 1..nq-1 = critical chains
+  int nq;                // queue 0 = bulk, 1..ncrit = critical chains, ncrit+1 = urgent (if nq > ncrit+1)
+  int ncrit;             // critical queues (one CTA each, exclusive SM)
+  int nurgent;           // CTAs serving the urgent queue
   int ntasks;
   double *bufs[BUF_COUNT];
   int *info;

@@ -30,6 +30,8 @@ namespace serinv {
 
 namespace {
 
+constexpr int URGENT_QUEUE = 1 << 20;  // placeholder id, renumbered to ncrit + 1 in finalize
+
 inline int ntiles(int64_t s) { return (int)((s + TILE - 1) / TILE); }
 inline int tdim(int64_t s, int t) { return (int)std::min<int64_t>(TILE, s - (int64_t)t * TILE); }
 
@@ -48,6 +50,7 @@ struct RawTask {
   Task t{};
   std::vector<Seg> segs;
   std::vector<int32_t> waits;  // counters (target = #producers, fixed at finalize)
+  std::vector<int32_t> late;   // waits checked late (TF_TRSM3 inputs)
   std::vector<int32_t> sigs;   // counters signalled (own counter first)
   double cost = 0.0;           // ns (scheduler model)
   double flops = 0.0;
@@ -114,14 +117,24 @@ struct Ctx {
   }
   int emit(RawTask &&rt) {
     if (rt.t.type == TK_GEMM)
-      rt.flops = gemm_flops(rt.t.m, rt.t.n, rt.segs) + ((rt.t.flags & TF_POST) ? 2.0 * rt.t.m * rt.t.n * rt.t.n : 0.0);
+      rt.flops = gemm_flops(rt.t.m, rt.t.n, rt.segs) + ((rt.t.flags & TF_POST) ? 2.0 * rt.t.m * rt.t.n * rt.t.n : 0.0) +
+                 ((rt.t.flags & TF_SYRK3) ? 2.0 * rt.t.m * rt.t.m * rt.t.n : 0.0);
     if (rt.t.type == TK_POTRF)
       rt.flops = 2.0 * rt.t.m * rt.t.n * [&] { double k = 0; for (auto &sg : rt.segs) k += sg.k; return k; }() +
-                 2.0 * rt.t.m * rt.t.m * rt.t.m / 3.0 + ((rt.t.flags & TF_TRSM2) ? 2.0 * rt.t.m3 * rt.t.m * rt.t.m : 0.0);
+                 2.0 * rt.t.m * rt.t.m * rt.t.m / 3.0 + ((rt.t.flags & TF_TRSM2) ? 2.0 * rt.t.m3 * rt.t.m * rt.t.m : 0.0) +
+                 ((rt.t.flags & TF_TRSM3) ? 2.0 * rt.t.m4 * rt.t.m * rt.t.m : 0.0);
     if (rt.t.type == TK_TRTRI) rt.flops = rt.t.m * (double)rt.t.m * rt.t.m / 3.0;
     rt.cost = task_cost(rt);
     std::sort(rt.waits.begin(), rt.waits.end());
     rt.waits.erase(std::unique(rt.waits.begin(), rt.waits.end()), rt.waits.end());
+    std::sort(rt.late.begin(), rt.late.end());
+    rt.late.erase(std::unique(rt.late.begin(), rt.late.end()), rt.late.end());
+    {
+      std::vector<int32_t> lt;
+      for (int32_t w : rt.late)
+        if (!std::binary_search(rt.waits.begin(), rt.waits.end(), w)) lt.push_back(w);
+      rt.late.swap(lt);
+    }
     int id = (int)tasks.size();
     int32_t o = new_ctr();
     rt.sigs.insert(rt.sigs.begin(), o);
@@ -211,6 +224,7 @@ struct Builder {
   std::map<int64_t, int> wdiag_task;
   std::map<std::tuple<int, int, int>, int> lam_task;
   std::vector<int32_t> input_waits;  // extra waits for tasks reading the problem's inputs
+  int flush_queue = 0;               // claim queue of update tasks being flushed
 
   Builder(Ctx &c, Problem &p) : cx(c), P(p) {}
 
@@ -271,6 +285,7 @@ struct Builder {
         for (int Z : P.rows[X]) P.Lchk[{Z, X}] = wsloc(cx.alloc((int64_t)P.size[Z] * s), s);
       }
     }
+    if (inverse) allocate_split();
   }
 
   // =================================================================== factor
@@ -325,6 +340,7 @@ struct Builder {
     add_update_segs(rt, Yi, qi, Yj, qj, cols);
     if (st.last >= 0) rt.waits.push_back(cx.ctr_of(st.last));
     for (int32_t w : input_waits) rt.waits.push_back(w);
+    rt.queue = flush_queue;
     st.last = cx.emit(std::move(rt));
     st.written = true;
   }
@@ -386,8 +402,29 @@ struct Builder {
           rt.t.out3 = r0.loc;
           rt.t.m3 = r0.h;
           rt.t.beta3 = (!st0->written && tb0.zero_init) ? 0.0 : 1.0;
-          if (r0.Y == X) rt.t.flags |= TF_ZERO_MIRROR;  // zero tile (c, c+1) = out + TILE columns
+          if (r0.Y == X) rt.t.zmask |= 1;  // zero tile (c, c+1) = out + TILE columns
           first_trsm = 1;
+        }
+        rt.t.nseg2 = (int32_t)rt.segs.size();
+        TileState *st1 = nullptr;
+        if (first_trsm == 1 && cx.opt.fuse_trsm3 && rts.size() >= 2) {
+          // the second sub-diagonal tile: its own inputs (a bulk TRSM of the previous
+          // column, earlier updates) are awaited late, after the POTRF
+          const RT &r1 = rts[1];
+          const BlkRef &tb1 = (r1.Y == X) ? d : B(r1.Y, X);
+          st1 = &tstate[tkey(r1.Y, X, r1.q, c)];
+          flush(r1.Y, r1.q, X, c, tb1, *st1, 1);
+          RawTask tmp;
+          if (!st1->pending.empty()) add_update_segs(tmp, r1.Y, r1.q, X, c, st1->pending);
+          for (auto &sg : tmp.segs) rt.segs.push_back(sg);
+          rt.late = tmp.waits;
+          if (st1->last >= 0) rt.late.push_back(cx.ctr_of(st1->last));
+          rt.t.flags |= TF_TRSM3;
+          rt.t.out4 = r1.loc;
+          rt.t.m4 = r1.h;
+          rt.t.beta4 = (!st1->written && tb1.zero_init) ? 0.0 : 1.0;
+          if (r1.Y == X) rt.t.zmask |= 2;  // zero tile (c, c+2)
+          first_trsm = 2;
         }
         rt.queue = cx.opt.critical_queues ? P.queue : 0;
         int id = cx.emit(std::move(rt));
@@ -402,11 +439,21 @@ struct Builder {
           st0->written = true;
           Lprod[key4(rts[0].Y, rts[0].q, X, c)] = id;
         }
+        if (st1) {
+          st1->pending.clear();
+          st1->last = id;
+          st1->written = true;
+          Lprod[key4(rts[1].Y, rts[1].q, X, c)] = id;
+        }
       }
+      uint64_t fused_diag = ~0ull;  // next diagonal tile whose column-(X,c) update is fused below
       for (size_t ri = first_trsm; ri < rts.size(); ++ri) {  // TRSM = (A - last update) W(c,c)^T
         const RT &r = rts[ri];
         const BlkRef &tb = (r.Y == X) ? d : B(r.Y, X);
         TileState &st = tstate[tkey(r.Y, X, r.q, c)];
+        // updates feeding the chain's next two tiles are near-critical: urgent queue
+        const bool near = cx.opt.critical_queues && cx.opt.split_chain && cx.opt.urgent_ctas > 0 && ri < 2;
+        flush_queue = near ? URGENT_QUEUE : 0;
         flush(r.Y, r.q, X, c, tb, st, 1);
         RawTask rt;
         rt.t.type = TK_GEMM;
@@ -422,29 +469,61 @@ struct Builder {
           rt.t.alpha = 0.0;
         if (st.last >= 0) rt.waits.push_back(cx.ctr_of(st.last));
         for (int32_t iw : input_waits) rt.waits.push_back(iw);
-        rt.waits.push_back(cx.ctr_of(Lprod.at(key4(X, c, X, c))));
-        rt.t.flags = TF_POST | TF_POST_T;
+        TileState *sdp = nullptr;
+        uint64_t dk = tkey(r.Y, r.Y, r.q, r.q);
+        if (cx.opt.split_chain && cx.opt.chain_syrk && ri == 0 && first_trsm == 0 && has(r.Y, r.Y)) {
+          const BlkRef &bd = B(r.Y, r.Y);
+          TileState &sd = tstate[dk];
+          if (!(bd.zero_init && !sd.written)) {
+            // the chain: L(K+1,K) = E W_K^T, then the next diagonal tile -= L L^T here,
+            // so the next POTRF starts from a fully updated tile.  The update of E runs
+            // while POTRF(K) is still busy: W_K and the diagonal tile's earlier updates
+            // are awaited late.
+            flush(r.Y, r.q, r.Y, r.q, bd, sd, 0);
+            flush_queue = 0;
+            rt.t.flags = TF_SYRK3;
+            rt.t.out3 = tileloc(bd.base, r.q, r.q);
+            rt.t.m3 = r.h;
+            rt.late.push_back(cx.ctr_of(Lprod.at(key4(X, c, X, c))));
+            if (sd.last >= 0) rt.late.push_back(cx.ctr_of(sd.last));
+            sdp = &sd;
+            fused_diag = dk;
+          }
+        }
+        if (!sdp) rt.waits.push_back(cx.ctr_of(Lprod.at(key4(X, c, X, c))));
+        rt.t.flags |= TF_POST | TF_POST_T;
         rt.t.r = tileloc(P.W[X], c, c);
         if (r.Y == X) {
           rt.t.flags |= TF_ZERO_MIRROR;
           rt.t.out2 = tileloc(d.base, c, r.q);
         }
         rt.sigs.push_back(fd);
-        // the second row tile below the diagonal feeds the next chain task's fused
-        // update: keep it on the critical queue too
-        if (cx.opt.critical_queues && ri == first_trsm && first_trsm == 1) rt.queue = P.queue;
+        // the sub-diagonal TRSMs feed the next POTRF: critical queues too
+        flush_queue = 0;
+        if (cx.opt.critical_queues) {
+          if (cx.opt.split_chain && first_trsm == 0 && ri == 0) rt.queue = P.queue2;
+          else if (cx.opt.split_chain && first_trsm == 0 && ri == 1 && cx.opt.urgent_ctas > 0) rt.queue = URGENT_QUEUE;
+          else if (ri == first_trsm && first_trsm == 1) rt.queue = P.queue;
+        }
         int id = cx.emit(std::move(rt));
         st.pending.clear();
         st.last = id;
         st.written = true;
         Lprod[key4(r.Y, r.q, X, c)] = id;
+        if (sdp) {
+          sdp->pending.clear();
+          sdp->last = id;
+          sdp->written = true;
+        }
       }
       for (size_t j = 0; j < rts.size(); ++j)
         for (size_t i = j; i < rts.size(); ++i) {
           const RT &ri = rts[i], &rj = rts[j];
           if (ri.Y == rj.Y && ri.q < rj.q) continue;
           if (rj.Y != X && ri.Y != rj.Y && !has(ri.Y, rj.Y)) continue;
-          tstate[tkey(ri.Y, rj.Y, ri.q, rj.q)].pending.push_back({X, c});
+          const uint64_t k = tkey(ri.Y, rj.Y, ri.q, rj.q);
+          if (k == fused_diag) continue;  // applied by the fused SYRK of the chain TRSM
+          tstate[k].pending.push_back({X, c});
         }
     }
   }
@@ -555,6 +634,95 @@ struct Builder {
       }
   }
 
+  // ---- split-K of the Takahashi tile tasks (better packing of the inversion waves)
+  int64_t split_base = -1;      // ring of partial tiles: 2 slots x tiles x pieces x TILE^2
+  int split_tiles = 0, split_pieces = 0, split_step = 0;
+  std::vector<int> last_reduce;  // per (slot, tile): REDUCE that last read the partials
+
+  void allocate_split() {
+    if (cx.opt.si_split <= 0) return;
+    int nn = (int)P.size.size();
+    for (int X = 0; X < nn; ++X) {
+      if (!P.elim[X] || P.rows[X].empty()) continue;
+      int nt = ntiles(P.size[X]), tiles = nt * (nt + 1) / 2;
+      int64_t K = 0;
+      for (int Y : P.rows[X]) {
+        tiles += ntiles(P.size[Y]) * nt;
+        K += P.size[Y];
+      }
+      split_tiles = std::max(split_tiles, tiles);
+      split_pieces = std::max(split_pieces, (int)((K + cx.opt.si_split - 1) / cx.opt.si_split));
+    }
+    if (split_pieces < 2) return;
+    split_base = cx.alloc((int64_t)2 * split_tiles * split_pieces * TILE * TILE);
+    last_reduce.assign((size_t)2 * split_tiles, -1);
+  }
+
+  static std::vector<Seg> slice(const std::vector<Seg> &segs, int k0, int k1) {
+    std::vector<Seg> out;
+    int off = 0;
+    for (const Seg &sg : segs) {
+      int a = std::max(k0, off), b = std::min(k1, off + sg.k);
+      if (a < b) {
+        Seg t = sg;
+        int lo = a - off;
+        t.k = b - a;
+        t.A.off += sg.ta ? (int64_t)lo * sg.A.ld : lo;
+        t.B.off += sg.tb ? lo : (int64_t)lo * sg.B.ld;
+        out.push_back(t);
+      }
+      off += sg.k;
+    }
+    return out;
+  }
+
+  // emit a Takahashi tile task, split along K into partial GEMMs + a fixed-order REDUCE
+  void emit_split(RawTask &&rt, int tile) {
+    int K = 0;
+    for (auto &sg : rt.segs) K += sg.k;
+    const int KS = cx.opt.si_split;
+    if (split_base < 0 || KS <= 0 || K < (3 * KS) / 2 || tile >= split_tiles) {
+      cx.emit(std::move(rt));
+      return;
+    }
+    int pieces = std::min(split_pieces, (K + KS - 1) / KS);
+    int per = (K + pieces - 1) / pieces;
+    const int slot = split_step & 1;
+    const int64_t tbase = split_base + (((int64_t)slot * split_tiles + tile) * split_pieces) * TILE * TILE;
+    int &lr = last_reduce[(size_t)slot * split_tiles + tile];
+    std::vector<int32_t> own;
+    for (int j = 0; j < pieces; ++j) {
+      RawTask pt;
+      pt.t.type = TK_GEMM;
+      pt.t.m = rt.t.m;
+      pt.t.n = rt.t.n;
+      pt.t.out = Loc{BUF_WS, TILE, tbase + (int64_t)j * TILE * TILE};
+      pt.t.alpha = 1.0;
+      pt.t.beta = 0.0;
+      pt.segs = slice(rt.segs, j * per, std::min(K, (j + 1) * per));
+      pt.waits = rt.waits;
+      if (lr >= 0) pt.waits.push_back(cx.ctr_of(lr));  // WAR on the partial slot
+      own.push_back(cx.ctr_of(cx.emit(std::move(pt))));
+    }
+    RawTask red;
+    red.t.type = TK_REDUCE;
+    red.t.m = rt.t.m;
+    red.t.n = rt.t.n;
+    red.t.out = rt.t.out;
+    red.t.c0 = rt.t.c0;
+    red.t.beta = rt.t.beta;
+    red.t.alpha = rt.t.alpha;
+    red.t.r = Loc{BUF_WS, TILE, tbase};
+    red.t.aux2 = (int64_t)TILE * TILE;
+    red.t.aux0 = pieces;
+    red.t.flags = rt.t.flags & TF_MIRROR;
+    red.t.out2 = rt.t.out2;
+    red.waits = rt.waits;
+    for (int32_t o : own) red.waits.push_back(o);
+    red.sigs = rt.sigs;
+    lr = cx.emit(std::move(red));
+  }
+
   // X_{Y,Z} row tile q: Y >= Z at blk(Y,Z) (row tile, op N), else blk(Z,Y)^T (col tile, op T)
   void xrow(RawTask &rt, int Y, int Z, int q, Loc &loc, int &trans, int &k) {
     if (Y >= Z) {
@@ -574,6 +742,7 @@ struct Builder {
     int nt = ntiles(P.size[X]);
     int32_t pre = gctr(predone, X);
     const auto &R = P.rows[X];
+    int tile = 0;
     for (int Y : R) {  // X_{Y,X}(q,c) = -sum_Z X_{Y,Z}(q,:) Lchk(Z,X)(:,c)
       const BlkRef &by = B(Y, X);
       for (int q = 0; q < ntiles(P.size[Y]); ++q)
@@ -595,7 +764,7 @@ struct Builder {
           rt.waits.push_back(pre);  // WAR: L_{Y,X} consumed by the precompute
           rt.sigs.push_back(XR(Y, X, q));
           rt.sigs.push_back(XC(Y, X, c));
-          cx.emit(std::move(rt));
+          emit_split(std::move(rt), tile++);
         }
     }
     // X_{X,X}(r,c) = Lambda(r,c) - sum_Y X_{Y,X}(:,r)^T Lchk(Y,X)(:,c), r >= c, mirrored
@@ -627,8 +796,9 @@ struct Builder {
           rt.sigs.push_back(XR(X, X, c));
           rt.sigs.push_back(XC(X, X, r));
         }
-        cx.emit(std::move(rt));
+        emit_split(std::move(rt), tile++);
       }
+    ++split_step;
   }
 };
 
@@ -642,6 +812,7 @@ Graph Ctx::finalize() {
   const int C = nctr;
   std::vector<int32_t> nprod(C, 0), nwaiter(C, 0);
   for (auto &t : tasks) {
+    for (int32_t w : t.late) t.waits.push_back(w);  // the scheduler sees early + late waits
     for (int32_t s : t.sigs) nprod[s]++;
     for (int32_t w : t.waits) nwaiter[w]++;
   }
@@ -739,7 +910,8 @@ Graph Ctx::finalize() {
     task.nseg = (int32_t)rt.segs.size();
     for (auto &s : rt.segs) g.segs.push_back(s);
     task.wait0 = (int32_t)g.waits.size();
-    task.nwait = (int32_t)rt.waits.size();
+    task.nwait = (int32_t)rt.waits.size();  // early waits first, the last nlate are late
+    task.nlate = (int32_t)rt.late.size();
     for (int32_t w : rt.waits) g.waits.push_back(Wait{w, nprod[w]});
     task.sig0 = (int32_t)g.sigs.size();
     task.nsig = (int32_t)rt.sigs.size();
@@ -747,6 +919,18 @@ Graph Ctx::finalize() {
     g.tasks.push_back(task);
     g.flops += rt.flops;
   }
+  int ncrit = 0;
+  bool has_urgent = false;
+  for (int t : order) {
+    if (tasks[t].queue == URGENT_QUEUE)
+      has_urgent = true;
+    else
+      ncrit = std::max(ncrit, tasks[t].queue);
+  }
+  for (int t : order)
+    if (tasks[t].queue == URGENT_QUEUE) tasks[t].queue = ncrit + 1;
+  g.ncrit = ncrit;
+  g.nurgent = has_urgent ? std::max(1, opt.urgent_ctas) : 0;
   int nq = 1;
   for (int t : order) nq = std::max(nq, tasks[t].queue + 1);
   g.qoff.assign(nq + 1, 0);
@@ -879,6 +1063,7 @@ Graph build_seq_ctx(Ctx &cx, int kind, int64_t n, int64_t b, int64_t a) {
       [&](int i) { return famA(b, a).at(i); }, Loc{BUF_TIP, (int32_t)a, 0}, false, (int)n, true,
       [&](int i) { return (int64_t)i * b; }, n * b);
   P.queue = 1;
+  P.queue2 = 2;
   Builder bld(cx, P);
   bld.allocate(inv);
   int nn = (int)P.size.size();
@@ -926,6 +1111,7 @@ void ppobtaf_part(Ctx &cx, PartState &ps, int64_t b, int64_t a) {
     middle_problem(ps.prob, ps.ls, cnt, b, a, ps.U, ps.Bbuf, ps.s);
   }
   ps.prob.queue = ps.queue;
+  ps.prob.queue2 = ps.queue + 1;
   ps.bld.reset(new Builder(cx, ps.prob));
   Builder &B = *ps.bld;
   B.allocate(true);
@@ -1036,6 +1222,7 @@ void reduced_from_records(Ctx &cx, int P, int64_t n, int64_t b, int64_t a, int32
       R.P, nr, b, a, [&](int i) { return R.D.at(i); }, [&](int i) { return R.Lo.at(i); },
       [&](int i) { return R.Ar.at(i); }, R.tip, false, nr, true, rb, n * b);
   R.P.queue = 1;
+  R.P.queue2 = 2;
   R.B.reset(new Builder(cx, R.P));
   R.B->input_waits = ready;
   R.B->allocate(true);
@@ -1096,22 +1283,28 @@ void ppobtasi_part(Ctx &cx, PartState &ps, int64_t b, bool have_wdiag) {
 
 }  // namespace
 
-int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a) {
-  // mirrors the allocation order of build_seq_ctx (checked in build_sequential)
-  auto up = [](int64_t d) { return (std::max<int64_t>(d, 1) + 31) / 32 * 32; };
+int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a, const BuildOptions &opt) {
+  // replays the allocations of build_seq_ctx (no tasks are built)
+  Ctx cx;
+  cx.opt = opt;
   bool inv = kind != 0;
-  int64_t tot = up(slot_bound(n, b, a));
-  tot += n * (up(b * b) + (inv ? up(b * b) : 0));
-  if (inv) tot += (n - 1) * up(b * b) + (a > 0 ? n * up(a * b) : 0);
-  if (a > 0) tot += up(a * a) + (inv ? up(a * a) : 0);
-  return tot * 8;
+  cx.slot_cap = slot_bound(n, b, a);
+  cx.slot_region = cx.alloc(cx.slot_cap);
+  Problem P;
+  chain_problem(
+      P, (int)n, b, a, [&](int i) { return famD(b).at(i); }, [&](int i) { return famL(b).at(i); },
+      [&](int i) { return famA(b, a).at(i); }, Loc{BUF_TIP, (int32_t)a, 0}, false, (int)n, true,
+      [&](int i) { return (int64_t)i * b; }, n * b);
+  Builder bld(cx, P);
+  bld.allocate(inv);
+  return cx.ws_top * 8;
 }
 
 Graph build_sequential(int kind, int64_t n, int64_t b, int64_t a, const BuildOptions &opt) {
   Ctx cx;
   cx.opt = opt;
   Graph g = build_seq_ctx(cx, kind, n, b, a);
-  if (g.error.empty() && g.ws_doubles * 8 > sequential_ws_bytes(kind, n, b, a))
+  if (g.error.empty() && g.ws_doubles * 8 > sequential_ws_bytes(kind, n, b, a, opt))
     g.error = "workspace accounting mismatch";
   return g;
 }
@@ -1158,7 +1351,7 @@ Graph build_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, const Buil
     parts[p].s = starts[p];
     parts[p].e = starts[p + 1];
     parts[p].ls = starts[p];
-    parts[p].queue = p + 1;
+    parts[p].queue = 2 * p + 1;
     ppobtaf_part(cx, parts[p], b, a);
   }
   int32_t packed = cx.new_ctr();

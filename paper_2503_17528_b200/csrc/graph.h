@@ -40,6 +40,8 @@ struct Graph {
   // claim queues: queue 0 = bulk, queues 1..nq-1 = critical chains (one CTA each,
   // alone on its SM).  qlist holds task indices, queue q = qlist[qoff[q] .. qoff[q+1]).
   std::vector<int32_t> qlist, qoff;
+  int ncrit = 0;     // queues 1..ncrit: one CTA each, alone on its SM
+  int nurgent = 0;   // queue ncrit+1 (if any): served by nurgent CTAs (near-critical tasks)
   std::string error;         // non-empty if building failed
 };
 
@@ -67,6 +69,7 @@ struct Problem {
   std::map<std::pair<int, int>, Loc> Lchk;     // Lchk(Z,X) = L_{Z,X} W_X
   std::vector<int64_t> slot;      // logdet slot base per node (-1: none)
   int queue = 0;                  // claim queue of this problem's POTRF chain (0 = bulk)
+  int queue2 = 0;                 // claim queue of the chain's sub-diagonal TRSMs (split chain)
 };
 
 struct BuildOptions {
@@ -74,14 +77,19 @@ struct BuildOptions {
   int update_group = 4;    // tile columns per chained update task (regular targets)
   bool schedule = true;
   bool critical_queues = true;  // dedicated CTAs for the POTRF chains
-  bool fuse_trsm = true;        // fuse the sub-diagonal TRSM into each POTRF task
+  bool fuse_trsm = false;       // fuse the sub-diagonal TRSM into each POTRF task
+  bool fuse_trsm3 = false;      // ... and the second sub-diagonal TRSM (late inputs)
+  bool split_chain = true;      // POTRF chain on one critical CTA, its TRSMs on a second one
+  bool chain_syrk = true;       // the sub-diagonal TRSM also applies its SYRK to the next diagonal tile
+  int urgent_ctas = 0;          // CTAs serving the near-critical queue (0: no urgent queue)
+  int si_split = 320;           // K per partial GEMM of the Takahashi tile tasks (0 = no split)
 };
 
 // Sequential problems (whole matrix).  kind: 0 = pobtaf, 1 = pobtasi, 2 = selinv.
 Graph build_sequential(int kind, int64_t n, int64_t b, int64_t a, const BuildOptions &opt);
 
 // Workspace bytes for the sequential kinds (doubles region + counters).
-int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a);
+int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a, const BuildOptions &opt = BuildOptions());
 
 // In-process partitioned pipeline on one device (PPOBTAF -> POBTARSSI -> PPOBTASI).
 Graph build_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, const BuildOptions &opt);

@@ -36,6 +36,7 @@ struct DevGraph {
   const int32_t *d_qlist = nullptr;
   const int32_t *d_qoff = nullptr;
   int nq = 1;
+  int ncrit = 0, nurgent = 0;
   int64_t nctr_alloc = 0;
   int64_t ntasks = 0;
   ~DevGraph() {
@@ -88,6 +89,8 @@ int upload(DevGraph &dg, int grid) {
   dg.d_qlist = (const int32_t *)put(g.qlist.data(), bq);
   dg.d_qoff = (const int32_t *)put(g.qoff.data(), bo);
   dg.nq = (int)g.qoff.size() - 1;
+  dg.ncrit = g.ncrit;
+  dg.nurgent = g.nurgent;
   dg.nctr_alloc = (int64_t)g.nctr + dg.nq + 2 + grid;
   if (cudaMalloc(&dg.ctr, (size_t)dg.nctr_alloc * sizeof(int32_t)) != cudaSuccess) return SERINV_ERR_CUDA;
   dg.ntasks = (int64_t)g.tasks.size();
@@ -152,6 +155,8 @@ int launch(serinv_handle_t h, DevGraph &dg, double *bufs[BUF_COUNT], int *d_info
   p.qlist = dg.d_qlist;
   p.qoff = dg.d_qoff;
   p.nq = dg.nq;
+  p.ncrit = dg.ncrit;
+  p.nurgent = dg.nurgent;
   p.ntasks = (int)dg.ntasks;
   for (int i = 0; i < BUF_COUNT; ++i) p.bufs[i] = bufs[i];
   p.info = d_info;
@@ -295,11 +300,23 @@ int serinv_plan(int64_t n, int P, double r, int64_t *starts) {
   return SERINV_OK;
 }
 
+// workspace queries of the partitioned graphs build the graph: memoise them
+static std::mutex g_ws_mu;
+static std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int64_t, int, int64_t, int64_t>, int64_t> g_ws_cache;
+
 int serinv_pselinv_ws(int64_t n, int64_t b, int64_t a, int P, double r, size_t *bytes) {
   if (!bytes) return -6;
+  if (n < 1 || b < 1 || a < 0) return SERINV_ERR_SHAPE;
   std::vector<int64_t> s;
   if (!plan_partitions(n, P, r, s)) return SERINV_ERR_PLAN;
-  *bytes = (size_t)pselinv_ws_bytes(n, b, a, P, r);
+  int64_t rb;
+  memcpy(&rb, &r, 8);
+  auto key = std::make_tuple(3, n, b, a, P, rb, 0, (int64_t)0, (int64_t)0);
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto it = g_ws_cache.find(key);
+  int64_t v = it != g_ws_cache.end() ? it->second : (g_ws_cache[key] = pselinv_ws_bytes(n, b, a, P, r));
+  if (v < 0) return SERINV_ERR_SHAPE;
+  *bytes = (size_t)v;
   return SERINV_OK;
 }
 
@@ -345,7 +362,16 @@ int serinv_ppobtaf_ws(const serinv_part_t *part, int64_t b, int64_t a, size_t *b
   int rc = check_part(part);
   if (rc) return rc;
   if (!bytes) return -4;
-  *bytes = (size_t)distributed_ws_bytes(part->P, part->rank, part->n_global, part->start, part->count, b, a);
+  if (b < 1 || a < 0) return SERINV_ERR_SHAPE;
+  auto key = std::make_tuple(4, part->n_global, b, a, part->P, (int64_t)0, part->rank, part->start, part->count);
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto it = g_ws_cache.find(key);
+  int64_t v = it != g_ws_cache.end()
+                  ? it->second
+                  : (g_ws_cache[key] = distributed_ws_bytes(part->P, part->rank, part->n_global, part->start,
+                                                            part->count, b, a));
+  if (v < 0) return SERINV_ERR_SHAPE;
+  *bytes = (size_t)v;
   return SERINV_OK;
 }
 

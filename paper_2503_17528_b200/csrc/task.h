@@ -34,7 +34,7 @@ enum TaskKind : int16_t {
   TK_LOGDET = 6,
 };
 
-enum TaskFlags : int16_t {
+enum TaskFlags : uint16_t {
   TF_MIRROR = 1,      // also store the transpose of the result at out2
   TF_POST = 2,        // right-multiply the result by op(R) (R is n x n)
   TF_POST_T = 4,      // op(R) = R^T (else R)
@@ -42,6 +42,8 @@ enum TaskFlags : int16_t {
   TF_TRANS_C0 = 16,   // TK_COPY: out = alpha * C0^T
   TF_W_OUT = 32,      // TK_POTRF: store W = L^{-1} at out2
   TF_TRSM2 = 64,      // TK_POTRF: fused TRSM of the sub-diagonal tile (out3)
+  TF_TRSM3 = 128,     // TK_POTRF: fused TRSM of the second sub-diagonal tile (out4)
+  TF_SYRK3 = 256,     // TK_GEMM (+TF_POST): then out3 (m x m) -= L L^T with L the result
 };
 
 // Buffer ids (kernel argument `bufs[]`, offsets in doubles).
@@ -75,7 +77,8 @@ struct Wait {
 };
 
 struct Task {
-  int16_t type, flags;
+  int16_t type;
+  uint16_t flags;
   int16_t m, n;         // output tile dims (<= SERINV_TILE)
   int32_t seg0, nseg;
   int32_t wait0, nwait;
@@ -89,8 +92,16 @@ struct Task {
   Loc out3;
   double beta3;
   int32_t m3, nseg1;
+  // TK_POTRF with TF_TRSM3: the second sub-diagonal tile at out4 (m4 rows),
+  // update segments [nseg2, nseg); its inputs are awaited LATE: waits
+  // [nwait - nlate, nwait) are checked only after the diagonal tile is done.
+  // zmask bit0 / bit1: zero the strict-upper mirror tile at out + 64 / out + 128.
+  Loc out4;
+  double beta4;
+  int32_t m4, nseg2;
+  int32_t nlate, zmask;
 };
 
 static_assert(sizeof(Loc) == 16, "Loc layout");
 static_assert(sizeof(Seg) == 40, "Seg layout");
-static_assert(sizeof(Task) == 160, "Task layout");
+static_assert(sizeof(Task) == 200, "Task layout");

@@ -51,11 +51,11 @@ def ptrs(A):
     return [A[k].ctypes.data_as(P_) for k in KEYS]
 
 
-def run_seq(kind, A0, grid=16, ug=4):
+def run_seq(kind, A0, grid=16, ug=4, si_split=-1):
     A, n, b, a = prep(A0)
     ld, info, nt = ctypes.c_double(0), ctypes.c_int(0), ctypes.c_int64(0)
     rc = lib().dag_run_sequential(kind, ctypes.c_int64(n), ctypes.c_int64(b), ctypes.c_int64(a), *ptrs(A),
-                                  ctypes.byref(ld), ctypes.byref(info), grid, ug, ctypes.byref(nt))
+                                  ctypes.byref(ld), ctypes.byref(info), grid, ug, ctypes.byref(nt), si_split)
     assert rc == 0
     return A, ld.value, info.value
 
@@ -86,6 +86,17 @@ def test_schedule_options_do_not_change_results(ug, grid):
     L, X, ld = seq.selinv(A0)
     R, ldr, info = run_seq(2, A0, grid=grid, ug=ug)
     assert inv.max_block_err(cut(R, X), X)[0] < 1e-12
+
+
+@pytest.mark.parametrize("si_split", [0, 16, 64, 100])
+def test_split_k_inversion(si_split):
+    # the Takahashi tile tasks split along K into partial GEMMs + fixed-order REDUCE
+    A0 = btagen.g2(3, 5, 130, 20)
+    L, X, ld = seq.selinv(A0)
+    for kind, src, ref in ((2, A0, X), (1, L, X)):
+        R, _, info = run_seq(kind, src, si_split=si_split)
+        assert info == 0
+        assert inv.max_block_err(cut(R, ref), ref)[0] < 1e-12
 
 
 def test_info_first_bad_pivot():

@@ -75,6 +75,15 @@ int run(const Graph &g, Ctx &c) {
       double *o = ptr(c, T.out);
       for (int i = 0; i < m; ++i)
         for (int j = 0; j < n; ++j) o[(int64_t)i * T.out.ld + j] = A_(i, j);
+      if (T.flags & TF_SYRK3) {
+        double *o3 = ptr(c, T.out3);
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < m; ++j) {
+            double s = 0;
+            for (int k = 0; k < n; ++k) s += A_(i, k) * A_(j, k);
+            o3[(int64_t)i * T.out3.ld + j] -= s;
+          }
+      }
       if (T.flags & TF_MIRROR) {
         double *o2 = ptr(c, T.out2);
         for (int i = 0; i < m; ++i)
@@ -136,32 +145,43 @@ int run(const Graph &g, Ctx &c) {
           if (!(A_(j, j) != 0.0) || !std::isfinite(A_(j, j)))
             if (!c.info || T.aux1 + j + 1 < c.info) c.info = T.aux1 + j + 1;
       }
-      if (T.type == TK_POTRF && (T.flags & TF_TRSM2)) {
-        // L2 = (beta3 * C3 + alpha * sum_{s >= nseg1} ...) W^T at out3 (m3 x m)
-        double alpha2 = (T.nseg > T.nseg1) ? T.alpha : 0.0;
-        std::vector<double> S2(T.m3 * m);
-        for (int i = 0; i < T.m3; ++i)
+      auto trsm_tile = [&](int s0, int s1, const Loc &out, int mm, double beta) {
+        // (beta * C + alpha * sum_{s0 <= s < s1} ...) * W^T  at out (mm x m)
+        double alpha = (s1 > s0) ? T.alpha : 0.0;
+        std::vector<double> S2(mm * m);
+        for (int i = 0; i < mm; ++i)
           for (int j = 0; j < m; ++j) {
             double s = 0;
-            for (int si = T.nseg1; si < T.nseg; ++si) {
+            for (int si = s0; si < s1; ++si) {
               const Seg &S = g.segs[T.seg0 + si];
               for (int k = 0; k < S.k; ++k) s += opget(c, S.A, S.ta, i, k) * opget(c, S.B, S.tb, k, j);
             }
-            double v = alpha2 * s;
-            if (T.beta3 != 0.0) v += T.beta3 * get(c, T.out3, i, j);
+            double v = alpha * s;
+            if (beta != 0.0) v += beta * get(c, out, i, j);
             S2[i * m + j] = v;
           }
-        double *o3 = ptr(c, T.out3);
-        for (int i = 0; i < T.m3; ++i)
+        double *o3 = ptr(c, out);
+        for (int i = 0; i < mm; ++i)
           for (int j = 0; j < m; ++j) {
             double s = 0;
             for (int k = 0; k < m; ++k) s += S2[i * m + k] * W[j * m + k];
-            o3[(int64_t)i * T.out3.ld + j] = s;
+            o3[(int64_t)i * out.ld + j] = s;
           }
-        if (T.flags & TF_ZERO_MIRROR) {
+      };
+      if (T.type == TK_POTRF && (T.flags & TF_TRSM2)) {
+        trsm_tile(T.nseg1, T.nseg2, T.out3, T.m3, T.beta3);
+        if (T.zmask & 1) {
           double *z = ptr(c, T.out) + SERINV_TILE;
           for (int i = 0; i < m; ++i)
             for (int j = 0; j < T.m3; ++j) z[(int64_t)i * T.out.ld + j] = 0.0;
+        }
+      }
+      if (T.type == TK_POTRF && (T.flags & TF_TRSM3)) {
+        trsm_tile(T.nseg2, T.nseg, T.out4, T.m4, T.beta4);
+        if (T.zmask & 2) {
+          double *z = ptr(c, T.out) + 2 * SERINV_TILE;
+          for (int i = 0; i < m; ++i)
+            for (int j = 0; j < T.m4; ++j) z[(int64_t)i * T.out.ld + j] = 0.0;
         }
       }
     } else if (T.type == TK_REDUCE) {
@@ -173,6 +193,7 @@ int run(const Graph &g, Ctx &c) {
           double v = T.alpha * s;
           if (T.beta != 0.0) v += T.beta * get(c, T.c0, i, j);
           o[(int64_t)i * T.out.ld + j] = v;
+          if (T.flags & TF_MIRROR) ptr(c, T.out2)[(int64_t)j * T.out2.ld + i] = v;
         }
     } else if (T.type == TK_COPY) {
       double *o = ptr(c, T.out);
@@ -197,10 +218,12 @@ extern "C" {
 
 // kind: 0 pobtaf, 1 pobtasi, 2 selinv.  Returns 0 on success; *info as serinv.
 int dag_run_sequential(int kind, int64_t n, int64_t b, int64_t a, double *diag, double *lower, double *arrow,
-                       double *tip, double *logdet, int *info, int grid, int update_group, int64_t *ntasks) {
+                       double *tip, double *logdet, int *info, int grid, int update_group, int64_t *ntasks,
+                       int si_split) {
   BuildOptions opt;
   opt.grid = grid;
   opt.update_group = update_group;
+  if (si_split >= 0) opt.si_split = si_split;
   Graph g = build_sequential(kind, n, b, a, opt);
   if (!g.error.empty()) {
     fprintf(stderr, "graph error: %s\n", g.error.c_str());

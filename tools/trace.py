@@ -74,6 +74,9 @@ def main():
                 print(f"    phase {names[k]:12s} {np.mean((cur - prev)[ok])/1e3:8.2f} us")
                 prev = np.where(ok, cur, prev)
 
+    pot_sms = set(sm[typ == 2].tolist())
+    shared = int(((typ == 1) & np.isin(sm, list(pot_sms))).sum())
+    print(f"  POTRF ran on SMs {sorted(pot_sms)[:8]}; GEMM tasks on those SMs: {shared}")
     # timeline utilisation in 10 buckets
     nb = 20
     edges = np.linspace(0, span, nb + 1)
