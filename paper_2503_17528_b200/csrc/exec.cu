@@ -560,13 +560,16 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
 #pragma unroll
           for (int t = 0; t < 4; ++t) cn[rg + 16 * t] = av[t];
         }
-        if (tid == 0) {
-          rsv[c0 + q] = rs;
-          dv[c0 + q] = d;
-          if (!(d > 0.0)) atomicMin(&s_bad, c0 + q);
-        }
         __syncthreads();
       }
+      // the pivot d_q is the untouched diagonal element held by thread (jj = q, rg = q)
+      if (rg == jj && jj < ncol) {
+        const double d = av[0];
+        rsv[c0 + jj] = rsqrt(d);
+        dv[c0 + jj] = d;
+        if (!(d > 0.0)) atomicMin(&s_bad, c0 + jj);
+      }
+      __syncthreads();
       // (3) scale the block's columns: L[i][k] = A[i][k] / sqrt(d_k) (i > k), sqrt(d_k) on the diagonal
       {
         const int k = c0 + jj;
@@ -721,17 +724,35 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
 }
 
 __device__ void run_reduce(const Params &p, const Task &T) {
+  // out = beta * C0 + alpha * sum_{j < cnt} P_j, fixed order j = 0..cnt-1; element pairs
   const double *src = lptr(p, T.r);
   const double *c0 = T.beta != 0.0 ? lptr(p, T.c0) : nullptr;
   double *o = lptr(p, T.out);
-  for (int idx = threadIdx.x; idx < T.m * T.n; idx += NT) {
-    int r = idx / T.n, c = idx - r * T.n;
-    double s = 0.0;
-    for (int j = 0; j < T.aux0; ++j) s += __ldcg(src + T.aux2 * j + (int64_t)r * T.r.ld + c);
-    double v = T.alpha * s;
-    if (c0) v += T.beta * __ldcg(c0 + (int64_t)r * T.c0.ld + c);
-    o[(int64_t)r * T.out.ld + c] = v;
-    if (T.flags & TF_MIRROR) lptr(p, T.out2)[(int64_t)c * T.out2.ld + r] = v;
+  const int n2 = (T.n + 1) >> 1;
+  for (int idx = threadIdx.x; idx < T.m * n2; idx += NT) {
+    const int r = idx / n2, c = 2 * (idx - r * n2);
+    const bool two = c + 1 < T.n;
+    double s0 = 0.0, s1 = 0.0;
+    const double *sp = src + (int64_t)r * T.r.ld + c;
+#pragma unroll 4
+    for (int j = 0; j < T.aux0; ++j) {
+      const double *q = sp + T.aux2 * j;
+      s0 += __ldcg(q);
+      if (two) s1 += __ldcg(q + 1);
+    }
+    double v0 = T.alpha * s0, v1 = T.alpha * s1;
+    if (c0) {
+      v0 += T.beta * __ldcg(c0 + (int64_t)r * T.c0.ld + c);
+      if (two) v1 += T.beta * __ldcg(c0 + (int64_t)r * T.c0.ld + c + 1);
+    }
+    double *op = o + (int64_t)r * T.out.ld + c;
+    op[0] = v0;
+    if (two) op[1] = v1;
+    if (T.flags & TF_MIRROR) {
+      double *o2 = lptr(p, T.out2);
+      o2[(int64_t)c * T.out2.ld + r] = v0;
+      if (two) o2[(int64_t)(c + 1) * T.out2.ld + r] = v1;
+    }
   }
 }
 

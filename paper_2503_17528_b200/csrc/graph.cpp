@@ -64,13 +64,16 @@ double gemm_flops(int m, int n, const std::vector<Seg> &segs) {
 }
 
 // Scheduler cost model (ns) for one CTA of a 2-CTA/SM persistent grid.
+// Calibrated on B200 task traces (tools/trace.py): bulk GEMM ~85 GFLOP/s per CTA with
+// two CTAs per SM, POTRF tile task ~21 us, REDUCE ~10 us.
 double task_cost(const RawTask &rt) {
-  const double ns_per_flop = 1.0 / 110.0;
+  const double ns_per_flop = 1.0 / 85.0;
   switch (rt.t.type) {
-    case TK_POTRF: return 5000.0 + rt.flops * ns_per_flop;
-    case TK_TRTRI: return 2500.0;
-    case TK_GEMM: return 900.0 + rt.flops * ns_per_flop;
-    default: return 700.0;
+    case TK_POTRF: return 19000.0 + rt.flops * ns_per_flop * 0.5;
+    case TK_TRTRI: return 6000.0;
+    case TK_GEMM: return 2500.0 + rt.flops * ns_per_flop;
+    case TK_REDUCE: return 6000.0;
+    default: return 2000.0;
   }
 }
 
