@@ -205,7 +205,7 @@ int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_
 /* Tracing: while d_trace != NULL, every launch whose graph has at most
  * bytes/96 tasks records 4 x uint64 per task (in emission order):
  * {claim time, start time (inputs ready), end time, meta}, times from the GPU
- * global timer (ns); meta = type | smid << 16 | m << 32 | n << 48; followed
+ * global timer (ns); meta = type | smid << 16 | m << 32 | flags << 48; followed
  * by 8 x uint64 per task of phase timestamps (POTRF / TRTRI tasks). 
  * Pass NULL to disable. */
 int serinv_set_trace(serinv_handle_t h, void *d_trace, size_t bytes);

@@ -412,8 +412,26 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem) {
   }
   store_acc(p, T, acc);
   if (T.flags & TF_SYRK3) {
-    // the next diagonal tile of the chain: out3 -= L L^T (L = this result, m x n)
+    // the next diagonal tile of the chain: out3 -= L L^T (L = this result, m x n);
+    // stage the target tile into smem with cp.async while the SYRK runs
     double *Lt = smem;
+    double *Ct = smem + SERINV_TILE * LDT;
+    {
+      const double *g = lptr(p, T.out3);
+      const bool vec = ((T.out3.off | T.out3.ld) & 1) == 0;
+      for (int idx = threadIdx.x; idx < SERINV_TILE * (SERINV_TILE / 2); idx += NT) {
+        const int r = idx >> 5, c = (idx & 31) * 2;
+        const int nv = (r < T.m) ? max(0, min(2, T.m - c)) : 0;
+        const double *src = g + (int64_t)r * T.out3.ld + c;
+        if (vec) {
+          cp_async16(Ct + r * LDT + c, nv ? src : g, nv * 8);
+        } else {
+          Ct[r * LDT + c] = nv > 0 ? __ldcg(src) : 0.0;
+          Ct[r * LDT + c + 1] = nv > 1 ? __ldcg(src + 1) : 0.0;
+        }
+      }
+      cp_commit();
+    }
     acc_to_smem(Lt, acc);
     __syncthreads();
 #pragma unroll
@@ -421,7 +439,18 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     mma_steps(Lt, LDT, 1, Lt, LDT, 1, acc, (T.n + 3) / 4);
-    apply_c0(p, -1.0, 1.0, T.out3, T.m, T.m, acc);
+    cp_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int r, c;
+          frag_rc(mi, ni, h, r, c);
+          acc[mi][ni][h] = Ct[r * LDT + c] - acc[mi][ni][h];
+        }
     store_tile(p, T.out3, T.m, T.m, acc);
     __syncthreads();
   }
@@ -911,7 +940,7 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
         rec[1] = t_start;
         rec[2] = globaltimer();
         rec[3] = (unsigned long long)(unsigned)T.type | ((unsigned long long)smid() << 16) |
-                 ((unsigned long long)(unsigned)T.m << 32) | ((unsigned long long)(unsigned)T.n << 48);
+                 ((unsigned long long)(unsigned)T.m << 32) | ((unsigned long long)(unsigned)T.flags << 48);
       }
     }
   }

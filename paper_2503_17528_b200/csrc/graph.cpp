@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <functional>
 #include <memory>
 #include <queue>
@@ -505,6 +506,7 @@ struct Builder {
         flush_queue = 0;
         if (cx.opt.critical_queues) {
           if (cx.opt.split_chain && first_trsm == 0 && ri == 0) rt.queue = P.queue2;
+          else if (cx.opt.split_chain && first_trsm == 0 && ri == 1 && cx.opt.rts1_chain) rt.queue = P.queue2;
           else if (cx.opt.split_chain && first_trsm == 0 && ri == 1 && cx.opt.urgent_ctas > 0) rt.queue = URGENT_QUEUE;
           else if (ri == first_trsm && first_trsm == 1) rt.queue = P.queue;
         }
@@ -1310,6 +1312,33 @@ Graph build_sequential(int kind, int64_t n, int64_t b, int64_t a, const BuildOpt
   if (g.error.empty() && g.ws_doubles * 8 > sequential_ws_bytes(kind, n, b, a, opt))
     g.error = "workspace accounting mismatch";
   return g;
+}
+
+void BuildOptions::apply_env() {
+  const char *e = getenv("SERINV_OPT");
+  if (!e) return;
+  std::string s(e);
+  size_t i = 0;
+  while (i < s.size()) {
+    size_t j = s.find(',', i);
+    if (j == std::string::npos) j = s.size();
+    std::string kv = s.substr(i, j - i);
+    size_t eq = kv.find('=');
+    if (eq != std::string::npos) {
+      std::string k = kv.substr(0, eq);
+      long v = strtol(kv.c_str() + eq + 1, nullptr, 10);
+      if (k == "update_group") update_group = (int)v;
+      else if (k == "critical_queues") critical_queues = v != 0;
+      else if (k == "fuse_trsm") fuse_trsm = v != 0;
+      else if (k == "fuse_trsm3") fuse_trsm3 = v != 0;
+      else if (k == "split_chain") split_chain = v != 0;
+      else if (k == "chain_syrk") chain_syrk = v != 0;
+      else if (k == "urgent_ctas") urgent_ctas = (int)v;
+      else if (k == "si_split") si_split = (int)v;
+      else if (k == "rts1_chain") rts1_chain = v != 0;
+    }
+    i = j + 1;
+  }
 }
 
 bool plan_partitions(int64_t n, int P, double r, std::vector<int64_t> &starts) {

@@ -83,6 +83,9 @@ struct BuildOptions {
   bool chain_syrk = true;       // the sub-diagonal TRSM also applies its SYRK to the next diagonal tile
   int urgent_ctas = 0;          // CTAs serving the near-critical queue (0: no urgent queue)
   int si_split = 320;           // K per partial GEMM of the Takahashi tile tasks (0 = no split)
+  bool rts1_chain = false;      // the second sub-diagonal TRSM also on the chain's TRSM queue
+  // overrides from the environment (SERINV_OPT="key=value,..."), for tuning runs
+  void apply_env();
 };
 
 // Sequential problems (whole matrix).  kind: 0 = pobtaf, 1 = pobtasi, 2 = selinv.

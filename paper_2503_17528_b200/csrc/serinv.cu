@@ -115,6 +115,7 @@ int get_graph(serinv_handle_t h, const GKey &key, DevGraph **out) {
   int64_t n = std::get<1>(key), b = std::get<2>(key), a = std::get<3>(key);
   BuildOptions opt;
   opt.grid = h->grid;
+  opt.apply_env();
   std::unique_ptr<DevGraph> dg(new DevGraph());
   if (kind <= 2) {
     dg->g = build_sequential(kind, n, b, a, opt);

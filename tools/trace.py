@@ -10,7 +10,7 @@ import btagen
 import paper_2503_17528_b200 as sb
 from paper_2503_17528_b200 import _lib
 
-NAMES = {1: "GEMM", 2: "POTRF", 3: "TRTRI", 4: "REDUCE", 5: "COPY", 6: "LOGDET"}
+NAMES = {1: "GEMM", 2: "POTRF", 3: "TRTRI", 4: "REDUCE", 5: "COPY", 6: "LOGDET", 11: "CHAIN_TS", 12: "TRSM", 13: "GEMM_MIR"}
 
 
 def main():
@@ -47,7 +47,13 @@ def main():
     claim, start, end, meta = tr[:, 0], tr[:, 1], tr[:, 2], tr[:, 3]
     t0 = claim.min()
     claim, start, end = claim - t0, start - t0, end - t0
-    typ = meta & 0xFFFF; sm = (meta >> 16) & 0xFFFF; m = (meta >> 32) & 0xFFFF; nn = (meta >> 48) & 0xFFFF
+    typ = meta & 0xFFFF; sm = (meta >> 16) & 0xFFFF; m = (meta >> 32) & 0xFFFF; fl = (meta >> 48) & 0xFFFF
+    nn = fl
+    # split GEMM by role: TRSM (post-multiply), chain TRSM+SYRK, mirrored (X_ii), other
+    typ = typ.copy()
+    typ[(typ == 1) & ((fl & 256) != 0)] = 11   # chain TRSM + SYRK
+    typ[(typ == 1) & ((fl & 2) != 0)] = 12     # TRSM / W-post
+    typ[(typ == 1) & ((fl & 1) != 0)] = 13     # mirrored X_ii
     span = end.max()
     print(f"tasks {T} makespan {span/1e6:.3f} ms  grid {st['grid']}  GF {st['flops']/1e9:.1f}")
     busy = (end - start).sum(); waited = (start - claim).sum()
@@ -75,7 +81,7 @@ def main():
                 prev = np.where(ok, cur, prev)
 
     pot_sms = set(sm[typ == 2].tolist())
-    shared = int(((typ == 1) & np.isin(sm, list(pot_sms))).sum())
+    shared = int(((typ != 2) & np.isin(sm, list(pot_sms))).sum())
     print(f"  POTRF ran on SMs {sorted(pot_sms)[:8]}; GEMM tasks on those SMs: {shared}")
     # timeline utilisation in 10 buckets
     nb = 20
