@@ -193,11 +193,10 @@ def main():
         if world > 1:
             dist.barrier()
 
-    # ---- inputs resident in HBM (pristine copy restored between steps, untimed)
+    # ---- inputs resident in HBM (pristine copy restored between steps, untimed); the
+    # generator's torch twin builds G1 directly in HBM, bit-identical to btagen.g1
     if world == 1:
-        A = btagen.g1(0, n, b, a)
-        host = {k: torch.from_numpy(A[k]) for k in ("diag", "lower", "arrow", "tip")}
-        pristine = {k: v.cuda() for k, v in host.items()}
+        pristine = btagen.g1_torch(0, n, b, a, device=f"cuda:{local}")
         work = {k: v.clone() for k, v in pristine.items()}
 
         def step(info=None, logdet=None):
@@ -205,11 +204,11 @@ def main():
                              check=False, info=info, logdet=logdet)
     else:
         from paper_2503_17528_b200 import distributed as sd
-        A = btagen.g1(0, n, b, a)
         parts = sb.plan(n, world, args.r)
         s, e = parts[rank]
-        host = sd.local_blocks(A, s, e, last=(rank == world - 1))
-        pristine = {k: torch.from_numpy(v).cuda() for k, v in host.items()}
+        pristine = btagen.g1_torch(0, n, b, a, device=f"cuda:{local}", start=s, end=e)
+        if pristine["lower"].shape[0] == 0:
+            pristine["lower"] = torch.zeros((1, b, b), dtype=torch.float64, device=f"cuda:{local}")
         work = {k: v.clone() for k, v in pristine.items()}
         ctx = sd.DistContext(h, world, rank, n, s, e - s, b, a, device=local)
 
@@ -225,7 +224,7 @@ def main():
         restore()
         step()
     torch.cuda.synchronize()
-    info = h.scalars()[0]
+    info = h.scalars()[0] if world == 1 else ctx.info
     if int(info.item()) != 0:
         raise SystemExit(f"factorisation failed: info={int(info.item())}")
 
@@ -256,8 +255,8 @@ def main():
     # ---- end to end through the public API with host buffers (pinned H2D, D2H of X + logdet)
     e2e = None
     if not args.no_e2e and world == 1:
-        pinned = {k: v.pin_memory() for k, v in host.items()}
-        out = {k: torch.empty_like(v).pin_memory() for k, v in host.items()}
+        pinned = {k: v.cpu().pin_memory() for k, v in pristine.items()}
+        out = {k: torch.empty_like(v).pin_memory() for k, v in pinned.items()}
         ld_host = torch.empty(1, dtype=torch.float64).pin_memory()
         h2d = sum(v.numel() * 8 for v in pinned.values())
         d2h = h2d + 8
@@ -267,11 +266,8 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for k in work:
-                work[k].copy_(pinned[k], non_blocking=True)
-            step()
-            for k in work:
-                out[k].copy_(work[k], non_blocking=True)
+            # public API with host buffers: H2D / D2H stream with the computation
+            sb.selinv_host(pinned, work, out, handle=h, check=False)
             ld_host.copy_(h.scalars()[1], non_blocking=True)
             e1.record(stream)
             torch.cuda.synchronize()

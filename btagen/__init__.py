@@ -220,3 +220,98 @@ def generate(kind: str, seed: int, n: int, b: int, a: int, **kw) -> BTA:
     if kind == "g2k":
         return g2k(seed, n, b, a, **kw)
     raise ValueError(f"unknown generator {kind!r}")
+
+
+# --------------------------------------------------------------------------- device twin
+# The same counter-based recipe in torch int64 arithmetic (wrapping multiply,
+# logical shifts by masking), so large inputs can be generated directly in HBM.
+# Bit-identical to the numpy path (tests/test_generators.py checks it on CPU).
+def _t_consts():
+    def s64(x):
+        x &= 0xFFFFFFFFFFFFFFFF
+        return x - (1 << 64) if x >= (1 << 63) else x
+    return s64(0x9E3779B97F4A7C15), s64(0xBF58476D1CE4E5B9), s64(0x94D049BB133111EB)
+
+
+def _t_shr(x, k):
+    return (x >> k) & ((1 << (64 - k)) - 1)
+
+
+def _t_mix(z):
+    _, m1, m2 = _t_consts()
+    z = (z ^ _t_shr(z, 30)) * m1
+    z = (z ^ _t_shr(z, 27)) * m2
+    return z ^ _t_shr(z, 31)
+
+
+def _t_seedkey(seed, stream):
+    import torch
+    gold, _, m2 = _t_consts()
+    s = torch.tensor([seed & 0x7FFFFFFFFFFFFFFF], dtype=torch.int64)
+    s = s * gold + stream * m2
+    return int(_t_mix(s + gold)[0])
+
+
+def _t_u_block(seed, stream, r0, c0, nr, nc, device):
+    import torch
+    gold, _, _ = _t_consts()
+    r = torch.arange(r0, r0 + nr, dtype=torch.int64, device=device)[:, None]
+    c = torch.arange(c0, c0 + nc, dtype=torch.int64, device=device)[None, :]
+    lo = torch.minimum(r, c)
+    hi = torch.maximum(r, c)
+    key = ((hi << 32) | lo) ^ _t_seedkey(seed, stream)
+    h = _t_mix(key + gold)
+    return _t_shr(h, 40).to(torch.float64) * _SCALE - 1.0
+
+
+def g1_torch(seed: int, n: int, b: int, a: int, device="cuda", start: int = 0, end: int | None = None):
+    """G1 generated with torch on `device` (dict of tensors, C-ABI layout);
+    bit-identical to g1(seed, n, b, a).  With a block range [start, end) it
+    returns the rank-local slice used by the distributed path: diag/arrow
+    [end-start], lower [end-start] (the coupling to the next rank included) or
+    [end-start-1] on the last rank, and the (replicated) tip.  Seeds < 2^63."""
+    import torch
+    end = n if end is None else end
+    cnt = end - start
+    last = end == n
+    nl = cnt - 1 if last else cnt
+    out = {"diag": torch.empty((cnt, b, b), dtype=torch.float64, device=device),
+           "lower": torch.empty((max(nl, 0), b, b), dtype=torch.float64, device=device),
+           "arrow": torch.empty((cnt, a, b), dtype=torch.float64, device=device),
+           "tip": torch.empty((a, a), dtype=torch.float64, device=device)}
+    N0 = n * b
+    rowsum = torch.zeros(cnt * b, dtype=torch.float64, device=device)
+    eye = torch.eye(b, dtype=torch.bool, device=device)
+    for i in range(max(0, start - 1), end):
+        if i >= start:
+            D = _t_u_block(seed, S_G1, i * b, i * b, b, b, device)
+            D.masked_fill_(eye, 0.0)
+            out["diag"][i - start] = D
+            rowsum[(i - start) * b:(i - start + 1) * b] += D.abs().sum(dim=1)
+        if i + 1 < n:
+            Lw = _t_u_block(seed, S_G1, (i + 1) * b, i * b, b, b, device)
+            if i >= start and i - start < nl:
+                out["lower"][i - start] = Lw
+            if start <= i + 1 < end:
+                rowsum[(i + 1 - start) * b:(i + 2 - start) * b] += Lw.abs().sum(dim=1)
+            if i >= start:
+                rowsum[(i - start) * b:(i - start + 1) * b] += Lw.abs().sum(dim=0)
+    tipsum = torch.zeros(a, dtype=torch.float64, device=device)
+    if a:
+        for i in range(n):  # the tip's diagonal needs every arrow block
+            W = _t_u_block(seed, S_G1, N0, i * b, a, b, device)
+            if start <= i < end:
+                out["arrow"][i - start] = W
+                rowsum[(i - start) * b:(i - start + 1) * b] += W.abs().sum(dim=0)
+            tipsum += W.abs().sum(dim=1)
+    idx = torch.arange(b, device=device)
+    for i in range(cnt):
+        out["diag"][i][idx, idx] = 1.0 + rowsum[i * b:(i + 1) * b]
+    if a:
+        Tt = _t_u_block(seed, S_G1, N0, N0, a, a, device)
+        Tt.masked_fill_(torch.eye(a, dtype=torch.bool, device=device), 0.0)
+        tipsum += Tt.abs().sum(dim=1)
+        ia = torch.arange(a, device=device)
+        Tt[ia, ia] = 1.0 + tipsum
+        out["tip"].copy_(Tt)
+    return out

@@ -121,6 +121,20 @@ int serinv_pobtasi(serinv_handle_t h, const serinv_bta_t *L, void *d_ws, size_t 
 int serinv_selinv(serinv_handle_t h, const serinv_bta_t *A, void *d_ws, size_t ws_bytes,
                   int *d_info, double *d_logdet, void *stream);
 
+/*
+ * serinv_selinv with HOST buffers and streaming IO: A_host (pinned host memory,
+ * same layout) is copied into the device buffers A_dev in chunks of blocks on an
+ * internal copy stream while the factorisation runs (each chunk bumps an arrival
+ * counter the task graph waits on, via cuStreamWriteValue32); the selected
+ * inverse is copied back to X_host (pinned; may equal A_host) node by node as
+ * soon as the backward pass finalises it (cuStreamWaitValue32 on the node's
+ * counter).  A_dev is overwritten by X.  `stream` is joined with both copy
+ * streams before the call's work completes on it.  Workspace: serinv_selinv_ws.
+ */
+int serinv_selinv_host(serinv_handle_t h, const serinv_bta_t *A_host, const serinv_bta_t *X_host,
+                       const serinv_bta_t *A_dev, void *d_ws, size_t ws_bytes, int *d_info, double *d_logdet,
+                       void *stream);
+
 /* ------------------------------------------------------------------------- */
 /* Partitioned method (Sec. 3, Alg. 3-6).                 */
 /* ------------------------------------------------------------------------- */

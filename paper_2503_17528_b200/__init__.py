@@ -20,7 +20,7 @@ import math
 from . import _lib
 from ._lib import BTA, GraphStats, Part
 
-__all__ = ["Handle", "pobtaf", "pobtasi", "selinv", "pselinv", "plan", "version",
+__all__ = ["Handle", "pobtaf", "pobtasi", "selinv", "selinv_host", "pselinv", "plan", "version",
            "NotPositiveDefinite", "SerinvError", "ppobtaf", "ppobtasi", "exchange_bytes",
            "graph_stats", "default_handle"]
 
@@ -185,6 +185,44 @@ def pobtasi(diag, lower, arrow, tip, *, handle: Handle | None = None, check: boo
 def selinv(diag, lower, arrow, tip, *, handle: Handle | None = None, check: bool = True, info=None, logdet=None):
     """In-place POBTAF + POBTASI as one task graph: A -> X.  Returns log det A."""
     return _run("selinv", diag, lower, arrow, tip, handle, check, info, logdet)
+
+
+def _bta_host(T, n, b, a):
+    import torch
+    for k in ("diag", "lower", "arrow", "tip"):
+        t = T.get(k)
+        if t is None:
+            continue
+        if not isinstance(t, torch.Tensor) or t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+            raise TypeError(f"host {k} must be a contiguous float64 CPU tensor (pinned for overlap)")
+
+    def ptr(t):
+        return t.data_ptr() if (t is not None and t.numel() > 0) else None
+    return BTA(n, b, a, ptr(T.get("diag")), ptr(T.get("lower")), ptr(T.get("arrow")), ptr(T.get("tip")))
+
+
+def selinv_host(A_host, D, X_host=None, *, handle: Handle | None = None, check: bool = True, info=None,
+                logdet=None):
+    """POBTAF + POBTASI from HOST buffers with streaming IO (serinv_selinv_host): the
+    H2D copy of A_host (pinned CPU tensors) into the device work buffers D overlaps
+    the factorisation, and X is copied back into X_host (default: A_host) node by
+    node while the inversion runs.  Returns log det A (check=True syncs)."""
+    L = _lib.lib()
+    h = handle or default_handle(D["diag"].device.index)
+    Ad = _bta(D["diag"], D.get("lower"), D.get("arrow"), D.get("tip"))
+    n, b, a = Ad.n, Ad.b, Ad.a
+    Ah = _bta_host(A_host, n, b, a)
+    Xh = _bta_host(X_host if X_host is not None else A_host, n, b, a)
+    nb = ctypes.c_size_t(0)
+    _check(L.serinv_selinv_ws(n, b, a, ctypes.byref(nb)), "selinv_ws")
+    ws = h.workspace(nb.value)
+    si, sl = h.scalars()
+    info = si if info is None else info
+    logdet = sl if logdet is None else logdet
+    rc = L.serinv_selinv_host(h._h, ctypes.byref(Ah), ctypes.byref(Xh), ctypes.byref(Ad), ws.data_ptr(), ws.numel(),
+                              info.data_ptr(), logdet.data_ptr(), _stream())
+    _check(rc, "selinv_host")
+    return _finish(h, info, logdet, check, b, n)
 
 
 def plan(n: int, P: int, r: float = 1.0):

@@ -63,6 +63,8 @@ def lib():
                                   c_p, c_p, c_p, c_p]
     L.serinv_graph_stats.argtypes = [c_p, ctypes.c_int, c_i64, c_i64, c_i64, ctypes.c_int,
                                      ctypes.c_double, ctypes.POINTER(GraphStats)]
+    L.serinv_selinv_host.argtypes = [c_p, ctypes.POINTER(BTA), ctypes.POINTER(BTA), ctypes.POINTER(BTA), c_p,
+                                     ctypes.c_size_t, c_p, c_p, c_p]
     L.serinv_set_trace.argtypes = [c_p, c_p, ctypes.c_size_t]
     L.serinv_last_launches.argtypes = [c_p, ctypes.POINTER(ctypes.c_int)]
     _lib = L
@@ -74,5 +76,5 @@ EXPORTED = [
     "serinv_pobtaf_ws", "serinv_pobtasi_ws", "serinv_selinv_ws", "serinv_prepare",
     "serinv_pobtaf", "serinv_pobtasi", "serinv_selinv", "serinv_plan",
     "serinv_pselinv_ws", "serinv_pselinv", "serinv_exchange_bytes", "serinv_ppobtaf_ws",
-    "serinv_ppobtaf", "serinv_ppobtasi", "serinv_graph_stats", "serinv_last_launches", "serinv_set_trace",
+    "serinv_ppobtaf", "serinv_ppobtasi", "serinv_graph_stats", "serinv_last_launches", "serinv_set_trace", "serinv_selinv_host",
 ]

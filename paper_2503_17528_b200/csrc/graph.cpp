@@ -52,6 +52,7 @@ struct RawTask {
   std::vector<Seg> segs;
   std::vector<int32_t> waits;  // counters (target = #producers, fixed at finalize)
   std::vector<int32_t> late;   // waits checked late (TF_TRSM3 inputs)
+  std::vector<Wait> ext;       // waits on EXTERNAL counters (stream-written), explicit targets
   std::vector<int32_t> sigs;   // counters signalled (own counter first)
   double cost = 0.0;           // ns (scheduler model)
   double flops = 0.0;
@@ -97,8 +98,18 @@ struct Ctx {
   int64_t slot_region = 0, slot_cap = 0, slot_count = 0;
   std::map<std::tuple<int32_t, int64_t, int, int>, int32_t> xrc;  // final-X row/col tile counters by location
   std::vector<int32_t> potrf_ctrs;                                  // every factor-done counter (LOGDET waits)
+  std::vector<Wait> ext_default;     // external waits added to every task emitted while set
+  std::vector<std::pair<int32_t, int>> fin;  // streaming IO: per node, counter of its final-X tasks
+  int32_t arr_ctr = -1;                      // streaming IO: blocks-arrived counter (external)
+  std::vector<char> is_ext;          // counter written by a stream (no producer task)
 
   int32_t new_ctr() { return nctr++; }
+  int32_t new_ext_ctr() {
+    int32_t c = nctr++;
+    if ((int)is_ext.size() < nctr) is_ext.resize(nctr, 0);
+    is_ext[c] = 1;
+    return c;
+  }
   int64_t alloc(int64_t doubles) {
     int64_t o = ws_top;
     ws_top += (std::max<int64_t>(doubles, 1) + 31) / 32 * 32;
@@ -139,6 +150,7 @@ struct Ctx {
         if (!std::binary_search(rt.waits.begin(), rt.waits.end(), w)) lt.push_back(w);
       rt.late.swap(lt);
     }
+    for (const Wait &w : ext_default) rt.ext.push_back(w);
     int id = (int)tasks.size();
     int32_t o = new_ctr();
     rt.sigs.insert(rt.sigs.begin(), o);
@@ -743,6 +755,8 @@ struct Builder {
   }
 
   // ================================================================ Takahashi
+  int32_t fin_ctr = -1;  // streaming IO: counter signalled by every final-X task of the node
+
   void invert_node(int X) {
     int nt = ntiles(P.size[X]);
     int32_t pre = gctr(predone, X);
@@ -769,6 +783,7 @@ struct Builder {
           rt.waits.push_back(pre);  // WAR: L_{Y,X} consumed by the precompute
           rt.sigs.push_back(XR(Y, X, q));
           rt.sigs.push_back(XC(Y, X, c));
+          if (fin_ctr >= 0) rt.sigs.push_back(fin_ctr);
           emit_split(std::move(rt), tile++);
         }
     }
@@ -801,6 +816,7 @@ struct Builder {
           rt.sigs.push_back(XR(X, X, c));
           rt.sigs.push_back(XC(X, X, r));
         }
+        if (fin_ctr >= 0) rt.sigs.push_back(fin_ctr);
         emit_split(std::move(rt), tile++);
       }
     ++split_step;
@@ -835,6 +851,7 @@ Graph Ctx::finalize() {
         g.error = "counter with no producer";
         return g;
       }
+  (void)is_ext;
   std::vector<int32_t> tdeg(N), cdeg(nprod);
   for (int i = 0; i < N; ++i) tdeg[i] = (int32_t)tasks[i].waits.size();
   std::vector<int> topo;
@@ -915,9 +932,12 @@ Graph Ctx::finalize() {
     task.nseg = (int32_t)rt.segs.size();
     for (auto &s : rt.segs) g.segs.push_back(s);
     task.wait0 = (int32_t)g.waits.size();
-    task.nwait = (int32_t)rt.waits.size();  // early waits first, the last nlate are late
+    task.nwait = (int32_t)(rt.waits.size() + rt.ext.size());  // early (+ external) waits, then nlate late
     task.nlate = (int32_t)rt.late.size();
-    for (int32_t w : rt.waits) g.waits.push_back(Wait{w, nprod[w]});
+    const size_t nearly = rt.waits.size() - rt.late.size();
+    for (size_t k = 0; k < nearly; ++k) g.waits.push_back(Wait{rt.waits[k], nprod[rt.waits[k]]});
+    for (const Wait &w : rt.ext) g.waits.push_back(w);
+    for (size_t k = nearly; k < rt.waits.size(); ++k) g.waits.push_back(Wait{rt.waits[k], nprod[rt.waits[k]]});
     task.sig0 = (int32_t)g.sigs.size();
     task.nsig = (int32_t)rt.sigs.size();
     for (int32_t s : rt.sigs) g.sigs.push_back(s);
@@ -950,6 +970,8 @@ Graph Ctx::finalize() {
   g.grid = opt.grid;
   g.ws_doubles = ws_top;
   g.nslots = slot_count;
+  for (auto &f : fin) g.fin.push_back(Wait{f.first, nprod[f.first]});
+  g.arr_ctr = arr_ctr;
   return g;
 }
 
@@ -1059,7 +1081,7 @@ void middle_problem(Problem &P, int64_t ls, int64_t cnt, int64_t b, int64_t a, L
 int64_t slot_bound(int64_t nblocks, int64_t b, int64_t a) { return nblocks * ntiles(b) + ntiles(a) + 8; }
 
 Graph build_seq_ctx(Ctx &cx, int kind, int64_t n, int64_t b, int64_t a) {
-  bool fact = kind != 1, inv = kind != 0;
+  bool fact = kind != 1, inv = kind != 0;  // kinds 2 and 6 (selinv, streaming IO) do both
   cx.slot_cap = slot_bound(n, b, a);
   cx.slot_region = cx.alloc(cx.slot_cap);
   Problem P;
@@ -1072,13 +1094,26 @@ Graph build_seq_ctx(Ctx &cx, int kind, int64_t n, int64_t b, int64_t a) {
   Builder bld(cx, P);
   bld.allocate(inv);
   int nn = (int)P.size.size();
+  const bool stream_io = kind == 6;
+  if (stream_io) cx.arr_ctr = cx.new_ext_ctr();
   if (fact) {
-    for (int X = 0; X < nn; ++X) bld.factor_node(X);
+    for (int X = 0; X < nn; ++X) {
+      // streaming IO: the column of node X reads blocks X and X+1 (counted in blocks arrived)
+      if (stream_io) cx.ext_default = {Wait{cx.arr_ctr, (int32_t)std::min<int64_t>(X + 2, n)}};
+      bld.factor_node(X);
+    }
+    cx.ext_default.clear();
     cx.logdet(Loc{BUF_LOGDET, 0, 0}, 0, cx.slot_count, Loc{BUF_WS, 0, 0}, 0, 0, {});
   }
   if (inv) {
     for (int X = 0; X < nn; ++X) bld.precompute_node(X, fact);
-    for (int X = nn - 1; X >= 0; --X) bld.invert_node(X);
+    for (int X = nn - 1; X >= 0; --X) {
+      if (stream_io) {
+        bld.fin_ctr = cx.new_ctr();
+        cx.fin.push_back({bld.fin_ctr, X});
+      }
+      bld.invert_node(X);
+    }
   }
   return cx.finalize();
 }
@@ -1292,7 +1327,7 @@ int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a, const Bui
   // replays the allocations of build_seq_ctx (no tasks are built)
   Ctx cx;
   cx.opt = opt;
-  bool inv = kind != 0;
+  bool inv = kind != 0;  // 1, 2, 6
   cx.slot_cap = slot_bound(n, b, a);
   cx.slot_region = cx.alloc(cx.slot_cap);
   Problem P;

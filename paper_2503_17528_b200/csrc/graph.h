@@ -40,6 +40,11 @@ struct Graph {
   // claim queues: queue 0 = bulk, queues 1..nq-1 = critical chains (one CTA each,
   // alone on its SM).  qlist holds task indices, queue q = qlist[qoff[q] .. qoff[q+1]).
   std::vector<int32_t> qlist, qoff;
+  // streaming IO (kind 6): blocks-arrived counter written by the H2D stream, and per
+  // node (fin[k].target = #producers) the counter of its final-X tasks, in the order
+  // the nodes finish (tip first, then blocks n-1 .. 0)
+  int32_t arr_ctr = -1;
+  std::vector<Wait> fin;
   int ncrit = 0;     // queues 1..ncrit: one CTA each, alone on its SM
   int nurgent = 0;   // queue ncrit+1 (if any): served by nurgent CTAs (near-critical tasks)
   std::string error;         // non-empty if building failed
@@ -88,7 +93,8 @@ struct BuildOptions {
   void apply_env();
 };
 
-// Sequential problems (whole matrix).  kind: 0 = pobtaf, 1 = pobtasi, 2 = selinv.
+// Sequential problems (whole matrix).  kind: 0 = pobtaf, 1 = pobtasi, 2 = selinv,
+// 6 = selinv with streaming host IO (external arrival counter + per-node final counters).
 Graph build_sequential(int kind, int64_t n, int64_t b, int64_t a, const BuildOptions &opt);
 
 // Workspace bytes for the sequential kinds (doubles region + counters).

@@ -3,11 +3,13 @@
 // Each compute entry point: validate arguments, fetch (or build + upload) the
 // cached task graph for the problem shape, reset its dependency counters, and
 // launch ONE persistent executor kernel (exec.cu) on the caller's stream.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -58,6 +60,8 @@ struct serinv_ctx {
   double *dummy = nullptr;  // logdet sink when the caller passes NULL
   unsigned long long *trace = nullptr;  // optional per-task trace buffer (device)
   size_t trace_cap = 0;                 // records
+  cudaStream_t s_in = nullptr, s_out = nullptr;  // streaming host IO copy streams
+  cudaEvent_t ev_start = nullptr, ev_in = nullptr, ev_out = nullptr;
   std::map<GKey, std::unique_ptr<DevGraph>> cache;
   std::mutex mu;
 };
@@ -104,7 +108,16 @@ int upload(DevGraph &dg, int grid) {
   return SERINV_OK;
 }
 
+int get_graph_impl(serinv_handle_t h, const GKey &key, DevGraph **out);
 int get_graph(serinv_handle_t h, const GKey &key, DevGraph **out) {
+  try {
+    return get_graph_impl(h, key, out);
+  } catch (const std::exception &e) {
+    fprintf(stderr, "serinv: graph build failed: %s\n", e.what());
+    return SERINV_ERR_SHAPE;
+  }
+}
+int get_graph_impl(serinv_handle_t h, const GKey &key, DevGraph **out) {
   std::lock_guard<std::mutex> lk(h->mu);
   auto it = h->cache.find(key);
   if (it != h->cache.end()) {
@@ -117,7 +130,7 @@ int get_graph(serinv_handle_t h, const GKey &key, DevGraph **out) {
   opt.grid = h->grid;
   opt.apply_env();
   std::unique_ptr<DevGraph> dg(new DevGraph());
-  if (kind <= 2) {
+  if (kind <= 2 || kind == 6) {
     dg->g = build_sequential(kind, n, b, a, opt);
   } else if (kind == 3) {
     int P = std::get<4>(key);
@@ -129,6 +142,7 @@ int get_graph(serinv_handle_t h, const GKey &key, DevGraph **out) {
     int P = std::get<4>(key);
     int rank = std::get<6>(key);
     int64_t start = std::get<7>(key), count = std::get<8>(key);
+    if (kind != 4 && kind != 5) return SERINV_ERR_SHAPE;
     dg->g = build_distributed(kind - 4, P, rank, n, start, count, b, a, opt);
   }
   if (!dg->g.error.empty()) {
@@ -142,10 +156,13 @@ int get_graph(serinv_handle_t h, const GKey &key, DevGraph **out) {
   return SERINV_OK;
 }
 
-int launch(serinv_handle_t h, DevGraph &dg, double *bufs[BUF_COUNT], int *d_info, cudaStream_t st) {
-  if (cudaMemsetAsync(dg.ctr, 0, (size_t)dg.nctr_alloc * sizeof(int32_t), st) != cudaSuccess)
-    return SERINV_ERR_CUDA;
-  if (cudaMemsetAsync(d_info, 0, sizeof(int), st) != cudaSuccess) return SERINV_ERR_CUDA;
+int launch(serinv_handle_t h, DevGraph &dg, double *bufs[BUF_COUNT], int *d_info, cudaStream_t st,
+           bool reset = true) {
+  if (reset) {
+    if (cudaMemsetAsync(dg.ctr, 0, (size_t)dg.nctr_alloc * sizeof(int32_t), st) != cudaSuccess)
+      return SERINV_ERR_CUDA;
+    if (cudaMemsetAsync(d_info, 0, sizeof(int), st) != cudaSuccess) return SERINV_ERR_CUDA;
+  }
   dev::Params p;
   p.tasks = dg.d_tasks;
   p.segs = dg.d_segs;
@@ -245,6 +262,11 @@ int serinv_destroy(serinv_handle_t h) {
   cudaDeviceSynchronize();
   h->cache.clear();
   if (h->dummy) cudaFree(h->dummy);
+  if (h->s_in) cudaStreamDestroy(h->s_in);
+  if (h->s_out) cudaStreamDestroy(h->s_out);
+  if (h->ev_start) cudaEventDestroy(h->ev_start);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_out) cudaEventDestroy(h->ev_out);
   delete h;
   return SERINV_OK;
 }
@@ -426,6 +448,124 @@ int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_
   out->flops = dg->g.flops;
   out->grid = h->grid;
   out->tile = SERINV_TILE;
+  return SERINV_OK;
+}
+
+// Driver stream memory operations, resolved through the runtime (no link-time
+// dependency on libcuda, so the library also loads on machines without a GPU).
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_writeValue32 p_writeValue32 = nullptr;
+static PFN_waitValue32 p_waitValue32 = nullptr;
+static bool load_stream_memops() {
+  if (p_writeValue32 && p_waitValue32) return true;
+  void *f1 = nullptr, *f2 = nullptr;
+  cudaDriverEntryPointQueryResult q1, q2;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f1, cudaEnableDefault, &q1) != cudaSuccess ||
+      cudaGetDriverEntryPoint("cuStreamWaitValue32", &f2, cudaEnableDefault, &q2) != cudaSuccess || !f1 || !f2)
+    return false;
+  p_writeValue32 = (PFN_writeValue32)f1;
+  p_waitValue32 = (PFN_waitValue32)f2;
+  return true;
+}
+
+// Streaming host IO: H2D of the input blocks and D2H of the selected inverse
+// overlap the factorisation / inversion.  The H2D stream copies chunks of blocks
+// in order and bumps the graph's arrival counter (cuStreamWriteValue32); the
+// D2H stream waits on each node's final-X counter (cuStreamWaitValue32) and
+// copies the node's blocks back while the kernel works on earlier blocks.
+int serinv_selinv_host(serinv_handle_t h, const serinv_bta_t *A_host, const serinv_bta_t *X_host,
+                       const serinv_bta_t *A_dev, void *d_ws, size_t ws_bytes, int *d_info, double *d_logdet,
+                       void *stream) {
+  if (!h) return SERINV_ERR_HANDLE;
+  int rc = check_bta(A_dev);
+  if (rc) return rc;
+  if (!A_host || !X_host) return -2;
+  if (A_host->n != A_dev->n || A_host->b != A_dev->b || A_host->a != A_dev->a || X_host->n != A_dev->n ||
+      X_host->b != A_dev->b || X_host->a != A_dev->a)
+    return -2;
+  if (!A_host->diag || !X_host->diag || (A_dev->n > 1 && (!A_host->lower || !X_host->lower)) ||
+      (A_dev->a > 0 && (!A_host->arrow || !A_host->tip || !X_host->arrow || !X_host->tip)))
+    return -2;
+  if (!d_info) return -7;
+  if (!d_ws || !aligned16(d_ws)) return SERINV_ERR_WS;
+  if (cudaSetDevice(h->device) != cudaSuccess) return SERINV_ERR_CUDA;
+  if (!load_stream_memops()) return SERINV_ERR_CUDA;
+  DevGraph *dg = nullptr;
+  const int64_t n = A_dev->n, b = A_dev->b, a = A_dev->a;
+  rc = get_graph(h, GKey(6, n, b, a, 1, 0, 0, 0, 0), &dg);
+  if (rc) return rc;
+  if ((int64_t)ws_bytes < dg->g.ws_doubles * 8) return SERINV_ERR_WS;
+  if (!h->s_in) {
+    if (cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming) != cudaSuccess)
+      return SERINV_ERR_CUDA;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(dg->ctr, 0, (size_t)dg->nctr_alloc * sizeof(int32_t), st) != cudaSuccess ||
+      cudaMemsetAsync(d_info, 0, sizeof(int), st) != cudaSuccess || cudaEventRecord(h->ev_start, st) != cudaSuccess)
+    return SERINV_ERR_CUDA;
+  if (cudaStreamWaitEvent(h->s_in, h->ev_start, 0) != cudaSuccess ||
+      cudaStreamWaitEvent(h->s_out, h->ev_start, 0) != cudaSuccess)
+    return SERINV_ERR_CUDA;
+  const size_t bb = (size_t)b * b * 8, ab = (size_t)a * b * 8;
+  // chunks of ~8 MB of blocks
+  const int64_t per_block = (int64_t)(2 * bb + ab);
+  const int64_t chunk = std::max<int64_t>(1, (8ll << 20) / std::max<int64_t>(per_block, 1));
+  // ---- H2D (in order), arrival counter = number of blocks present
+  auto h2d = [&](void *dst, const void *src, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->s_in) : cudaSuccess;
+  };
+  auto d2h = [&](void *dst, const void *src, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->s_out) : cudaSuccess;
+  };
+  CUdeviceptr arr = (CUdeviceptr)(dg->ctr + dg->g.arr_ctr);
+  if (a > 0 && h2d(A_dev->tip, A_host->tip, (size_t)a * a * 8) != cudaSuccess) return SERINV_ERR_CUDA;
+  for (int64_t i0 = 0; i0 < n; i0 += chunk) {
+    const int64_t i1 = std::min(n, i0 + chunk);
+    if (h2d(A_dev->diag + i0 * b * b, A_host->diag + i0 * b * b, (size_t)(i1 - i0) * bb) != cudaSuccess)
+      return SERINV_ERR_CUDA;
+    const int64_t l1 = std::min(i1, n - 1);
+    if (l1 > i0 && h2d(A_dev->lower + i0 * b * b, A_host->lower + i0 * b * b, (size_t)(l1 - i0) * bb) != cudaSuccess)
+      return SERINV_ERR_CUDA;
+    if (a > 0 && h2d(A_dev->arrow + i0 * a * b, A_host->arrow + i0 * a * b, (size_t)(i1 - i0) * ab) != cudaSuccess)
+      return SERINV_ERR_CUDA;
+    if (p_writeValue32((CUstream)h->s_in, arr, (cuuint32_t)i1, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+      return SERINV_ERR_CUDA;
+  }
+  // ---- the kernel (counters already reset on `st`)
+  double *bufs[BUF_COUNT] = {A_dev->diag, A_dev->lower, A_dev->arrow, A_dev->tip, (double *)d_ws, nullptr, nullptr,
+                             d_logdet ? d_logdet : h->dummy};
+  rc = launch(h, *dg, bufs, d_info, st, false);
+  if (rc) return rc;
+  // ---- D2H as nodes finish: fin[] = [tip (if a > 0), block n-1, ..., block 0]
+  auto waitv = [&](const Wait &w) {
+    return p_waitValue32((CUstream)h->s_out, (CUdeviceptr)(dg->ctr + w.ctr), (cuuint32_t)w.target,
+                               CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS;
+  };
+  size_t k = 0;
+  if (a > 0) {
+    if (!waitv(dg->g.fin[k++])) return SERINV_ERR_CUDA;
+    if (d2h(X_host->tip, A_dev->tip, (size_t)a * a * 8) != cudaSuccess) return SERINV_ERR_CUDA;
+  }
+  for (int64_t i1 = n; i1 > 0; i1 -= chunk) {
+    const int64_t i0 = std::max<int64_t>(0, i1 - chunk);
+    for (int64_t i = i1 - 1; i >= i0; --i)
+      if (!waitv(dg->g.fin[k++])) return SERINV_ERR_CUDA;
+    if (d2h(X_host->diag + i0 * b * b, A_dev->diag + i0 * b * b, (size_t)(i1 - i0) * bb) != cudaSuccess)
+      return SERINV_ERR_CUDA;
+    const int64_t l1 = std::min(i1, n - 1);
+    if (l1 > i0 && d2h(X_host->lower + i0 * b * b, A_dev->lower + i0 * b * b, (size_t)(l1 - i0) * bb) != cudaSuccess)
+      return SERINV_ERR_CUDA;
+    if (a > 0 && d2h(X_host->arrow + i0 * a * b, A_dev->arrow + i0 * a * b, (size_t)(i1 - i0) * ab) != cudaSuccess)
+      return SERINV_ERR_CUDA;
+  }
+  if (cudaEventRecord(h->ev_in, h->s_in) != cudaSuccess || cudaEventRecord(h->ev_out, h->s_out) != cudaSuccess ||
+      cudaStreamWaitEvent(st, h->ev_in, 0) != cudaSuccess || cudaStreamWaitEvent(st, h->ev_out, 0) != cudaSuccess)
+    return SERINV_ERR_CUDA;
   return SERINV_OK;
 }
 

@@ -56,3 +56,20 @@ def test_g2_fill_in_decay_is_slow():
 
 def test_bytes():
     assert btagen.bta_bytes(8, 4, 2) == 8 * (8 * 16 + 7 * 16 + 8 * 8 + 4)
+
+
+def test_torch_twin_of_g1_is_bit_identical():
+    import torch
+    for (n, b, a, seed) in [(5, 7, 3, 1), (3, 16, 0, 9), (2, 5, 4, 12345)]:
+        A = btagen.g1(seed, n, b, a)
+        T = btagen.g1_torch(seed, n, b, a, device="cpu")
+        for k in ("diag", "lower", "arrow", "tip"):
+            assert np.array_equal(A[k], T[k].numpy()), k
+        # rank-local slices
+        for (s, e) in [(0, 2), (1, n), (1, 3)] if n > 3 else [(0, n)]:
+            Tl = btagen.g1_torch(seed, n, b, a, device="cpu", start=s, end=e)
+            assert np.array_equal(Tl["diag"].numpy(), A["diag"][s:e])
+            nl = e - s - 1 if e == n else e - s
+            assert np.array_equal(Tl["lower"].numpy(), A["lower"][s:s + nl])
+            assert np.array_equal(Tl["arrow"].numpy(), A["arrow"][s:e])
+            assert np.array_equal(Tl["tip"].numpy(), A["tip"])

@@ -130,3 +130,21 @@ def test_launch_count_is_one_kernel():
     h = sb.default_handle()
     sb.selinv(*args(D), handle=h)
     assert h.last_launches() == 1
+
+
+@pytest.mark.parametrize("n,b,a", [(9, 128, 8), (40, 64, 4), (5, 200, 0), (1, 64, 3)])
+def test_selinv_host_streaming(n, b, a):
+    """serinv_selinv_host: H2D / D2H stream with the computation (arrival / final counters)."""
+    import torch
+    sb = _sb()
+    A = btagen.g2(6, n, b, a)
+    L, X, ld = seq.selinv(A)
+    host = {k: torch.from_numpy(np.ascontiguousarray(A[k])).pin_memory() for k in ("diag", "lower", "arrow", "tip")}
+    out = {k: torch.empty_like(v).pin_memory() for k, v in host.items()}
+    D = {k: torch.empty(v.shape, dtype=torch.float64, device="cuda") for k, v in host.items()}
+    for rep in range(2):
+        ldg = sb.selinv_host(host, D, out)
+        G = {k: v.numpy() for k, v in out.items()}
+        e, where = inv.max_block_err(G, X)
+        assert e <= TOL, (e, where)
+        assert abs(ldg - ld) <= 1e-12 * max(1.0, abs(ld))

@@ -79,6 +79,17 @@ def test_sequential_graphs(n, b, a):
     assert inv.max_block_err(cut(S, X), X)[0] < 1e-12
 
 
+@pytest.mark.parametrize("n,b,a", [(6, 70, 5), (3, 64, 0), (1, 30, 2)])
+def test_streaming_io_graph(n, b, a):
+    # kind 6 (serinv_selinv_host): same results as selinv, all final-X counters complete
+    A0 = btagen.g2(2, n, b, a)
+    L, X, ld = seq.selinv(A0)
+    R, ldr, info = run_seq(6, A0)
+    assert info == 0
+    assert inv.max_block_err(cut(R, X), X)[0] < 1e-12
+    assert abs(ldr - ld) <= 1e-12 * max(1, abs(ld))
+
+
 @pytest.mark.parametrize("ug", [1, 2, 7])
 @pytest.mark.parametrize("grid", [1, 3, 296])
 def test_schedule_options_do_not_change_results(ug, grid):

@@ -30,6 +30,7 @@ inline double opget(Ctx &c, const Loc &l, int trans, int i, int j) {
 
 int run(const Graph &g, Ctx &c) {
   c.ctr.assign(g.nctr, 0);
+  if (g.arr_ctr >= 0) c.ctr[g.arr_ctr] = 1 << 30;  // streaming IO: every block has arrived
   std::vector<double> acc(SERINV_TILE * SERINV_TILE), tmp(SERINV_TILE * SERINV_TILE);
   for (size_t t = 0; t < g.tasks.size(); ++t) {
     const Task &T = g.tasks[t];
@@ -243,6 +244,10 @@ int dag_run_sequential(int kind, int64_t n, int64_t b, int64_t a, double *diag, 
   *info = c.info;
   if (logdet) *logdet = ld;
   if (ntasks) *ntasks = (int64_t)g.tasks.size();
+  // streaming IO: every final-X counter reached its target
+  if (rc == 0)
+    for (const Wait &w : g.fin)
+      if (c.ctr[w.ctr] != w.target) return -5;
   return rc;
 }
 
