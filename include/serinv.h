@@ -224,6 +224,11 @@ int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_
  * Pass NULL to disable. */
 int serinv_set_trace(serinv_handle_t h, void *d_trace, size_t bytes);
 
+/* Diagnostic: `ntasks` independent 64 x 64 tile GEMMs (K = k, in nseg segments)
+ * through the persistent executor; measures the tile engine's throughput.
+ * d_ws needs >= 8 * (2 * 64 * 64 * k + 64^3) bytes. */
+int serinv_bench_gemm(serinv_handle_t h, int ntasks, int k, int nseg, void *d_ws, size_t ws_bytes, void *stream);
+
 /* Number of kernel launches enqueued by the last compute call of this handle. */
 int serinv_last_launches(serinv_handle_t h, int *launches);
 

@@ -65,6 +65,7 @@ def lib():
                                      ctypes.c_double, ctypes.POINTER(GraphStats)]
     L.serinv_selinv_host.argtypes = [c_p, ctypes.POINTER(BTA), ctypes.POINTER(BTA), ctypes.POINTER(BTA), c_p,
                                      ctypes.c_size_t, c_p, c_p, c_p]
+    L.serinv_bench_gemm.argtypes = [c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, ctypes.c_size_t, c_p]
     L.serinv_set_trace.argtypes = [c_p, c_p, ctypes.c_size_t]
     L.serinv_last_launches.argtypes = [c_p, ctypes.POINTER(ctypes.c_int)]
     _lib = L
@@ -76,5 +77,5 @@ EXPORTED = [
     "serinv_pobtaf_ws", "serinv_pobtasi_ws", "serinv_selinv_ws", "serinv_prepare",
     "serinv_pobtaf", "serinv_pobtasi", "serinv_selinv", "serinv_plan",
     "serinv_pselinv_ws", "serinv_pselinv", "serinv_exchange_bytes", "serinv_ppobtaf_ws",
-    "serinv_ppobtaf", "serinv_ppobtasi", "serinv_graph_stats", "serinv_last_launches", "serinv_set_trace", "serinv_selinv_host",
+    "serinv_ppobtaf", "serinv_ppobtasi", "serinv_graph_stats", "serinv_last_launches", "serinv_set_trace", "serinv_selinv_host", "serinv_bench_gemm",
 ]

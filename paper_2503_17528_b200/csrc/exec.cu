@@ -113,6 +113,22 @@ __device__ void record_info(int *info, int v) {
 __device__ __forceinline__ void load_operand(double *s, const double *base, int ld, bool km, int R, int K, int k0,
                                              bool vec) {
   const int tid = threadIdx.x;
+  if (vec && R == SERINV_TILE && k0 + KC <= K) {  // full chunk: no bounds predicates
+    if (!km) {
+#pragma unroll
+      for (int it = 0; it < (SERINV_TILE * (KC / 2)) / NT; ++it) {
+        const int idx = tid + it * NT, r = idx >> 4, kk = (idx & 15) * 2;
+        cp_async16(s + r * LD_MK + kk, base + (int64_t)r * ld + k0 + kk, 16);
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < (KC * (SERINV_TILE / 2)) / NT; ++it) {
+        const int idx = tid + it * NT, kk = idx >> 5, r = (idx & 31) * 2;
+        cp_async16(s + kk * LD_KM + r, base + (int64_t)(k0 + kk) * ld + r, 16);
+      }
+    }
+    return;
+  }
   if (!km) {
 #pragma unroll
     for (int it = 0; it < (SERINV_TILE * (KC / 2)) / NT; ++it) {
@@ -169,6 +185,46 @@ __device__ __forceinline__ void mma_steps(const double *As, int sAr, int sAk, co
       dmma(acc[0][ni], a0, b[ni]);
       dmma(acc[1][ni], a1, b[ni]);
     }
+  }
+}
+
+// mma_steps on the two staged operand layouts with compile-time strides
+// (immediate LDS offsets); a full chunk (KC/4 k-steps) is fully unrolled.
+template <bool AKM, bool BKM>
+__device__ __forceinline__ void mma_chunk(const double *As, const double *Bs, double (&acc)[2][4][2], int ksteps) {
+  constexpr int sAr = AKM ? 1 : LD_MK, sAk = AKM ? LD_KM : 1;
+  constexpr int sBn = BKM ? 1 : LD_MK, sBk = BKM ? LD_KM : 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kq = lane & 3;
+  const double *Ap = As + ((warp >> 1) * 16 + (lane >> 2)) * sAr + kq * sAk;
+  const double *Bp = Bs + ((warp & 1) * 32 + (lane >> 2)) * sBn + kq * sBk;
+  auto step = [&](int ks) {
+    const double a0 = Ap[ks * 4 * sAk], a1 = Ap[8 * sAr + ks * 4 * sAk];
+    double b[4];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = Bp[ni * 8 * sBn + ks * 4 * sBk];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      dmma(acc[0][ni], a0, b[ni]);
+      dmma(acc[1][ni], a1, b[ni]);
+    }
+  };
+  if (ksteps == KC / 4) {
+#pragma unroll
+    for (int ks = 0; ks < KC / 4; ++ks) step(ks);
+  } else {
+    for (int ks = 0; ks < ksteps; ++ks) step(ks);
+  }
+}
+
+__device__ __forceinline__ void mma_chunk_lay(bool akm, bool bkm, const double *As, const double *Bs,
+                                              double (&acc)[2][4][2], int ksteps) {
+  if (akm) {
+    if (bkm) mma_chunk<true, true>(As, Bs, acc, ksteps);
+    else mma_chunk<true, false>(As, Bs, acc, ksteps);
+  } else {
+    if (bkm) mma_chunk<false, true>(As, Bs, acc, ksteps);
+    else mma_chunk<false, false>(As, Bs, acc, ksteps);
   }
 }
 
@@ -238,9 +294,9 @@ __device__ __forceinline__ void gemm_mainloop2(const Params &p, int s0, int ns, 
     int kleft = S.k - ck;
     int ksteps = kleft >= KC ? KC / 4 : (kleft + 3) / 4;
     if (DUAL && inB)
-      mma_steps(As, akm ? 1 : LD_MK, akm ? LD_KM : 1, Bs, bkm ? 1 : LD_MK, bkm ? LD_KM : 1, acc2, ksteps);
+      mma_chunk_lay(akm, bkm, As, Bs, acc2, ksteps);
     else
-      mma_steps(As, akm ? 1 : LD_MK, akm ? LD_KM : 1, Bs, bkm ? 1 : LD_MK, bkm ? LD_KM : 1, acc, ksteps);
+      mma_chunk_lay(akm, bkm, As, Bs, acc, ksteps);
     ck += KC;
     if (ck >= S.k) {
       ck = 0;

@@ -693,16 +693,19 @@ struct Builder {
     return out;
   }
 
-  // emit a Takahashi tile task, split along K into partial GEMMs + a fixed-order REDUCE
-  void emit_split(RawTask &&rt, int tile) {
+  // emit a Takahashi tile task, split along K into partial GEMMs + a fixed-order REDUCE.
+  // wave = number of tile tasks of this dependency wave: split only as much as needed
+  // to give every CTA of the grid ~2 tasks (big waves are not split at all).
+  void emit_split(RawTask &&rt, int tile, int wave) {
     int K = 0;
     for (auto &sg : rt.segs) K += sg.k;
     const int KS = cx.opt.si_split;
-    if (split_base < 0 || KS <= 0 || K < (3 * KS) / 2 || tile >= split_tiles) {
+    const int want = (2 * std::max(1, cx.opt.grid) + wave - 1) / std::max(1, wave);
+    int pieces = std::min({split_pieces, (K + KS - 1) / std::max(1, KS), want});
+    if (split_base < 0 || KS <= 0 || pieces < 2 || tile >= split_tiles) {
       cx.emit(std::move(rt));
       return;
     }
-    int pieces = std::min(split_pieces, (K + KS - 1) / KS);
     int per = (K + pieces - 1) / pieces;
     const int slot = split_step & 1;
     const int64_t tbase = split_base + (((int64_t)slot * split_tiles + tile) * split_pieces) * TILE * TILE;
@@ -762,6 +765,9 @@ struct Builder {
     int32_t pre = gctr(predone, X);
     const auto &R = P.rows[X];
     int tile = 0;
+    int wave1 = 0;
+    for (int Y : R) wave1 += ntiles(P.size[Y]) * nt;
+    const int wave2 = nt * (nt + 1) / 2;
     for (int Y : R) {  // X_{Y,X}(q,c) = -sum_Z X_{Y,Z}(q,:) Lchk(Z,X)(:,c)
       const BlkRef &by = B(Y, X);
       for (int q = 0; q < ntiles(P.size[Y]); ++q)
@@ -784,7 +790,7 @@ struct Builder {
           rt.sigs.push_back(XR(Y, X, q));
           rt.sigs.push_back(XC(Y, X, c));
           if (fin_ctr >= 0) rt.sigs.push_back(fin_ctr);
-          emit_split(std::move(rt), tile++);
+          emit_split(std::move(rt), tile++, wave1);
         }
     }
     // X_{X,X}(r,c) = Lambda(r,c) - sum_Y X_{Y,X}(:,r)^T Lchk(Y,X)(:,c), r >= c, mirrored
@@ -817,7 +823,7 @@ struct Builder {
           rt.sigs.push_back(XC(X, X, r));
         }
         if (fin_ctr >= 0) rt.sigs.push_back(fin_ctr);
-        emit_split(std::move(rt), tile++);
+        emit_split(std::move(rt), tile++, wave2);
       }
     ++split_step;
   }
@@ -1374,6 +1380,31 @@ void BuildOptions::apply_env() {
     }
     i = j + 1;
   }
+}
+
+// Diagnostic graph: ntasks independent 64 x 64 tile GEMMs with K = k (A, B row
+// strips, NT) reading/writing disjoint workspace regions -- measures the tile
+// engine's throughput without dependencies.
+Graph build_gemm_bench(int ntasks, int k, int nseg, const BuildOptions &opt) {
+  Ctx cx;
+  cx.opt = opt;
+  const int64_t strip = (int64_t)TILE * k;
+  int64_t A = cx.alloc(strip * 64), Bm = cx.alloc(strip * 64), C = cx.alloc((int64_t)TILE * TILE * 64);
+  for (int t = 0; t < ntasks; ++t) {
+    RawTask rt;
+    rt.t.type = TK_GEMM;
+    rt.t.m = rt.t.n = TILE;
+    rt.t.out = Loc{BUF_WS, TILE, C + (int64_t)(t % 64) * TILE * TILE};
+    rt.t.c0 = rt.t.out;
+    rt.t.alpha = -1.0;
+    rt.t.beta = 1.0;
+    int kk = k / nseg;
+    for (int s2 = 0; s2 < nseg; ++s2)
+      rt.segs.push_back(mkseg(Loc{BUF_WS, (int32_t)k, A + (t % 64) * strip + s2 * kk}, 0,
+                              Loc{BUF_WS, (int32_t)k, Bm + ((t + 7) % 64) * strip + s2 * kk}, 1, kk));
+    cx.emit(std::move(rt));
+  }
+  return cx.finalize();
 }
 
 bool plan_partitions(int64_t n, int P, double r, std::vector<int64_t> &starts) {

@@ -112,6 +112,9 @@ int64_t distributed_ws_bytes(int P, int rank, int64_t n_global, int64_t start, i
                              int64_t b, int64_t a);
 int64_t exchange_doubles(int64_t b, int64_t a);
 
+// Diagnostic: independent tile GEMMs (engine throughput).
+Graph build_gemm_bench(int ntasks, int k, int nseg, const BuildOptions &opt);
+
 // Partition plan (reading R6).  Returns false if infeasible.
 bool plan_partitions(int64_t n, int P, double r, std::vector<int64_t> &starts);
 

@@ -58,6 +58,7 @@ struct serinv_ctx {
   int smem = 0;
   int last_launches = 0;
   double *dummy = nullptr;  // logdet sink when the caller passes NULL
+  int *dummy_info = nullptr;
   unsigned long long *trace = nullptr;  // optional per-task trace buffer (device)
   size_t trace_cap = 0;                 // records
   cudaStream_t s_in = nullptr, s_out = nullptr;  // streaming host IO copy streams
@@ -130,7 +131,9 @@ int get_graph_impl(serinv_handle_t h, const GKey &key, DevGraph **out) {
   opt.grid = h->grid;
   opt.apply_env();
   std::unique_ptr<DevGraph> dg(new DevGraph());
-  if (kind <= 2 || kind == 6) {
+  if (kind == 9) {
+    dg->g = build_gemm_bench((int)n, (int)b, (int)std::max<int64_t>(1, a), opt);
+  } else if (kind <= 2 || kind == 6) {
     dg->g = build_sequential(kind, n, b, a, opt);
   } else if (kind == 3) {
     int P = std::get<4>(key);
@@ -252,6 +255,7 @@ int serinv_create(serinv_handle_t *h, int cuda_device) {
     return SERINV_ERR_CUDA;
   c->grid = c->sms * per_sm;
   if (cudaMalloc(&c->dummy, 256) != cudaSuccess) return SERINV_ERR_CUDA;
+  c->dummy_info = (int *)(c->dummy + 16);
   *h = c.release();
   return SERINV_OK;
 }
@@ -567,6 +571,19 @@ int serinv_selinv_host(serinv_handle_t h, const serinv_bta_t *A_host, const seri
       cudaStreamWaitEvent(st, h->ev_in, 0) != cudaSuccess || cudaStreamWaitEvent(st, h->ev_out, 0) != cudaSuccess)
     return SERINV_ERR_CUDA;
   return SERINV_OK;
+}
+
+int serinv_bench_gemm(serinv_handle_t h, int ntasks, int k, int nseg, void *d_ws, size_t ws_bytes, void *stream) {
+  if (!h) return SERINV_ERR_HANDLE;
+  if (ntasks < 1 || k < 1 || nseg < 1 || k % nseg) return -2;
+  if (!d_ws || !aligned16(d_ws)) return SERINV_ERR_WS;
+  if (cudaSetDevice(h->device) != cudaSuccess) return SERINV_ERR_CUDA;
+  DevGraph *dg = nullptr;
+  int rc = get_graph(h, GKey(9, ntasks, k, nseg, 1, 0, 0, 0, 0), &dg);
+  if (rc) return rc;
+  if ((int64_t)ws_bytes < dg->g.ws_doubles * 8) return SERINV_ERR_WS;
+  double *bufs[BUF_COUNT] = {nullptr, nullptr, nullptr, nullptr, (double *)d_ws, nullptr, nullptr, h->dummy};
+  return launch(h, *dg, bufs, h->dummy_info, (cudaStream_t)stream);
 }
 
 int serinv_set_trace(serinv_handle_t h, void *d_trace, size_t bytes) {

@@ -21,8 +21,7 @@ def main():
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     n, b, a = args.n, args.b, args.a
-    A = btagen.g1(0, n, b, a)
-    D = {k: torch.from_numpy(A[k]).cuda() for k in ("diag", "lower", "arrow", "tip")}
+    D = btagen.g1_torch(0, n, b, a)
     h = sb.default_handle()
     kindid = {"pobtaf": 0, "pobtasi": 1, "selinv": 2, "pselinv": 3}[args.kind]
     st = sb.graph_stats(kindid, n, b, a, args.P)
