@@ -254,28 +254,48 @@ __device__ __forceinline__ void gemm_mainloop2(const Params &p, int s0, int ns, 
   for (int s = 0; s < ns; ++s) nchA += (segsA[s].k + KC - 1) / KC;
   for (int s = 0; s < nsb; ++s) nchB += (segsB[s].k + KC - 1) / KC;
   const int nchunks = nchA + nchB;
+  // Segment descriptors are copied into registers at segment switches only:
+  // the cp.async asm carries a memory clobber, so reading them through a
+  // reference would re-load them from global memory on every chunk.
+  struct Cur {
+    const double *a, *b;
+    int lda, ldb, k, R;
+    bool akm, bkm, va, vb;
+  };
+  auto fetch = [&](int idx, bool inB) {
+    const Seg S = inB ? segsB[idx] : segsA[idx];
+    Cur c;
+    c.a = lptr(p, S.A);
+    c.b = lptr(p, S.B);
+    c.lda = S.A.ld;
+    c.ldb = S.B.ld;
+    c.k = S.k;
+    c.R = inB ? mb : m;
+    c.akm = S.ta != 0;
+    c.bkm = S.tb == 0;
+    c.va = ((S.A.off | S.A.ld) & 1) == 0;
+    c.vb = ((S.B.off | S.B.ld) & 1) == 0;
+    return c;
+  };
   // load-side cursor (list A, then list B)
   int ls = 0, lk = 0, lj = 0;
+  Cur L = fetch(0, nchA == 0);
   auto issue = [&](int stage) {
-    const bool inB = lj >= nchA;
-    const Seg &S = inB ? segsB[ls] : segsA[ls];
-    const int R = inB ? mb : m;
     ++lj;
     double *As = smem + stage * 2 * OPSZ;
-    double *Bs = As + OPSZ;
-    bool vecA = ((S.A.off | S.A.ld) & 1) == 0;
-    bool vecB = ((S.B.off | S.B.ld) & 1) == 0;
-    load_operand(As, lptr(p, S.A), S.A.ld, S.ta != 0, R, S.k, lk, vecA);
-    load_operand(Bs, lptr(p, S.B), S.B.ld, S.tb == 0, n, S.k, lk, vecB);
+    load_operand(As, L.a, L.lda, L.akm, L.R, L.k, lk, L.va);
+    load_operand(As + OPSZ, L.b, L.ldb, L.bkm, n, L.k, lk, L.vb);
     lk += KC;
-    if (lk >= S.k) {
+    if (lk >= L.k && lj < nchunks) {
       lk = 0;
       ++ls;
       if (lj == nchA) ls = 0;  // switch to list B
+      L = fetch(ls, lj >= nchA);
     }
   };
-  // compute-side cursor (segment layouts)
+  // compute-side cursor
   int cs = 0, ck = 0;
+  Cur C = L;
 #pragma unroll
   for (int j = 0; j < STAGES - 1; ++j) {
     if (j < nchunks) issue(j);
@@ -287,21 +307,20 @@ __device__ __forceinline__ void gemm_mainloop2(const Params &p, int s0, int ns, 
     if (j + STAGES - 1 < nchunks) issue((j + STAGES - 1) % STAGES);
     cp_commit();
     const bool inB = j >= nchA;
-    const Seg &S = inB ? segsB[cs] : segsA[cs];
     const double *As = smem + (j % STAGES) * 2 * OPSZ;
     const double *Bs = As + OPSZ;
-    const bool akm = S.ta != 0, bkm = S.tb == 0;
-    int kleft = S.k - ck;
+    int kleft = C.k - ck;
     int ksteps = kleft >= KC ? KC / 4 : (kleft + 3) / 4;
     if (DUAL && inB)
-      mma_chunk_lay(akm, bkm, As, Bs, acc2, ksteps);
+      mma_chunk_lay(C.akm, C.bkm, As, Bs, acc2, ksteps);
     else
-      mma_chunk_lay(akm, bkm, As, Bs, acc, ksteps);
+      mma_chunk_lay(C.akm, C.bkm, As, Bs, acc, ksteps);
     ck += KC;
-    if (ck >= S.k) {
+    if (ck >= C.k && j + 1 < nchunks) {
       ck = 0;
       ++cs;
       if (j + 1 == nchA) cs = 0;
+      C = fetch(cs, j + 1 >= nchA);
     }
   }
   cp_wait<0>();
