@@ -565,17 +565,106 @@ __device__ __forceinline__ void warp_mma16(const double *As, int lda, const doub
   }
 }
 
+// 1/sqrt(x) and 1/x without the library's out-of-range slow paths (a branch
+// there makes the surrounding shuffles warp-collective): MUFU seed + one
+// third-order Newton step (~2^-69 relative before rounding), valid for normal
+// positive x.  x <= 0 or NaN gives NaN/inf, which the caller flags.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-(y * y), x, 1.0);
+  return fma(fma(e, 0.375, 0.5), y * e, y);
+}
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y, 1.0);
+  return fma(fma(e, e, e), y, y);
+}
+
+// Warp-level Cholesky + inverse of the 16 x 16 diagonal block at (c0, c0) of St
+// (rows/columns >= m are padded with the identity).  Right-looking elimination on
+// the symmetric block; the same row operations carried on Z = I give Z = L^{-1}
+// (the elimination matrix M with M A = L^T).  Lane l owns column j = l & 15, rows
+// i = 8 (l >> 4) + t, t < 8.  Per pivot p (d = current A[p][p]):
+//   a[i][j] -= A[i][p] A[p][j] / d   (i, j > p),   z[i][j] -= A[i][p] Z[p][j] / d  (i > p),
+//   column p of L = A[:, p] / sqrt(d), row p of Z scaled by 1 / sqrt(d).
+// The next pivot d' = A[p+1][p+1] - A[p+1][p]^2 / d is formed by every lane
+// from two values shuffled one step early, so the serial chain per pivot is one
+// reciprocal and one FMA (no shuffle, no sqrt on it).  Writes L (upper zeroed)
+// to St, Z to Wt, the pivots to dv, the first non-positive pivot to *s_bad.
+// Must be called by a whole, converged warp.
+__device__ __forceinline__ void leaf_chol16(double *St, double *Wt, double *dv, int c0, int m, int *s_bad) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, j = lane & 15, h = lane >> 4;
+  double a[8], z[8], dj = 1.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int i = 8 * h + t;
+    const bool valid = (c0 + i < m) && (c0 + j < m);
+    a[t] = valid ? St[(c0 + i) * LDT + c0 + j] : ((i == j) ? 1.0 : 0.0);
+    z[t] = (i == j) ? 1.0 : 0.0;
+  }
+  double d = __shfl_sync(FULL, a[0], 0);
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    const int tp = p & 7, hp = p >> 3;
+    const int t1 = (p + 1) & 7, h1 = (p + 1) >> 3;
+    double x = 0.0, y = 1.0;
+    if (p < 15) {  // compile-time
+      x = __shfl_sync(FULL, a[t1], p + 16 * h1);      // A[p+1][p]
+      y = __shfl_sync(FULL, a[t1], p + 1 + 16 * h1);  // A[p+1][p+1]
+    }
+    const double apj = __shfl_sync(FULL, a[tp], j + 16 * hp);
+    const double zpj = __shfl_sync(FULL, z[tp], j + 16 * hp);
+    double colp[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) colp[t] = __shfl_sync(FULL, a[t], p + 16 * h);
+    const double id = rcp_nr(d);
+    const double dn = fma(-(x * x), id, y);
+    const double rs = rsqrt_nr(d);
+    const double fa = (j > p) ? apj * id : 0.0;
+    const double fz = zpj * id;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const bool below = 8 * h + t > p;
+      a[t] = below ? fma(-colp[t], fa, a[t]) : a[t];
+      z[t] = below ? fma(-colp[t], fz, z[t]) : z[t];
+    }
+    // branch-free (a divergent branch here turns every shuffle into a collective)
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int i = 8 * h + t;
+      const double sc = (i > p) ? a[t] * rs : ((i == p) ? d * rs : 0.0);
+      a[t] = (j == p) ? sc : a[t];
+    }
+    z[tp] = (h == hp) ? z[tp] * rs : z[tp];
+    dj = (j == p) ? d : dj;
+    d = dn;
+  }
+  if (h == (j >> 3) && c0 + j < m) {
+    dv[c0 + j] = dj;
+    if (!(dj > 0.0)) atomicMin(s_bad, c0 + j);
+  }
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int i = 8 * h + t;
+    const bool valid = (c0 + i < m) && (c0 + j < m) && i >= j;
+    St[(c0 + i) * LDT + c0 + j] = valid ? a[t] : 0.0;
+    Wt[(c0 + i) * LDT + c0 + j] = valid ? z[t] : 0.0;
+  }
+}
+
 // Diagonal-tile task: optional fused pre-update (GEMM), Cholesky (factor) of the
 // 64 x 64 tile, its inverse W = L^{-1}, log-det partial, info, and the fused TRSM
 // of the sub-diagonal tile (next link of the critical chain).
 //
-// Cholesky: thread (r = tid & 15, c = tid >> 4) owns S[i][k], i = r + 16 ii,
-// k = c + 16 kk, so the 16 owners of a column form one half-warp.  At step j the
-// owners of column j+1 (already updated) take the pivot by shuffle, scale the
-// column by rsqrt(d) and publish it; everybody applies the rank-1 update of L
-// column j (branch-free).  One CTA barrier per pivot.
-// Inverse: blocked on 16 x 16 blocks: the 4 diagonal blocks by right-looking
-// substitution in 4 warps, then the off-diagonal blocks level by level
+// Cholesky: left-looking over 16-column blocks, the 16 x 16 diagonal blocks
+// factored and inverted by one warp in registers (leaf_chol16), the rows below
+// by DMMA with the leaf's inverse.
+// Inverse: blocked on 16 x 16 blocks: the 4 diagonal blocks come from the leaves
+// (TRTRI-only tasks: right-looking substitution in 4 warps), then the off-diagonal
+// blocks level by level
 // W_ij = -W_ii (sum_k L_ik W_kj) with DMMA (one warp per block).
 __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bool factor, int tsk) {
   const int tid = threadIdx.x, r = tid & 15, c = tid >> 4;
@@ -610,10 +699,10 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   __syncthreads();
   phase_mark(p, tsk, 0);
   if (factor) {
-    // Left-looking over 16-column blocks; inside a block one barrier per pivot.
-    // Thread (jj = tid & 15, rg = tid >> 4) owns A[i][16 cb + jj], i = 16 cb + rg + 16 t.
-    const int jj = tid & 15, rg = tid >> 4;
-    double *colb = lb;  // [2][64] unscaled pivot columns
+    // Left-looking over 16-column blocks.  Per block: (1) DMMA update of the
+    // block columns from the finished columns to the left, (2) one warp factors
+    // and inverts the 16 x 16 diagonal block in registers (leaf_chol16, no CTA
+    // barrier per pivot), (3) the rows below: L = A W_kk^T by DMMA.
     for (int cb = 0; cb * 16 < m; ++cb) {
       const int c0 = 16 * cb;
       const int nrow = m - c0;  // rows c0..m-1
@@ -634,63 +723,37 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
         }
         __syncthreads();
       }
-      // (2) 16 pivots
-      double av[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int i = c0 + rg + 16 * t;
-        av[t] = (i < m) ? St[i * LDT + c0 + jj] : 0.0;
-      }
-      if (jj == 0) {
-#pragma unroll
-        for (int t = 0; t < 4; ++t) colb[rg + 16 * t] = av[t];  // local row index i - c0
+      // (2) diagonal block (warp 0); the other warps zero the strict upper part above it
+      if (__all_sync(0xffffffffu, warp == 0)) {  // vote: the compiler sees a converged warp
+        leaf_chol16(St, Wt, dv, c0, m, &s_bad);
+      } else {
+        for (int idx = tid - 32; idx < c0 * 16; idx += NT - 32) St[(idx >> 4) * LDT + c0 + (idx & 15)] = 0.0;
       }
       __syncthreads();
-      const int ncol = min(16, nrow);
-      for (int q = 0; q < ncol; ++q) {
-        const double *cq = colb + (q & 1) * SERINV_TILE;
-        const double d = cq[q];
-        const double rs = rsqrt(d);
-        const double id = rs * rs;
-        const double lk = cq[jj] * id;
+      // (3) panel below the diagonal block
+      const int r0 = c0 + 16;
+      if (r0 < m) {
+        const int ngr = (m - r0 + 7) / 8;
+        if (warp < ngr) {
+          const int r8 = r0 + 8 * warp, g = lane >> 2, q = lane & 3;
+          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int il = rg + 16 * t;  // local row
-          const double f = (jj > q && jj <= il) ? cq[il] * lk : 0.0;
-          av[t] -= f;
-        }
-        if (jj == q + 1) {
-          double *cn = colb + ((q + 1) & 1) * SERINV_TILE;
+          for (int k0 = 0; k0 < 16; k0 += 4) {
+            const double av = St[(r8 + g) * LDT + c0 + k0 + q];
+            const double b0 = Wt[(c0 + g) * LDT + c0 + k0 + q];
+            const double b1 = Wt[(c0 + 8 + g) * LDT + c0 + k0 + q];
+            dmma(acc[0], av, b0);
+            dmma(acc[1], av, b1);
+          }
+          __syncwarp();
 #pragma unroll
-          for (int t = 0; t < 4; ++t) cn[rg + 16 * t] = av[t];
+          for (int ni = 0; ni < 2; ++ni) {
+            St[(r8 + g) * LDT + c0 + 8 * ni + 2 * q] = acc[ni][0];
+            St[(r8 + g) * LDT + c0 + 8 * ni + 2 * q + 1] = acc[ni][1];
+          }
         }
         __syncthreads();
       }
-      // the pivot d_q is the untouched diagonal element held by thread (jj = q, rg = q)
-      if (rg == jj && jj < ncol) {
-        const double d = av[0];
-        rsv[c0 + jj] = rsqrt(d);
-        dv[c0 + jj] = d;
-        if (!(d > 0.0)) atomicMin(&s_bad, c0 + jj);
-      }
-      __syncthreads();
-      // (3) scale the block's columns: L[i][k] = A[i][k] / sqrt(d_k) (i > k), sqrt(d_k) on the diagonal
-      {
-        const int k = c0 + jj;
-        const double rk = (k < m) ? rsv[k] : 0.0;
-        const double dk = (k < m) ? dv[k] : 0.0;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int i = c0 + rg + 16 * t;
-          if (i < SERINV_TILE) {
-            const double x = (i > k) ? av[t] * rk : ((i == k) ? dk * rk : 0.0);
-            St[i * LDT + k] = (i < m && k < m) ? x : 0.0;
-          }
-        }
-        // rows above the block in these columns are the strict upper part: zero
-        for (int i = rg; i < c0; i += 16) St[i * LDT + k] = 0.0;
-      }
-      __syncthreads();
     }
   } else {
     // TRTRI-only: L given; zero its upper part, 1 / L_jj
@@ -709,8 +772,9 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   }
   __syncthreads();
   phase_mark(p, tsk, 1);
-  // ---- inverse, diagonal 16 x 16 blocks: warp w < 4 inverts block w (lanes 0..15 = columns)
-  if (warp < 4 && 16 * warp < m && lane < 16) {
+  // ---- inverse, diagonal 16 x 16 blocks (TRTRI-only; the factor path's leaves produced
+  // them): warp w < 4 inverts block w (lanes 0..15 = columns)
+  if (!factor && warp < 4 && 16 * warp < m && lane < 16) {
     const int base = 16 * warp, cc = lane;
     double w[16], a[16];
 #pragma unroll
