@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--r", type=float, default=1.0, help="load-balance ratio for N > 1")
+    ap.add_argument("--partitions", default="auto",
+                    help="N = 1: intra-GPU partitions, e.g. 1 (sequential), 8, 256x16 (nested); "
+                         "'auto' = the library's plan (serinv_auto_partitions)")
     return ap.parse_args()
 
 
@@ -195,13 +198,19 @@ def main():
 
     # ---- inputs resident in HBM (pristine copy restored between steps, untimed); the
     # generator's torch twin builds G1 directly in HBM, bit-identical to btagen.g1
+    Ps = [1]
     if world == 1:
+        Ps = (sb.auto_partitions(n, b) if args.partitions == "auto"
+              else [int(x) for x in args.partitions.split("x")])
         pristine = btagen.g1_torch(0, n, b, a, device=f"cuda:{local}")
         work = {k: v.clone() for k, v in pristine.items()}
 
         def step(info=None, logdet=None):
-            return sb.selinv(work["diag"], work["lower"], work["arrow"], work["tip"], handle=h,
-                             check=False, info=info, logdet=logdet)
+            if Ps == [1]:
+                return sb.selinv(work["diag"], work["lower"], work["arrow"], work["tip"], handle=h,
+                                 check=False, info=info, logdet=logdet)
+            return sb.pselinv(work["diag"], work["lower"], work["arrow"], work["tip"], Ps, handle=h,
+                              check=False, info=info, logdet=logdet)
     else:
         from paper_2503_17528_b200 import distributed as sd
         parts = sb.plan(n, world, args.r)
@@ -244,7 +253,7 @@ def main():
             torch.cuda.synchronize()
             barrier()
             times.append(e0.elapsed_time(e1) / 1e3)
-    launches = h.last_launches()
+    launches = h.last_launches() * (1 if world == 1 else 2)  # N > 1: ppobtaf + ppobtasi
     t = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -266,8 +275,15 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            # public API with host buffers: H2D / D2H stream with the computation
-            sb.selinv_host(pinned, work, out, handle=h, check=False)
+            if Ps == [1]:
+                # public API with host buffers: H2D / D2H stream with the computation
+                sb.selinv_host(pinned, work, out, handle=h, check=False)
+            else:  # partitioned: H2D, pselinv, D2H on the stream
+                for k in work:
+                    work[k].copy_(pinned[k], non_blocking=True)
+                step()
+                for k in work:
+                    out[k].copy_(work[k], non_blocking=True)
             ld_host.copy_(h.scalars()[1], non_blocking=True)
             e1.record(stream)
             torch.cuda.synchronize()
@@ -293,10 +309,12 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"{args.config} n={n_loc} b={b} a={a} per GPU", "n_global": n, "b": b, "a": a,
-                       "generator": "g1 seed 0", "parallelism": f"partitions{world}" if world > 1 else "single",
+                       "generator": "g1 seed 0", "parallelism": f"partitions{world}" if world > 1 else
+                       ("single" if Ps == [1] else "intra-GPU partitions " + "x".join(map(str, Ps))),
                        "l2": f"inputs {bta_bytes(n_loc, b, a) / 1e9:.2f} GB per GPU > 126 MB L2",
-                       "step": "POBTAF+POBTASI (serinv_selinv)" if world == 1 else
-                               "PPOBTAF + NCCL all-gather + PPOBTASI"},
+                       "step": ("POBTAF+POBTASI (serinv_selinv)" if Ps == [1] else
+                                "PPOBTAF+POBTARSSI+PPOBTASI in one launch (serinv_pselinv_nested)")
+                               if world == 1 else "PPOBTAF + NCCL all-gather + PPOBTASI"},
             "seconds_per_step": round(sec_per_step, 6),
             "tflops_pobtaf_plus_pobtasi": round(value, 4),
             "fraction_of_fp64_peak": round(value / (FP64_PEAK_TFLOPS * N), 4),

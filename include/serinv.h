@@ -163,6 +163,29 @@ int serinv_pselinv(serinv_handle_t h, const serinv_bta_t *A, int P, double r, vo
                    size_t ws_bytes, int *d_info, double *d_logdet, void *stream);
 
 /*
+ * Nested solving (Sec. 4.2 "nested solving"; SURVEY 8(f)
+ * f1/f3) on ONE device: Ps[0] partitions of A; the reduced system A_r (2 Ps[0]-1
+ * blocks) is itself solved by the partitioned algorithm with Ps[1] partitions,
+ * and so on for nlev <= SERINV_MAX_LEVELS levels; the last reduced system is
+ * solved as one chain.  Every level must be feasible (serinv_plan with ratio r;
+ * levels >= 1 need Ps[k] >= 2 and 2 Ps[k-1] - 1 >= 2 Ps[k] - 1).  Same result
+ * as serinv_selinv (X in place, log det) up to rounding.  Errors as
+ * serinv_pselinv; SERINV_ERR_PLAN for an infeasible level.
+ *
+ * serinv_auto_partitions: the library's default plan for n blocks of size b on
+ * one B200 (partitions of ~64 blocks for b <= 128, ~32 for b <= 512, nested
+ * until the last reduced system has <= 48 / 16 blocks; {1} = sequential for
+ * large b, where the chains are throughput-bound).  Writes min(levels, cap)
+ * entries of Ps and returns the number of levels (>= 1).
+ */
+#define SERINV_MAX_LEVELS 4
+int serinv_auto_partitions(int64_t n, int64_t b, int *Ps, int cap);
+int serinv_pselinv_nested_ws(int64_t n, int64_t b, int64_t a, int nlev, const int *Ps, double r,
+                             size_t *bytes);
+int serinv_pselinv_nested(serinv_handle_t h, const serinv_bta_t *A, int nlev, const int *Ps, double r,
+                          void *d_ws, size_t ws_bytes, int *d_info, double *d_logdet, void *stream);
+
+/*
  * Distributed partitioned method, one process per GPU (rank p of P owns the
  * blocks [starts[p], starts[p+1]) of serinv_plan).  The caller passes its LOCAL
  * blocks:
@@ -215,6 +238,9 @@ typedef struct {
 } serinv_graph_stats_t;
 int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_t a, int P,
                        double r, serinv_graph_stats_t *out);
+/* the same for the nested partitioned graph of serinv_pselinv_nested */
+int serinv_graph_stats_nested(serinv_handle_t h, int64_t n, int64_t b, int64_t a, int nlev, const int *Ps,
+                              double r, serinv_graph_stats_t *out);
 
 /* Tracing: while d_trace != NULL, every launch whose graph has at most
  * bytes/96 tasks records 4 x uint64 per task (in emission order):

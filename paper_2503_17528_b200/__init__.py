@@ -22,7 +22,7 @@ from ._lib import BTA, GraphStats, Part
 
 __all__ = ["Handle", "pobtaf", "pobtasi", "selinv", "selinv_host", "pselinv", "plan", "version",
            "NotPositiveDefinite", "SerinvError", "ppobtaf", "ppobtasi", "exchange_bytes",
-           "graph_stats", "default_handle"]
+           "graph_stats", "default_handle", "auto_partitions"]
 
 
 class SerinvError(RuntimeError):
@@ -232,21 +232,34 @@ def plan(n: int, P: int, r: float = 1.0):
     return [(starts[p], starts[p + 1]) for p in range(P)]
 
 
-def pselinv(diag, lower, arrow, tip, P: int, r: float = 1.0, *, handle: Handle | None = None,
+def auto_partitions(n: int, b: int) -> list[int]:
+    """The library's default one-device nesting plan (serinv_auto_partitions)."""
+    out = (ctypes.c_int * 8)()
+    k = _lib.lib().serinv_auto_partitions(n, b, out, 8)
+    if k < 1:
+        raise SerinvError(k, "auto_partitions")
+    return list(out[:k])
+
+
+def pselinv(diag, lower, arrow, tip, P, r: float = 1.0, *, handle: Handle | None = None,
             check: bool = True, info=None, logdet=None):
     """In-process partitioned selected inversion on one device (PPOBTAF -> POBTARSSI ->
-    PPOBTASI, Sec. 3) with P partitions.  A -> X in place.  Returns log det."""
+    PPOBTASI, Sec. 3) with P partitions.  P may be a sequence [P0, P1, ...]:
+    nested solving (Sec. 4.2), the reduced system of level k solved with P_{k+1}
+    partitions.  A -> X in place.  Returns log det."""
     L = _lib.lib()
     h = handle or default_handle(diag.device.index)
     A = _bta(diag, lower, arrow, tip)
+    Ps = [int(P)] if isinstance(P, int) else [int(x) for x in P]
+    arr = (ctypes.c_int * len(Ps))(*Ps)
     nb = ctypes.c_size_t(0)
-    _check(L.serinv_pselinv_ws(A.n, A.b, A.a, P, float(r), ctypes.byref(nb)), "pselinv_ws")
+    _check(L.serinv_pselinv_nested_ws(A.n, A.b, A.a, len(Ps), arr, float(r), ctypes.byref(nb)), "pselinv_ws")
     ws = h.workspace(nb.value)
     si, sl = h.scalars()
     info = si if info is None else info
     logdet = sl if logdet is None else logdet
-    rc = L.serinv_pselinv(h._h, ctypes.byref(A), P, float(r), ws.data_ptr(), ws.numel(), info.data_ptr(),
-                          logdet.data_ptr(), _stream())
+    rc = L.serinv_pselinv_nested(h._h, ctypes.byref(A), len(Ps), arr, float(r), ws.data_ptr(), ws.numel(),
+                                 info.data_ptr(), logdet.data_ptr(), _stream())
     _check(rc, "pselinv")
     return _finish(h, info, logdet, check, A.b, A.n)
 
@@ -257,10 +270,16 @@ def exchange_bytes(b: int, a: int) -> int:
     return nb.value
 
 
-def graph_stats(kind: int, n: int, b: int, a: int, P: int = 1, r: float = 1.0, handle: Handle | None = None):
+def graph_stats(kind: int, n: int, b: int, a: int, P=1, r: float = 1.0, handle: Handle | None = None):
     h = handle or default_handle()
     st = GraphStats()
-    _check(_lib.lib().serinv_graph_stats(h._h, kind, n, b, a, P, float(r), ctypes.byref(st)), "graph_stats")
+    if kind == 3 and not isinstance(P, int):
+        Ps = [int(x) for x in P]
+        arr = (ctypes.c_int * len(Ps))(*Ps)
+        _check(_lib.lib().serinv_graph_stats_nested(h._h, n, b, a, len(Ps), arr, float(r), ctypes.byref(st)),
+               "graph_stats")
+    else:
+        _check(_lib.lib().serinv_graph_stats(h._h, kind, n, b, a, P, float(r), ctypes.byref(st)), "graph_stats")
     return dict(tasks=st.tasks, counters=st.counters, flops=st.flops, grid=st.grid, tile=st.tile)
 
 

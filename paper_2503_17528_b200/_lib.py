@@ -55,6 +55,13 @@ def lib():
     L.serinv_pselinv_ws.argtypes = [c_i64, c_i64, c_i64, ctypes.c_int, ctypes.c_double, sz]
     L.serinv_pselinv.argtypes = [c_p, ctypes.POINTER(BTA), ctypes.c_int, ctypes.c_double, c_p,
                                  ctypes.c_size_t, c_p, c_p, c_p]
+    ip = ctypes.POINTER(ctypes.c_int)
+    L.serinv_auto_partitions.argtypes = [c_i64, c_i64, ip, ctypes.c_int]
+    L.serinv_pselinv_nested_ws.argtypes = [c_i64, c_i64, c_i64, ctypes.c_int, ip, ctypes.c_double, sz]
+    L.serinv_pselinv_nested.argtypes = [c_p, ctypes.POINTER(BTA), ctypes.c_int, ip, ctypes.c_double, c_p,
+                                        ctypes.c_size_t, c_p, c_p, c_p]
+    L.serinv_graph_stats_nested.argtypes = [c_p, c_i64, c_i64, c_i64, ctypes.c_int, ip, ctypes.c_double,
+                                            ctypes.POINTER(GraphStats)]
     L.serinv_exchange_bytes.argtypes = [c_i64, c_i64, sz]
     L.serinv_ppobtaf_ws.argtypes = [ctypes.POINTER(Part), c_i64, c_i64, sz]
     L.serinv_ppobtaf.argtypes = [c_p, ctypes.POINTER(Part), ctypes.POINTER(BTA), c_p, ctypes.c_size_t,
@@ -78,4 +85,5 @@ EXPORTED = [
     "serinv_pobtaf", "serinv_pobtasi", "serinv_selinv", "serinv_plan",
     "serinv_pselinv_ws", "serinv_pselinv", "serinv_exchange_bytes", "serinv_ppobtaf_ws",
     "serinv_ppobtaf", "serinv_ppobtasi", "serinv_graph_stats", "serinv_last_launches", "serinv_set_trace", "serinv_selinv_host", "serinv_bench_gemm",
+    "serinv_auto_partitions", "serinv_pselinv_nested_ws", "serinv_pselinv_nested", "serinv_graph_stats_nested",
 ]

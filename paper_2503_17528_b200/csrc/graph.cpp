@@ -1005,6 +1005,17 @@ Fam famD(int64_t b) { return Fam{BUF_DIAG, 0, b * b, (int32_t)b}; }
 Fam famL(int64_t b) { return Fam{BUF_LOWER, 0, b * b, (int32_t)b}; }
 Fam famA(int64_t b, int64_t a) { return Fam{BUF_ARROW, 0, a * b, (int32_t)b}; }
 
+// The BTA matrix a (nested) partitioned solve works on: block families and the
+// global first row of block i (for info); the tip always lives in BUF_TIP.
+struct View {
+  Fam D, Lo, Ar;
+  std::function<int64_t(int64_t)> row;
+  int64_t tip_row = 0;
+};
+View top_view(int64_t n, int64_t b, int64_t a) {
+  return View{famD(b), famL(b), famA(b, a), [b](int64_t i) { return i * b; }, n * b};
+}
+
 // A BT(A) chain problem: nodes 0..m-1 of size b (diag D(i), lower Lo(i) = (i+1,i),
 // arrow Ar(i)), then the arrow node m (size a, storage tip) if a > 0.  Nodes
 // [0, elim_upto) are eliminated; the arrow node iff elim_tip.
@@ -1044,8 +1055,8 @@ void chain_problem(Problem &P, int m, int64_t b, int64_t a, std::function<Loc(in
 // nodes 0..k-1 = blocks s+1..e-1 (k = e-s-1; node k-1 is the boundary l),
 // F = k (block s, moved last by the implicit shifting permutation),
 // arrow = k+1.  Bbuf(j) stores the fill-in block (F, node j): rows f, columns j.
-void middle_problem(Problem &P, int64_t ls, int64_t cnt, int64_t b, int64_t a, Loc U, const Fam &Bbuf,
-                    int64_t glob_s) {
+void middle_problem(Problem &P, const View &V, int64_t ls, int64_t cnt, int64_t b, int64_t a, Loc U,
+                    const Fam &Bbuf, int64_t glob_s) {
   int k = (int)(cnt - 1);
   int F = k, A = k + 1;
   int nn = k + 1 + (a > 0 ? 1 : 0);
@@ -1060,26 +1071,26 @@ void middle_problem(Problem &P, int64_t ls, int64_t cnt, int64_t b, int64_t a, L
   P.rows.assign(nn, {});
   for (int j = 0; j < k; ++j) {
     int64_t li = ls + 1 + j;
-    P.rowbase[j] = (glob_s + 1 + j) * b;
-    P.blk[{j, j}] = blkref(famD(b).at(li), (int)b, (int)b);
+    P.rowbase[j] = V.row(glob_s + 1 + j);
+    P.blk[{j, j}] = blkref(V.D.at(li), (int)b, (int)b);
     bool el = j + 1 < k;
     if (el) {
-      P.blk[{j + 1, j}] = blkref(famL(b).at(li), (int)b, (int)b);
+      P.blk[{j + 1, j}] = blkref(V.Lo.at(li), (int)b, (int)b);
       P.rows[j].push_back(j + 1);
     }
     // B_{s+1} = A_{s+1,s}^T is copied in; later B_j start as fill-in zeros
     P.blk[{F, j}] = blkref(Bbuf.at(j), (int)b, (int)b, j > 0);
     if (el) P.rows[j].push_back(F);
     if (a > 0) {
-      P.blk[{A, j}] = blkref(famA(b, a).at(li), (int)a, (int)b);
+      P.blk[{A, j}] = blkref(V.Ar.at(li), (int)a, (int)b);
       if (el) P.rows[j].push_back(A);
     }
   }
-  P.rowbase[F] = glob_s * b;
-  P.blk[{F, F}] = blkref(famD(b).at(ls), (int)b, (int)b);
+  P.rowbase[F] = V.row(glob_s);
+  P.blk[{F, F}] = blkref(V.D.at(ls), (int)b, (int)b);
   if (a > 0) {
     P.rowbase[A] = -1;
-    P.blk[{A, F}] = blkref(famA(b, a).at(ls), (int)a, (int)b);
+    P.blk[{A, F}] = blkref(V.Ar.at(ls), (int)a, (int)b);
     P.blk[{A, A}] = blkref(U, (int)a, (int)a, true);
   }
 }
@@ -1137,7 +1148,9 @@ struct PartState {
   Fam Bbuf{};                 // fill-in chain (middle partitions)
   std::vector<int32_t> done;  // counters: everything the factor phase wrote
   int nelim = 0;
-  int queue = 1;              // critical claim queue of this partition's chain
+  int queue = 1;              // critical claim queue of this partition's chain (0: bulk)
+  View V;                     // the matrix this partition belongs to
+  std::vector<int32_t> inw;   // counters after which the partition's input blocks are ready
 };
 
 // PPOBTAF for one partition (Alg. 3 line 3 / line 5): factor the interior and
@@ -1148,22 +1161,24 @@ void ppobtaf_part(Ctx &cx, PartState &ps, int64_t b, int64_t a) {
   ps.U = wsloc(cx.alloc(std::max<int64_t>(a * a, 1)), std::max<int64_t>(a, 1));
   if (top) {
     int64_t ls = ps.ls;
+    const View &V = ps.V;
     chain_problem(
-        ps.prob, (int)cnt, b, a, [&](int i) { return famD(b).at(ls + i); }, [&](int i) { return famL(b).at(ls + i); },
-        [&](int i) { return famA(b, a).at(ls + i); }, ps.U, true, (int)cnt - 1, false,
-        [&](int i) { return (ps.s + i) * b; }, -1);
+        ps.prob, (int)cnt, b, a, [&](int i) { return V.D.at(ls + i); }, [&](int i) { return V.Lo.at(ls + i); },
+        [&](int i) { return V.Ar.at(ls + i); }, ps.U, true, (int)cnt - 1, false,
+        [&](int i) { return V.row(ps.s + i); }, -1);
   } else {
     ps.Bbuf = Fam{BUF_WS, cx.alloc((cnt - 1) * b * b), b * b, (int32_t)b};
-    middle_problem(ps.prob, ps.ls, cnt, b, a, ps.U, ps.Bbuf, ps.s);
+    middle_problem(ps.prob, ps.V, ps.ls, cnt, b, a, ps.U, ps.Bbuf, ps.s);
   }
   ps.prob.queue = ps.queue;
-  ps.prob.queue2 = ps.queue + 1;
+  ps.prob.queue2 = ps.queue > 0 ? ps.queue + 1 : 0;
   ps.bld.reset(new Builder(cx, ps.prob));
   Builder &B = *ps.bld;
+  B.input_waits = ps.inw;
   B.allocate(true);
   if (!top) {  // B_{s+1} = A_{s+1,s}^T (Alg. 4 line 1, reading R7)
     int32_t c = cx.new_ctr();
-    cx.copy_block(ps.Bbuf.at(0), famL(b).at(ps.ls), (int)b, (int)b, true, {}, {c});
+    cx.copy_block(ps.Bbuf.at(0), ps.V.Lo.at(ps.ls), (int)b, (int)b, true, ps.inw, {c});
     B.input_waits.push_back(c);
     ps.done.push_back(c);
   }
@@ -1200,19 +1215,20 @@ void pack_part(Ctx &cx, PartState &ps, int P, int64_t b, int64_t a, int32_t rbuf
   auto rec = [&](int64_t off, int64_t ld) { return Loc{rbuf, (int32_t)ld, r0 + off}; };
   int64_t cnt = ps.e - ps.s, ls = ps.ls;
   const auto &w = ps.done;
+  const View &V = ps.V;
   if (ps.p == 0) {
-    cx.copy_block(rec(x.bd0(), b), famD(b).at(ls + cnt - 1), (int)b, (int)b, false, w, {sig});
-    if (a > 0) cx.copy_block(rec(x.ar0(), b), famA(b, a).at(ls + cnt - 1), (int)a, (int)b, false, w, {sig});
+    cx.copy_block(rec(x.bd0(), b), V.D.at(ls + cnt - 1), (int)b, (int)b, false, w, {sig});
+    if (a > 0) cx.copy_block(rec(x.ar0(), b), V.Ar.at(ls + cnt - 1), (int)a, (int)b, false, w, {sig});
   } else {
-    cx.copy_block(rec(x.bd0(), b), famD(b).at(ls), (int)b, (int)b, false, w, {sig});
-    cx.copy_block(rec(x.bd1(), b), famD(b).at(ls + cnt - 1), (int)b, (int)b, false, w, {sig});
+    cx.copy_block(rec(x.bd0(), b), V.D.at(ls), (int)b, (int)b, false, w, {sig});
+    cx.copy_block(rec(x.bd1(), b), V.D.at(ls + cnt - 1), (int)b, (int)b, false, w, {sig});
     cx.copy_block(rec(x.lw1(), b), ps.Bbuf.at(cnt - 2), (int)b, (int)b, false, w, {sig});
     if (a > 0) {
-      cx.copy_block(rec(x.ar0(), b), famA(b, a).at(ls), (int)a, (int)b, false, w, {sig});
-      cx.copy_block(rec(x.ar1(), b), famA(b, a).at(ls + cnt - 1), (int)a, (int)b, false, w, {sig});
+      cx.copy_block(rec(x.ar0(), b), V.Ar.at(ls), (int)a, (int)b, false, w, {sig});
+      cx.copy_block(rec(x.ar1(), b), V.Ar.at(ls + cnt - 1), (int)a, (int)b, false, w, {sig});
     }
   }
-  if (ps.p < P - 1) cx.copy_block(rec(x.lw0(), b), famL(b).at(ls + cnt - 1), (int)b, (int)b, false, {}, {sig});
+  if (ps.p < P - 1) cx.copy_block(rec(x.lw0(), b), V.Lo.at(ls + cnt - 1), (int)b, (int)b, false, ps.inw, {sig});
   if (a > 0) cx.copy_block(rec(x.U(), a), ps.U, (int)a, (int)a, false, w, {sig});
 }
 
@@ -1221,13 +1237,16 @@ struct Reduced {
   Loc tip;
   Problem P;
   std::unique_ptr<Builder> B;
+  View V;                      // A_r as a BTA matrix (for a nested solve)
+  std::vector<int32_t> ready;  // A_r assembled (blocks and reduced tip)
 };
 
 // Assemble A_r (2P-1 blocks, reading R9) from the P records at (rbuf, rec0 +
 // p*recsz), then POBTARSSI = POBTAF + POBTASI on it (Sec. 3.3).  The reduced tip
 // A_nn + U_0 + ... + U_{P-1} (reading R8) is formed in place in BUF_TIP.
-void reduced_from_records(Ctx &cx, int P, int64_t n, int64_t b, int64_t a, int32_t rbuf, int64_t rec0, int64_t recsz,
-                          const std::vector<int64_t> &starts, const std::vector<int32_t> &inwaits, Reduced &R) {
+void assemble_reduced(Ctx &cx, const View &V0, int P, int64_t b, int64_t a, int32_t rbuf, int64_t rec0,
+                      int64_t recsz, const std::vector<int64_t> &starts, const std::vector<int32_t> &inwaits,
+                      Reduced &R) {
   XRec x{b, a};
   int nr = 2 * P - 1;
   R.D = Fam{BUF_WS, cx.alloc(nr * b * b), b * b, (int32_t)b};
@@ -1254,28 +1273,45 @@ void reduced_from_records(Ctx &cx, int P, int64_t n, int64_t b, int64_t a, int32
     cx.reduce_block(R.tip, R.tip, 1.0, rec(0, x.U(), a), recsz, P, 1.0, (int)a, (int)a, inwaits, {ct});
     ready.push_back(ct);
   }
-  auto rb = [&](int i) -> int64_t {
-    int64_t blk;
-    if (i == 0)
-      blk = starts[1] - 1;
-    else {
-      int p = (i + 1) / 2;
-      blk = (i & 1) ? starts[p] : starts[p + 1] - 1;
-    }
-    return blk >= 0 ? blk * b : n * b;
-  };
+  std::function<int64_t(int64_t)> vrow = V0.row;
+  const int64_t tip_row = V0.tip_row;
+  std::vector<int64_t> st = starts;
+  R.V = View{R.D, R.Lo, R.Ar,
+             [st, vrow, tip_row](int64_t i) -> int64_t {
+               int64_t blk;
+               if (i == 0)
+                 blk = st[1] - 1;
+               else {
+                 int p = (int)((i + 1) / 2);
+                 blk = (i & 1) ? st[p] : st[p + 1] - 1;
+               }
+               return blk >= 0 ? vrow(blk) : tip_row;
+             },
+             tip_row};
+  R.ready = ready;
+}
+
+// POBTARSSI on an assembled A_r: POBTAF + POBTASI as one chain (Sec. 3.3).
+void solve_reduced_chain(Ctx &cx, int64_t b, int64_t a, int nr, Reduced &R) {
   chain_problem(
       R.P, nr, b, a, [&](int i) { return R.D.at(i); }, [&](int i) { return R.Lo.at(i); },
-      [&](int i) { return R.Ar.at(i); }, R.tip, false, nr, true, rb, n * b);
+      [&](int i) { return R.Ar.at(i); }, R.tip, false, nr, true, [&](int i) { return R.V.row(i); }, R.V.tip_row);
   R.P.queue = 1;
   R.P.queue2 = 2;
   R.B.reset(new Builder(cx, R.P));
-  R.B->input_waits = ready;
+  R.B->input_waits = R.ready;
   R.B->allocate(true);
   int nn = (int)R.P.size.size();
   for (int X = 0; X < nn; ++X) R.B->factor_node(X);
   for (int X = 0; X < nn; ++X) R.B->precompute_node(X, true);
   for (int X = nn - 1; X >= 0; --X) R.B->invert_node(X);
+}
+
+void reduced_from_records(Ctx &cx, const View &V0, int P, int64_t b, int64_t a, int32_t rbuf, int64_t rec0,
+                          int64_t recsz, const std::vector<int64_t> &starts, const std::vector<int32_t> &inwaits,
+                          Reduced &R) {
+  assemble_reduced(cx, V0, P, b, a, rbuf, rec0, recsz, starts, inwaits, R);
+  solve_reduced_chain(cx, b, a, 2 * P - 1, R);
 }
 
 // Copy the true-inverse boundary blocks of partition ps from X_r into its
@@ -1307,7 +1343,7 @@ void scatter_xr(Ctx &cx, PartState &ps, int P, int64_t b, int64_t a, const Reduc
     cp(Q.blk.at({F, L}).base, R.Lo.at(2 * p - 1), (int)b, (int)b, true);  // Q_{e-1} = X_r(L_p,F_p)^T
   }
   if (p < P - 1)  // coupling to the next partition: X_r(F_{p+1}, L_p)
-    cp(famL(b).at(ps.ls + (ps.e - ps.s) - 1), R.Lo.at(2 * p), (int)b, (int)b, false);
+    cp(ps.V.Lo.at(ps.ls + (ps.e - ps.s) - 1), R.Lo.at(2 * p), (int)b, (int)b, false);
   // the tip node of the partition now stands for the true X_nn (in BUF_TIP)
   if (a > 0) Q.blk[{nn - 1, nn - 1}] = blkref(R.tip, (int)a, (int)a);
 }
@@ -1323,7 +1359,9 @@ void ppobtasi_part(Ctx &cx, PartState &ps, int64_t b, bool have_wdiag) {
   if (ps.p > 0) {  // X_{s+1,s} = Q_{s+1}^T (reading R10)
     std::vector<int32_t> w;
     for (int q = 0; q < ntiles(b); ++q) w.push_back(cx.XRC(ps.Bbuf.at(0), q, 0));
-    cx.copy_block(famL(b).at(ps.ls), ps.Bbuf.at(0), (int)b, (int)b, true, w, {});
+    const Loc dst = ps.V.Lo.at(ps.ls);
+    cx.copy_block(dst, ps.Bbuf.at(0), (int)b, (int)b, true, w, {},
+                  [&](RawTask &rt, int q, int c) { cx.sig_xblock(rt, dst, q, c); });
   }
 }
 
@@ -1377,6 +1415,7 @@ void BuildOptions::apply_env() {
       else if (k == "urgent_ctas") urgent_ctas = (int)v;
       else if (k == "si_split") si_split = (int)v;
       else if (k == "rts1_chain") rts1_chain = v != 0;
+      else if (k == "max_crit") max_crit = (int)v;
     }
     i = j + 1;
   }
@@ -1430,46 +1469,94 @@ bool plan_partitions(int64_t n, int P, double r, std::vector<int64_t> &starts) {
 
 int64_t exchange_doubles(int64_t b, int64_t a) { return (4 * b * b + 2 * a * b + a * a + 1 + 31) / 32 * 32; }
 
-Graph build_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, const BuildOptions &opt) {
+// One level of the (nested) partitioned solve of the BTA matrix V (n blocks, tip
+// in BUF_TIP): PPOBTAF on Ps[lvl] partitions, A_r (2P-1 blocks) assembled, then
+// solved by the next level (Ps[lvl+1] > 1: the same algorithm applied to A_r,
+// nested solving, Sec. 4.2) or as one chain (POBTARSSI), X_r scattered,
+// PPOBTASI.  Returns false (nothing emitted) if the plan is infeasible.
+bool psolve_level(Ctx &cx, const View &V, int64_t n, int64_t b, int64_t a, const std::vector<int> &Ps, size_t lvl,
+                  double r, const std::vector<int32_t> &inw) {
+  const int P = Ps[lvl];
   std::vector<int64_t> starts;
-  if (!plan_partitions(n, P, r, starts)) {
+  if (P < 1 || (lvl > 0 && P < 2) || !plan_partitions(n, P, r, starts)) return false;
+  const int64_t recsz = exchange_doubles(b, a);
+  const int64_t recs = cx.alloc(recsz * P);
+  std::vector<PartState> parts(P);
+  // exclusive-SM chains only for a few top-level partitions (each takes two SMs)
+  const bool crit = lvl == 0 && 2 * P <= cx.opt.max_crit;
+  for (int p = 0; p < P; ++p) {
+    parts[p].p = p;
+    parts[p].s = starts[p];
+    parts[p].e = starts[p + 1];
+    parts[p].ls = starts[p];
+    parts[p].queue = crit ? 2 * p + 1 : 0;
+    parts[p].V = V;
+    parts[p].inw = inw;
+    ppobtaf_part(cx, parts[p], b, a);
+  }
+  int32_t packed = cx.new_ctr();
+  for (int p = 0; p < P; ++p) pack_part(cx, parts[p], P, b, a, BUF_WS, recs + p * recsz, packed);
+  Reduced R;
+  assemble_reduced(cx, V, P, b, a, BUF_WS, recs, recsz, starts, {packed}, R);
+  const int nr = 2 * P - 1;
+  bool nested = lvl + 1 < Ps.size() && psolve_level(cx, R.V, nr, b, a, Ps, lvl + 1, r, R.ready);
+  if (!nested) solve_reduced_chain(cx, b, a, nr, R);
+  for (int p = 0; p < P; ++p) {
+    parts[p].done.push_back(packed);  // scatter overwrites what the pack copies read
+    scatter_xr(cx, parts[p], P, b, a, R);
+    ppobtasi_part(cx, parts[p], b, true);
+  }
+  return true;
+}
+
+Graph build_pselinv(int64_t n, int64_t b, int64_t a, const std::vector<int> &Ps, double r, const BuildOptions &opt) {
+  std::vector<int64_t> starts;
+  if (Ps.empty() || !plan_partitions(n, Ps[0], r, starts)) {
     Graph bad;
     bad.error = "infeasible plan";
     return bad;
   }
   Ctx cx;
   cx.opt = opt;
-  cx.slot_cap = slot_bound(n + 2 * P, b, a);
+  cx.slot_cap = slot_bound(n + 2 * Ps[0], b, a);
   cx.slot_region = cx.alloc(cx.slot_cap);
-  int64_t recsz = exchange_doubles(b, a);
-  int64_t recs = cx.alloc(recsz * P);
-  std::vector<PartState> parts(P);
-  for (int p = 0; p < P; ++p) {
-    parts[p].p = p;
-    parts[p].s = starts[p];
-    parts[p].e = starts[p + 1];
-    parts[p].ls = starts[p];
-    parts[p].queue = 2 * p + 1;
-    ppobtaf_part(cx, parts[p], b, a);
-  }
-  int32_t packed = cx.new_ctr();
-  for (int p = 0; p < P; ++p) pack_part(cx, parts[p], P, b, a, BUF_WS, recs + p * recsz, packed);
-  Reduced R;
-  reduced_from_records(cx, P, n, b, a, BUF_WS, recs, recsz, starts, {packed}, R);
-  for (int p = 0; p < P; ++p) {
-    parts[p].done.push_back(packed);  // scatter overwrites what the pack copies read
-    scatter_xr(cx, parts[p], P, b, a, R);
-    ppobtasi_part(cx, parts[p], b, true);
-  }
+  psolve_level(cx, top_view(n, b, a), n, b, a, Ps, 0, r, {});
   cx.logdet(Loc{BUF_LOGDET, 0, 0}, 0, cx.slot_count, Loc{BUF_WS, 0, 0}, 0, 0, {});
   return cx.finalize();
 }
 
-int64_t pselinv_ws_bytes(int64_t n, int64_t b, int64_t a, int P, double r) {
+Graph build_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, const BuildOptions &opt) {
+  return build_pselinv(n, b, a, std::vector<int>{P}, r, opt);
+}
+
+int64_t pselinv_ws_bytes(int64_t n, int64_t b, int64_t a, const std::vector<int> &Ps, double r) {
   BuildOptions opt;
   opt.schedule = false;
-  Graph g = build_pselinv(n, b, a, P, r, opt);
+  Graph g = build_pselinv(n, b, a, Ps, r, opt);
   return g.error.empty() ? g.ws_doubles * 8 : -1;
+}
+
+int64_t pselinv_ws_bytes(int64_t n, int64_t b, int64_t a, int P, double r) {
+  return pselinv_ws_bytes(n, b, a, std::vector<int>{P}, r);
+}
+
+// Default nesting for one device: partitions of about `len` blocks at every level
+// until the reduced system is short enough to solve as one chain.  Small blocks
+// have latency-bound chains (the per-step work is tiny), so they are cut short.
+std::vector<int> auto_partitions(int64_t n, int64_t b) {
+  std::vector<int> Ps;
+  const int64_t len = b <= 128 ? 64 : (b <= 512 ? 32 : 1 << 30);
+  const int64_t chain_max = b <= 128 ? 48 : 16;
+  int64_t m = n;
+  while (m > chain_max && (int)Ps.size() < 4) {
+    int64_t P = std::min<int64_t>((m + len - 1) / len, (m + 1) / 3);
+    if (P < 2) break;
+    P = std::min<int64_t>(P, 4096);
+    Ps.push_back((int)P);
+    m = 2 * P - 1;
+  }
+  if (Ps.empty()) Ps.push_back(1);
+  return Ps;
 }
 
 // Distributed per-rank graphs.  Phase 0 (ppobtaf): factor the local partition
@@ -1491,6 +1578,7 @@ Graph build_distributed(int phase, int P, int rank, int64_t n, int64_t start, in
   ps.s = start;
   ps.e = start + count;
   ps.ls = 0;
+  ps.V = top_view(n, b, a);  // local storage (block `start` at index ls = 0), global rows
   ppobtaf_part(cx, ps, b, a);
   if (phase == 0) {
     int32_t packed = cx.new_ctr();
@@ -1517,7 +1605,7 @@ Graph build_distributed(int phase, int P, int rank, int64_t n, int64_t start, in
   st[0] = 0;
   st[P] = n;
   Reduced R;
-  reduced_from_records(cx, P, n, b, a, BUF_EXT1, 0, recsz, st, {}, R);
+  reduced_from_records(cx, ps.V, P, b, a, BUF_EXT1, 0, recsz, st, {}, R);
   scatter_xr(cx, ps, P, b, a, R);
   ppobtasi_part(cx, ps, b, false);  // W tiles recomputed by TRTRI (no fused POTRF here)
   // log det = sum of the ranks' partials (rank order) + 2 sum log diag of POBTAF(A_r)

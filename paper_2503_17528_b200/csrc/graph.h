@@ -89,6 +89,7 @@ struct BuildOptions {
   int urgent_ctas = 0;          // CTAs serving the near-critical queue (0: no urgent queue)
   int si_split = 320;           // K per partial GEMM of the Takahashi tile tasks (0 = no split)
   bool rts1_chain = false;      // the second sub-diagonal TRSM also on the chain's TRSM queue
+  int max_crit = 16;            // partitioned solves: exclusive-SM chains only if 2P <= max_crit
   // overrides from the environment (SERINV_OPT="key=value,..."), for tuning runs
   void apply_env();
 };
@@ -103,6 +104,12 @@ int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a, const Bui
 // In-process partitioned pipeline on one device (PPOBTAF -> POBTARSSI -> PPOBTASI).
 Graph build_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, const BuildOptions &opt);
 int64_t pselinv_ws_bytes(int64_t n, int64_t b, int64_t a, int P, double r);
+// nested partitioned solve: Ps[0] partitions of the matrix, Ps[1] of its reduced
+// system, ... (the last reduced system is solved as one chain)
+Graph build_pselinv(int64_t n, int64_t b, int64_t a, const std::vector<int> &Ps, double r, const BuildOptions &opt);
+int64_t pselinv_ws_bytes(int64_t n, int64_t b, int64_t a, const std::vector<int> &Ps, double r);
+// default one-device nesting plan for n blocks of size b ({1} = sequential)
+std::vector<int> auto_partitions(int64_t n, int64_t b);
 
 // Distributed per-rank graphs.  phase 0 = ppobtaf (+ pack into EXT0 send buffer),
 // phase 1 = ppobtasi (assemble from EXT1 recv buffer, POBTARSSI, backward).

@@ -140,7 +140,10 @@ int get_graph_impl(serinv_handle_t h, const GKey &key, DevGraph **out) {
     double r;
     int64_t rb = std::get<5>(key);
     memcpy(&r, &rb, 8);
-    dg->g = build_pselinv(n, b, a, P, r, opt);
+    std::vector<int> Ps{P};
+    int64_t more = std::get<7>(key);  // nested levels 1.. (16 bits each)
+    for (int l = 1; l < (int)std::get<8>(key); ++l) Ps.push_back((int)((more >> (16 * (l - 1))) & 0xffff));
+    dg->g = build_pselinv(n, b, a, Ps, r, opt);
   } else {
     int P = std::get<4>(key);
     int rank = std::get<6>(key);
@@ -369,6 +372,72 @@ int serinv_pselinv(serinv_handle_t h, const serinv_bta_t *A, int P, double r, vo
   return launch(h, *dg, bufs, d_info, (cudaStream_t)stream);
 }
 
+// nested plan -> (feasible, key fields)
+static int nested_key(int64_t n, int nlev, const int *Ps, double r, int64_t *more) {
+  if (nlev < 1 || nlev > SERINV_MAX_LEVELS || !Ps) return SERINV_ERR_PLAN;
+  int64_t m = n;
+  *more = 0;
+  for (int l = 0; l < nlev; ++l) {
+    std::vector<int64_t> s;
+    if (Ps[l] < 1 || Ps[l] > 0xffff || (l > 0 && Ps[l] < 2) || !plan_partitions(m, Ps[l], r, s))
+      return SERINV_ERR_PLAN;
+    if (l > 0) *more |= (int64_t)Ps[l] << (16 * (l - 1));
+    m = 2 * (int64_t)Ps[l] - 1;
+  }
+  if (nlev > 1 && Ps[0] < 2) return SERINV_ERR_PLAN;
+  return SERINV_OK;
+}
+
+int serinv_auto_partitions(int64_t n, int64_t b, int *Ps, int cap) {
+  if (n < 1 || b < 1 || !Ps || cap < 1) return SERINV_ERR_SHAPE;
+  std::vector<int> v = auto_partitions(n, b);
+  if ((int)v.size() > SERINV_MAX_LEVELS) v.resize(SERINV_MAX_LEVELS);
+  for (int i = 0; i < (int)v.size() && i < cap; ++i) Ps[i] = v[i];
+  return (int)v.size();
+}
+
+int serinv_pselinv_nested_ws(int64_t n, int64_t b, int64_t a, int nlev, const int *Ps, double r, size_t *bytes) {
+  if (!bytes) return -7;
+  if (n < 1 || b < 1 || a < 0) return SERINV_ERR_SHAPE;
+  int64_t more;
+  int rc = nested_key(n, nlev, Ps, r, &more);
+  if (rc) return rc;
+  if (nlev == 1) return serinv_pselinv_ws(n, b, a, Ps[0], r, bytes);
+  int64_t rb;
+  memcpy(&rb, &r, 8);
+  auto key = std::make_tuple(3, n, b, a, Ps[0], rb, 0, more, (int64_t)nlev);
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto it = g_ws_cache.find(key);
+  int64_t v = it != g_ws_cache.end() ? it->second
+                                     : (g_ws_cache[key] = pselinv_ws_bytes(n, b, a, std::vector<int>(Ps, Ps + nlev), r));
+  if (v < 0) return SERINV_ERR_SHAPE;
+  *bytes = (size_t)v;
+  return SERINV_OK;
+}
+
+int serinv_pselinv_nested(serinv_handle_t h, const serinv_bta_t *A, int nlev, const int *Ps, double r, void *d_ws,
+                          size_t ws_bytes, int *d_info, double *d_logdet, void *stream) {
+  if (!h) return SERINV_ERR_HANDLE;
+  int rc = check_bta(A);
+  if (rc) return rc;
+  if (!d_info) return -8;
+  if (!d_ws || !aligned16(d_ws)) return SERINV_ERR_WS;
+  int64_t more;
+  rc = nested_key(A->n, nlev, Ps, r, &more);
+  if (rc) return rc;
+  if (nlev == 1) return serinv_pselinv(h, A, Ps[0], r, d_ws, ws_bytes, d_info, d_logdet, stream);
+  if (cudaSetDevice(h->device) != cudaSuccess) return SERINV_ERR_CUDA;
+  int64_t rb;
+  memcpy(&rb, &r, 8);
+  DevGraph *dg = nullptr;
+  rc = get_graph(h, GKey(3, A->n, A->b, A->a, Ps[0], rb, 0, more, nlev), &dg);
+  if (rc) return rc;
+  if ((int64_t)ws_bytes < dg->g.ws_doubles * 8) return SERINV_ERR_WS;
+  double *bufs[BUF_COUNT] = {A->diag, A->lower, A->arrow, A->tip, (double *)d_ws, nullptr, nullptr,
+                             d_logdet ? d_logdet : h->dummy};
+  return launch(h, *dg, bufs, d_info, (cudaStream_t)stream);
+}
+
 int serinv_exchange_bytes(int64_t b, int64_t a, size_t *bytes) {
   if (!bytes) return -3;
   if (b < 1 || a < 0) return SERINV_ERR_SHAPE;
@@ -446,6 +515,28 @@ int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_
   cudaSetDevice(h->device);
   DevGraph *dg = nullptr;
   int rc = get_graph(h, GKey(kind, n, b, a, kind == 3 ? P : 1, rb, 0, 0, 0), &dg);
+  if (rc) return rc;
+  out->tasks = dg->ntasks;
+  out->counters = dg->g.nctr;
+  out->flops = dg->g.flops;
+  out->grid = h->grid;
+  out->tile = SERINV_TILE;
+  return SERINV_OK;
+}
+
+int serinv_graph_stats_nested(serinv_handle_t h, int64_t n, int64_t b, int64_t a, int nlev, const int *Ps, double r,
+                              serinv_graph_stats_t *out) {
+  if (!h) return SERINV_ERR_HANDLE;
+  if (!out) return -8;
+  int64_t more;
+  int rc = nested_key(n, nlev, Ps, r, &more);
+  if (rc) return rc;
+  int64_t rb = 0;
+  memcpy(&rb, &r, 8);
+  cudaSetDevice(h->device);
+  DevGraph *dg = nullptr;
+  rc = get_graph(h, nlev == 1 ? GKey(3, n, b, a, Ps[0], rb, 0, 0, 0) : GKey(3, n, b, a, Ps[0], rb, 0, more, nlev),
+                 &dg);
   if (rc) return rc;
   out->tasks = dg->ntasks;
   out->counters = dg->g.nctr;

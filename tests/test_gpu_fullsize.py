@@ -37,13 +37,13 @@ def test_full_size_against_oracle(cfg):
     assert abs(ldg - ld) <= 1e-12 * abs(ld)
 
 
-def _closed_form_check(n, b, a, samples, tol=1e-10):
+def _closed_form_check(n, b, a, samples, tol=1e-10, Ps=None):
     import torch
     sb = _sb()
     A, fac = btagen.g2k(2, n, b, a, with_factors=True)
     c = cf.closed_form(n, b, a, fac)
     D = to_dev(A)
-    ldg = sb.selinv(*args(D))
+    ldg = sb.selinv(*args(D)) if Ps is None else sb.pselinv(*args(D), Ps)
     assert abs(ldg - c.logdet()) <= 1e-11 * abs(c.logdet())
     for i in samples:
         Xd = D["diag"][i].cpu().numpy()
@@ -61,6 +61,14 @@ def _closed_form_check(n, b, a, samples, tol=1e-10):
 def test_c5_closed_form():
     n = 16384
     _closed_form_check(n, 64, 8, [0, 1, 2, 777, 8191, n // 2 + 3, n - 2, n - 1])
+
+
+def test_c5_closed_form_nested_auto_plan():
+    # the launch configuration bench.py times for small b: the library's nested plan
+    n = 16384
+    Ps = _sb().auto_partitions(n, 64)
+    assert len(Ps) >= 2
+    _closed_form_check(n, 64, 8, [0, 1, 2, 127, 128, 777, 8191, n // 2 + 3, n - 2, n - 1], Ps=Ps)
 
 
 @pytest.mark.slow

@@ -38,6 +38,32 @@ def test_pselinv(P, n, b, a, gen):
     assert abs(ldg - ld) <= 1e-12 * max(1.0, abs(ld))
 
 
+@pytest.mark.parametrize("Ps", [[4, 2], [8, 4], [16, 5, 2], [6, 3]])
+@pytest.mark.parametrize("n,b,a,gen", [(48, 64, 4, "g2"), (40, 70, 5, "g2"), (64, 33, 0, "g1")])
+def test_pselinv_nested(Ps, n, b, a, gen):
+    # nested solving (Sec. 4.2): same X and log det as the sequential oracle
+    sb = _sb()
+    A = btagen.generate(gen, 7 + len(Ps), n, b, a)
+    L, X, ld = seq.selinv(A)
+    D = to_dev(A)
+    ldg = sb.pselinv(*args(D), Ps)
+    e, where = inv.max_block_err(to_host(D), X)
+    assert e <= TOL, (Ps, e, where)
+    assert abs(ldg - ld) <= 1e-12 * max(1.0, abs(ld))
+
+
+def test_pselinv_nested_not_positive_definite():
+    sb = _sb()
+    n, b, a = 40, 16, 2
+    A = btagen.g1(5, n, b, a)
+    blk = par.plan(n, 4, 1.0)[1][0]  # a level-0 boundary block, eliminated at level 1
+    A["diag"][blk][2, 2] = -1e6
+    D = to_dev(A)
+    with pytest.raises(sb.NotPositiveDefinite) as ei:
+        sb.pselinv(*args(D), [4, 2])
+    assert ei.value.row == blk * b + 3
+
+
 def test_pselinv_ratio_and_smallest_middles():
     sb = _sb()
     A = btagen.g2(3, 9, 48, 3)

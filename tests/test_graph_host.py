@@ -155,3 +155,56 @@ def test_partition_plan_matches_oracle_reading():
                     assert plan(n, P, r) == par.plan(n, P, r)
     except ImportError:
         pytest.skip("libserinv.so not built")
+
+
+def run_nested(A0, Ps, r=1.0, grid=16):
+    A, n, b, a = prep(A0)
+    ldv, info, nt = ctypes.c_double(0), ctypes.c_int(0), ctypes.c_int64(0)
+    arr = (ctypes.c_int * len(Ps))(*Ps)
+    rc = lib().dag_run_pselinv_nested(ctypes.c_int64(n), ctypes.c_int64(b), ctypes.c_int64(a), len(Ps), arr,
+                                      ctypes.c_double(r), *ptrs(A), ctypes.byref(ldv), ctypes.byref(info), grid,
+                                      ctypes.byref(nt))
+    return rc, A, ldv.value, info.value
+
+
+@pytest.mark.parametrize("Ps", [[4, 2], [5, 3], [8, 3], [8, 4, 2], [3, 2]])
+@pytest.mark.parametrize("n,b,a", [(40, 4, 2), (33, 9, 0), (48, 66, 3)])
+def test_nested_pselinv_graphs(Ps, n, b, a):
+    # nested solving (Sec. 4.2): the reduced system of level k is itself solved by
+    # the partitioned algorithm with Ps[k+1] partitions; X and log det must equal
+    # the sequential selected inversion for any nesting (SURVEY 8(c) O3 pin)
+    A0 = btagen.g2(11, n, b, a)
+    L, X, ld = seq.selinv(A0)
+    rc, R, ldv, info = run_nested(A0, Ps)
+    assert rc == 0 and info == 0
+    e, where = inv.max_block_err(cut(R, X), X)
+    assert e < 1e-11, (Ps, e, where)
+    assert abs(ldv - ld) <= 1e-12 * max(1, abs(ld))
+
+
+def test_nested_info_reports_global_row():
+    # a bad pivot inside a block that is eliminated at nesting level 1 (a partition
+    # boundary of level 0) is reported with its global row
+    n, b, a = 40, 6, 2
+    A0 = btagen.g1(5, n, b, a)
+    starts = par.plan(n, 4, 1.0)
+    blk = starts[1][0]  # first block of partition 1: a level-0 boundary
+    A0["diag"][blk][2, 2] = -1e6
+    rc, R, ldv, info = run_nested(A0, [4, 2])
+    assert rc == 0
+    assert info == blk * b + 3
+    assert np.isnan(ldv)
+
+
+def test_auto_partitions_policy():
+    out = (ctypes.c_int * 8)()
+    k = lib().dag_auto_partitions(ctypes.c_int64(16384), ctypes.c_int64(64), out, 8)
+    Ps = list(out[:k])
+    assert Ps[0] >= 64 and all(p >= 2 for p in Ps)
+    m = 16384
+    for P in Ps:  # every level feasible, last reduced system short
+        assert m >= 2 * P - 1
+        m = 2 * P - 1
+    assert m <= 48
+    k = lib().dag_auto_partitions(ctypes.c_int64(365), ctypes.c_int64(2048), out, 8)
+    assert list(out[:k]) == [1]

@@ -251,11 +251,12 @@ int dag_run_sequential(int kind, int64_t n, int64_t b, int64_t a, double *diag, 
   return rc;
 }
 
-int dag_run_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, double *diag, double *lower, double *arrow,
-                    double *tip, double *logdet, int *info, int grid, int64_t *ntasks) {
+int dag_run_pselinv_nested(int64_t n, int64_t b, int64_t a, int nlev, const int *Ps, double r, double *diag,
+                           double *lower, double *arrow, double *tip, double *logdet, int *info, int grid,
+                           int64_t *ntasks) {
   BuildOptions opt;
   opt.grid = grid;
-  Graph g = build_pselinv(n, b, a, P, r, opt);
+  Graph g = build_pselinv(n, b, a, std::vector<int>(Ps, Ps + nlev), r, opt);
   if (!g.error.empty()) {
     fprintf(stderr, "graph error: %s\n", g.error.c_str());
     return -2;
@@ -275,6 +276,17 @@ int dag_run_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, double *di
   if (logdet) *logdet = ld;
   if (ntasks) *ntasks = (int64_t)g.tasks.size();
   return rc;
+}
+
+int dag_run_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, double *diag, double *lower, double *arrow,
+                    double *tip, double *logdet, int *info, int grid, int64_t *ntasks) {
+  return dag_run_pselinv_nested(n, b, a, 1, &P, r, diag, lower, arrow, tip, logdet, info, grid, ntasks);
+}
+
+int dag_auto_partitions(int64_t n, int64_t b, int *Ps, int cap) {
+  std::vector<int> v = auto_partitions(n, b);
+  for (int i = 0; i < (int)v.size() && i < cap; ++i) Ps[i] = v[i];
+  return (int)v.size();
 }
 
 // Simulate P ranks of the distributed path on the host.  Global arrays in, X out

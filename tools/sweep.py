@@ -22,9 +22,12 @@ def run(name, Ps, reps=2):
     for P in Ps:
         try:
             t0 = time.time()
-            if P == 1:
+            if P == "auto":
+                P = sb.auto_partitions(n, b)
+            if P == 1 or P == [1]:
+                P = 1
                 sb.graph_stats(2, n, b, a)
-            else:
+            elif isinstance(P, int):
                 sb.graph_stats(3, n, b, a, P)
             tb = time.time() - t0
             best = 1e9
@@ -51,4 +54,5 @@ def run(name, Ps, reps=2):
 if __name__ == "__main__":
     for spec in sys.argv[1:]:
         name, ps = spec.split(":")
-        run(name, [int(x) for x in ps.split(",")])
+        run(name, [x if x == "auto" else ([int(y) for y in x.split("x")] if "x" in x else int(x))
+                   for x in ps.split(",")])

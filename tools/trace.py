@@ -17,13 +17,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("kind")
     ap.add_argument("n", type=int); ap.add_argument("b", type=int); ap.add_argument("a", type=int)
-    ap.add_argument("--P", type=int, default=1)
+    ap.add_argument("--P", default="1", help="partitions; nested as 256x16; 'auto'")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     n, b, a = args.n, args.b, args.a
     D = btagen.g1_torch(0, n, b, a)
     h = sb.default_handle()
     kindid = {"pobtaf": 0, "pobtasi": 1, "selinv": 2, "pselinv": 3}[args.kind]
+    args.P = sb.auto_partitions(n, b) if args.P == "auto" else [int(x) for x in args.P.split("x")]
+    if len(args.P) == 1:
+        args.P = args.P[0]
     st = sb.graph_stats(kindid, n, b, a, args.P)
     T = st["tasks"]
     buf = torch.zeros(12 * T, dtype=torch.int64, device="cuda")
