@@ -442,7 +442,7 @@ struct Builder {
           if (r1.Y == X) rt.t.zmask |= 2;  // zero tile (c, c+2)
           first_trsm = 2;
         }
-        rt.queue = cx.opt.critical_queues ? P.queue : 0;
+        rt.queue = cx.opt.critical_queues ? P.q1(X) : 0;
         int id = cx.emit(std::move(rt));
         st.pending.clear();
         st.last = id;
@@ -517,10 +517,10 @@ struct Builder {
         // the sub-diagonal TRSMs feed the next POTRF: critical queues too
         flush_queue = 0;
         if (cx.opt.critical_queues) {
-          if (cx.opt.split_chain && first_trsm == 0 && ri == 0) rt.queue = P.queue2;
-          else if (cx.opt.split_chain && first_trsm == 0 && ri == 1 && cx.opt.rts1_chain) rt.queue = P.queue2;
+          if (cx.opt.split_chain && first_trsm == 0 && ri == 0) rt.queue = P.q2(X);
+          else if (cx.opt.split_chain && first_trsm == 0 && ri == 1 && cx.opt.rts1_chain) rt.queue = P.q2(X);
           else if (cx.opt.split_chain && first_trsm == 0 && ri == 1 && cx.opt.urgent_ctas > 0) rt.queue = URGENT_QUEUE;
-          else if (ri == first_trsm && first_trsm == 1) rt.queue = P.queue;
+          else if (ri == first_trsm && first_trsm == 1) rt.queue = P.q1(X);
         }
         int id = cx.emit(std::move(rt));
         st.pending.clear();
@@ -1097,7 +1097,114 @@ void middle_problem(Problem &P, const View &V, int64_t ls, int64_t cnt, int64_t 
 
 int64_t slot_bound(int64_t nblocks, int64_t b, int64_t a) { return nblocks * ntiles(b) + ntiles(a) + 8; }
 
+// Two-sided ("twisted") elimination of the whole BTA matrix, used by the fused
+// selinv (kind 2).  Blocks 0..m-1 are eliminated top-down (Alg. 1 as written,
+// P:260-271), blocks n-1..m+1 bottom-up (Alg. 1 applied to the block-reversed
+// matrix, which is again BTA), the two chains interleaved in one elimination
+// order; the meeting block m is eliminated last before the tip.  This is the
+// symmetric block permutation [0, n-1, 1, n-2, ..., m, tip] of A: every block
+// couples only to its chain successor and the tip, so no fill-in leaves the
+// pattern and the flop count is exactly Alg. 1 + Alg. 2; X = A^{-1} on the
+// pattern and log det A are permutation invariant (reading R13).  The
+// factor L differs from Alg. 1's on the bottom half, so POBTAF alone (kind 0)
+// and POBTASI (kind 1) keep the one-sided chain.  The dependent chain is half
+// as long: two critical chains run concurrently on their own CTAs.
+//
+// Bottom-chain couplings A_{j-1,j} = A_{j,j-1}^T (storage lower[j-1]) are
+// transposed into workspace T(j) first (row-major factor / inverse storage),
+// and X_{j,j-1} = T(j)^T is transposed back into lower[j-1] at the end.
+struct Twist {
+  int64_t m = 0;
+  std::vector<int> pos;           // block -> node
+  Fam T{};                        // T(j) at T.at(j - m - 1), j = m+1..n-1
+};
+
+bool use_twist(int kind, int64_t n, const BuildOptions &opt) {
+  return kind == 2 && opt.twist_min_n > 0 && n >= std::max(3, opt.twist_min_n);
+}
+
+void twisted_problem(Ctx &cx, Problem &P, Twist &tw, int64_t n, int64_t b, int64_t a) {
+  const int64_t m = (n - 1) / 2;
+  tw.m = m;
+  tw.T = Fam{BUF_WS, cx.alloc((n - 1 - m) * b * b), b * b, (int32_t)b};
+  std::vector<int64_t> order;  // node -> block
+  for (int64_t k = 0; k < m || k < n - 1 - m; ++k) {
+    if (k < m) order.push_back(k);
+    if (k < n - 1 - m) order.push_back(n - 1 - k);
+  }
+  order.push_back(m);
+  const int nn = (int)n + (a > 0 ? 1 : 0), A = (int)n;  // node n = tip
+  tw.pos.assign(n, 0);
+  for (int X = 0; X < (int)n; ++X) tw.pos[order[X]] = X;
+  P.size.assign(nn, (int)b);
+  if (a > 0) P.size[A] = (int)a;
+  P.elim.assign(nn, 1);
+  P.accum.assign(nn, 0);
+  if (a > 0) P.accum[A] = 1;
+  P.rowbase.resize(nn);
+  P.rows.assign(nn, {});
+  P.nqueue.assign(nn, 1);
+  P.nqueue2.assign(nn, 2);
+  for (int64_t i = 0; i < n; ++i) {
+    const int X = tw.pos[i];
+    P.rowbase[X] = i * b;
+    P.blk[{X, X}] = blkref(famD(b).at(i), (int)b, (int)b);
+    if (i < m) {  // top chain: successor i+1, L_{i+1,i} in lower[i]
+      P.blk[{tw.pos[i + 1], X}] = blkref(famL(b).at(i), (int)b, (int)b);
+      P.rows[X].push_back(tw.pos[i + 1]);
+    } else if (i > m) {  // bottom chain: successor i-1, in T(i)
+      P.blk[{tw.pos[i - 1], X}] = blkref(tw.T.at(i - m - 1), (int)b, (int)b);
+      P.rows[X].push_back(tw.pos[i - 1]);
+      P.nqueue[X] = 3;
+      P.nqueue2[X] = 4;
+    }
+    if (a > 0) {
+      P.blk[{A, X}] = blkref(famA(b, a).at(i), (int)a, (int)b);
+      P.rows[X].push_back(A);
+    }
+  }
+  if (a > 0) {
+    P.rowbase[A] = n * b;
+    P.blk[{A, A}] = blkref(Loc{BUF_TIP, (int32_t)a, 0}, (int)a, (int)a);
+  }
+}
+
+Graph build_twisted_selinv(Ctx &cx, int64_t n, int64_t b, int64_t a) {
+  cx.slot_cap = slot_bound(n, b, a);
+  cx.slot_region = cx.alloc(cx.slot_cap);
+  Problem P;
+  Twist tw;
+  twisted_problem(cx, P, tw, n, b, a);
+  Builder bld(cx, P);
+  bld.allocate(true);
+  const int nn = (int)P.size.size();
+  std::vector<int32_t> tin(n, -1);
+  for (int64_t j = tw.m + 1; j < n; ++j) {  // T(j) = A_{j,j-1}^T
+    tin[j] = cx.new_ctr();
+    cx.copy_block(tw.T.at(j - tw.m - 1), famL(b).at(j - 1), (int)b, (int)b, true, {}, {tin[j]});
+  }
+  std::vector<int64_t> blk_of(nn, -1);
+  for (int64_t i = 0; i < n; ++i) blk_of[tw.pos[i]] = i;
+  for (int X = 0; X < nn; ++X) {
+    bld.input_waits.clear();
+    if (blk_of[X] > tw.m) bld.input_waits.push_back(tin[blk_of[X]]);
+    bld.factor_node(X);
+  }
+  bld.input_waits.clear();
+  cx.logdet(Loc{BUF_LOGDET, 0, 0}, 0, cx.slot_count, Loc{BUF_WS, 0, 0}, 0, 0, {});
+  for (int X = 0; X < nn; ++X) bld.precompute_node(X, true);
+  for (int X = nn - 1; X >= 0; --X) bld.invert_node(X);
+  for (int64_t j = tw.m + 1; j < n; ++j) {  // X_{j,j-1} = T(j)^T
+    const Loc src = tw.T.at(j - tw.m - 1);
+    std::vector<int32_t> w;
+    for (int q = 0; q < ntiles(b); ++q) w.push_back(cx.XRC(src, q, 0));
+    cx.copy_block(famL(b).at(j - 1), src, (int)b, (int)b, true, w, {});
+  }
+  return cx.finalize();
+}
+
 Graph build_seq_ctx(Ctx &cx, int kind, int64_t n, int64_t b, int64_t a) {
+  if (use_twist(kind, n, cx.opt)) return build_twisted_selinv(cx, n, b, a);
   bool fact = kind != 1, inv = kind != 0;  // kinds 2 and 6 (selinv, streaming IO) do both
   cx.slot_cap = slot_bound(n, b, a);
   cx.slot_region = cx.alloc(cx.slot_cap);
@@ -1375,6 +1482,13 @@ int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a, const Bui
   cx.slot_cap = slot_bound(n, b, a);
   cx.slot_region = cx.alloc(cx.slot_cap);
   Problem P;
+  if (use_twist(kind, n, opt)) {
+    Twist tw;
+    twisted_problem(cx, P, tw, n, b, a);
+    Builder bld(cx, P);
+    bld.allocate(true);
+    return cx.ws_top * 8;
+  }
   chain_problem(
       P, (int)n, b, a, [&](int i) { return famD(b).at(i); }, [&](int i) { return famL(b).at(i); },
       [&](int i) { return famA(b, a).at(i); }, Loc{BUF_TIP, (int32_t)a, 0}, false, (int)n, true,
@@ -1416,6 +1530,7 @@ void BuildOptions::apply_env() {
       else if (k == "si_split") si_split = (int)v;
       else if (k == "rts1_chain") rts1_chain = v != 0;
       else if (k == "max_crit") max_crit = (int)v;
+      else if (k == "twist_min_n") twist_min_n = (int)v;
     }
     i = j + 1;
   }

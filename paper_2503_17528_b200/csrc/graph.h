@@ -75,6 +75,11 @@ struct Problem {
   std::vector<int64_t> slot;      // logdet slot base per node (-1: none)
   int queue = 0;                  // claim queue of this problem's POTRF chain (0 = bulk)
   int queue2 = 0;                 // claim queue of the chain's sub-diagonal TRSMs (split chain)
+  // per-node overrides of (queue, queue2) (empty: every node uses queue / queue2);
+  // a twisted problem runs two independent chains, each on its own critical CTAs
+  std::vector<int> nqueue, nqueue2;
+  int q1(int X) const { return nqueue.empty() ? queue : nqueue[X]; }
+  int q2(int X) const { return nqueue2.empty() ? queue2 : nqueue2[X]; }
 };
 
 struct BuildOptions {
@@ -90,6 +95,7 @@ struct BuildOptions {
   int si_split = 320;           // K per partial GEMM of the Takahashi tile tasks (0 = no split)
   bool rts1_chain = false;      // the second sub-diagonal TRSM also on the chain's TRSM queue
   int max_crit = 16;            // partitioned solves: exclusive-SM chains only if 2P <= max_crit
+  int twist_min_n = 4;          // selinv: two-sided (twisted) elimination if n >= twist_min_n (0: never)
   // overrides from the environment (SERINV_OPT="key=value,..."), for tuning runs
   void apply_env();
 };

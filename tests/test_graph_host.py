@@ -208,3 +208,23 @@ def test_auto_partitions_policy():
     assert m <= 48
     k = lib().dag_auto_partitions(ctypes.c_int64(365), ctypes.c_int64(2048), out, 8)
     assert list(out[:k]) == [1]
+
+
+@pytest.mark.parametrize("n,b,a", [(4, 70, 5), (9, 64, 3), (12, 33, 0), (7, 130, 70), (3, 5, 2)])
+def test_twisted_selinv_graph(n, b, a, monkeypatch):
+    # selinv eliminates the two halves of the chain towards the meeting block
+    # (reading R13): same X and log det as Alg. 1 + Alg. 2, different task list
+    A0 = btagen.g2(6, n, b, a)
+    L, X, ld = seq.selinv(A0)
+    counts = {}
+    for mode in ("twisted", "one-sided"):
+        monkeypatch.setenv("SERINV_OPT", "twist_min_n=3" if mode == "twisted" else "twist_min_n=0")
+        A, nn, bb, aa = prep(A0)
+        ldv, info, nt = ctypes.c_double(0), ctypes.c_int(0), ctypes.c_int64(0)
+        rc = lib().dag_run_sequential(2, ctypes.c_int64(nn), ctypes.c_int64(bb), ctypes.c_int64(aa), *ptrs(A),
+                                      ctypes.byref(ldv), ctypes.byref(info), 16, 4, ctypes.byref(nt), -1)
+        assert rc == 0 and info.value == 0
+        assert inv.max_block_err(cut(A, X), X)[0] < 1e-12, mode
+        assert abs(ldv.value - ld) <= 1e-12 * max(1, abs(ld))
+        counts[mode] = nt.value
+    assert counts["twisted"] != counts["one-sided"]

@@ -225,6 +225,7 @@ int dag_run_sequential(int kind, int64_t n, int64_t b, int64_t a, double *diag, 
   opt.grid = grid;
   opt.update_group = update_group;
   if (si_split >= 0) opt.si_split = si_split;
+  opt.apply_env();  // SERINV_OPT (e.g. twist_min_n=0: one-sided chain)
   Graph g = build_sequential(kind, n, b, a, opt);
   if (!g.error.empty()) {
     fprintf(stderr, "graph error: %s\n", g.error.c_str());
