@@ -239,6 +239,12 @@ typedef struct {
 int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_t a, int P,
                        double r, serinv_graph_stats_t *out);
 /* the same for the nested partitioned graph of serinv_pselinv_nested */
+/* Diagnostic (tools/): the claimed task list of the cached graph for (kind, n, b, a, P, r).
+ * rec: ntasks x 10 int32 {type, flags, m, n, wait0, nwait, nlate, sig0, nsig, claim queue};
+ * waits / sigs: counter ids (sizes returned in *nw / *ns; pass NULL arrays to query).
+ * Host pointers, caller-owned.  Returns 0 or a negative argument / SERINV_ERR_* code. */
+int serinv_graph_dump(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_t a, int P, double r,
+                      int32_t *rec, int32_t *waits, int64_t *nw, int32_t *sigs, int64_t *ns);
 int serinv_graph_stats_nested(serinv_handle_t h, int64_t n, int64_t b, int64_t a, int nlev, const int *Ps,
                               double r, serinv_graph_stats_t *out);
 

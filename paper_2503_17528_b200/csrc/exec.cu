@@ -460,6 +460,242 @@ __device__ void store_acc(const Params &p, const Task &T, const double (&acc)[2]
 }
 
 // ---------------------------------------------------------------------------
+// Wide GEMM tasks: m <= 128 output rows (two row tiles) x n <= 64 columns.
+// Same task semantics as run_gemm (segments, alpha/beta C0, TF_POST, TF_MIRROR)
+// for the bulk updates whose row tiles share their operand lists (the
+// Takahashi tile products, the L W precompute): the A panel feeds 128 rows per
+// B panel, so each staged byte carries 1.33x the DMMA work of a 64 x 64 tile
+// (L2 -> SMEM traffic per flop -25 %), and the per-task overhead is amortised
+// over twice the flops.  8 warps of 32 x 32 (4 x 4 DMMA fragments), a 2-stage
+// cp.async pipeline over k-chunks of 32 in the same 110.6 KB of shared memory.
+// ---------------------------------------------------------------------------
+constexpr int WROWS = 2 * SERINV_TILE;          // 128
+constexpr int LDW_KM = WROWS + 4;               // [k][row] stride for 128 rows (132 = 4 mod 16)
+constexpr int WA_SZ = WROWS * LD_MK;            // 4608 doubles >= 32 * 132
+constexpr int WSTAGE = WA_SZ + OPSZ;            // A (128 rows) + B (64 rows)
+static_assert(2 * WSTAGE <= SMEM_DOUBLES, "wide stages fit");
+static_assert(KC * LDW_KM <= WA_SZ, "wide km layout fits");
+static_assert((WROWS + SERINV_TILE) * LDT <= SMEM_DOUBLES, "wide post-multiply fits");
+
+// op(X) is R x K (R <= ROWS); layouts as in load_operand, km stride ROWS + 4
+template <int ROWS>
+__device__ __forceinline__ void load_operand_w(double *s, const double *base, int ld, bool km, int R, int K, int k0,
+                                               bool vec) {
+  constexpr int LDK = ROWS + 4;
+  const int tid = threadIdx.x;
+  if (!km) {
+#pragma unroll
+    for (int it = 0; it < (ROWS * (KC / 2)) / NT; ++it) {
+      const int idx = tid + it * NT, r = idx >> 4, kk = (idx & 15) * 2;
+      const int kg = k0 + kk;
+      const int nv = (r < R) ? max(0, min(2, K - kg)) : 0;
+      double *dst = s + r * LD_MK + kk;
+      const double *src = base + (int64_t)r * ld + kg;
+      if (vec) {
+        cp_async16(dst, nv ? src : base, nv * 8);
+      } else {
+        dst[0] = nv > 0 ? __ldcg(src) : 0.0;
+        dst[1] = nv > 1 ? __ldcg(src + 1) : 0.0;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int it = 0; it < (KC * (ROWS / 2)) / NT; ++it) {
+      const int idx = tid + it * NT, kk = idx / (ROWS / 2), r = (idx % (ROWS / 2)) * 2;
+      const int kg = k0 + kk;
+      const int nv = (kg < K) ? max(0, min(2, R - r)) : 0;
+      double *dst = s + kk * LDK + r;
+      const double *src = base + (int64_t)kg * ld + r;
+      if (vec) {
+        cp_async16(dst, nv ? src : base, nv * 8);
+      } else {
+        dst[0] = nv > 0 ? __ldcg(src) : 0.0;
+        dst[1] = nv > 1 ? __ldcg(src + 1) : 0.0;
+      }
+    }
+  }
+}
+
+// acc(32 x 32 warp tile of a 128 x 64 output) += A * B over `ksteps` k-steps of 4;
+// A elem (row, k) at As[row*sAr + k*sAk]; B elem (k, col) at Bs[col*sBn + k*sBk].
+template <int sAr, int sAk, int sBn, int sBk>
+__device__ __forceinline__ void wide_steps(const double *As, const double *Bs, double (&acc)[4][4][2], int ksteps) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kq = lane & 3;
+  const double *Ap = As + ((warp >> 1) * 32 + (lane >> 2)) * sAr + kq * sAk;
+  const double *Bp = Bs + ((warp & 1) * 32 + (lane >> 2)) * sBn + kq * sBk;
+  auto step = [&](int ks) {
+    double a[4], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = Ap[mi * 8 * sAr + ks * 4 * sAk];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = Bp[ni * 8 * sBn + ks * 4 * sBk];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+  };
+  if (ksteps == KC / 4) {
+#pragma unroll
+    for (int ks = 0; ks < KC / 4; ++ks) step(ks);
+  } else {
+    for (int ks = 0; ks < ksteps; ++ks) step(ks);
+  }
+}
+
+__device__ __forceinline__ void wide_chunk(bool akm, bool bkm, const double *As, const double *Bs,
+                                           double (&acc)[4][4][2], int ksteps) {
+  if (akm) {
+    if (bkm) wide_steps<1, LDW_KM, 1, LD_KM>(As, Bs, acc, ksteps);
+    else wide_steps<1, LDW_KM, LD_MK, 1>(As, Bs, acc, ksteps);
+  } else {
+    if (bkm) wide_steps<LD_MK, 1, 1, LD_KM>(As, Bs, acc, ksteps);
+    else wide_steps<LD_MK, 1, LD_MK, 1>(As, Bs, acc, ksteps);
+  }
+}
+
+__device__ __forceinline__ void wide_rc(int mi, int ni, int h, int &r, int &c) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  r = (warp >> 1) * 32 + mi * 8 + (lane >> 2);
+  c = (warp & 1) * 32 + ni * 8 + 2 * (lane & 3) + h;
+}
+
+__device__ void run_gemm_wide(const Params &p, const Task &T, double *smem) {
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int m = T.m, n = T.n;
+  const Seg *segs = p.segs + T.seg0;
+  int nch = 0;
+  for (int s = 0; s < T.nseg; ++s) nch += (segs[s].k + KC - 1) / KC;
+  struct Cur {
+    const double *a, *b;
+    int lda, ldb, k;
+    bool akm, bkm, va, vb;
+  };
+  auto fetch = [&](int idx) {
+    const Seg S = segs[idx];
+    Cur c;
+    c.a = lptr(p, S.A);
+    c.b = lptr(p, S.B);
+    c.lda = S.A.ld;
+    c.ldb = S.B.ld;
+    c.k = S.k;
+    c.akm = S.ta != 0;
+    c.bkm = S.tb == 0;
+    c.va = ((S.A.off | S.A.ld) & 1) == 0;
+    c.vb = ((S.B.off | S.B.ld) & 1) == 0;
+    return c;
+  };
+  if (nch > 0) {
+    int ls = 0, lk = 0, lj = 0;
+    Cur L = fetch(0);
+    auto issue = [&](int stage) {
+      ++lj;
+      double *As = smem + stage * WSTAGE;
+      load_operand_w<WROWS>(As, L.a, L.lda, L.akm, m, L.k, lk, L.va);
+      load_operand_w<SERINV_TILE>(As + WA_SZ, L.b, L.ldb, L.bkm, n, L.k, lk, L.vb);
+      lk += KC;
+      if (lk >= L.k && lj < nch) {
+        lk = 0;
+        L = fetch(++ls);
+      }
+    };
+    int cs = 0, ck = 0;
+    Cur C = L;
+    issue(0);
+    cp_commit();
+    for (int j = 0; j < nch; ++j) {
+      cp_wait<0>();
+      __syncthreads();
+      if (j + 1 < nch) issue((j + 1) & 1);
+      cp_commit();
+      const double *As = smem + (j & 1) * WSTAGE;
+      const int kleft = C.k - ck;
+      const int ksteps = kleft >= KC ? KC / 4 : (kleft + 3) / 4;
+      wide_chunk(C.akm, C.bkm, As, As + WA_SZ, acc, ksteps);
+      ck += KC;
+      if (ck >= C.k && j + 1 < nch) {
+        ck = 0;
+        C = fetch(++cs);
+      }
+    }
+    cp_wait<0>();
+    __syncthreads();
+  }
+  // acc = alpha * acc + beta * C0
+  {
+    const double *c0 = (T.beta != 0.0) ? lptr(p, T.c0) : nullptr;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int r, cc;
+          wide_rc(mi, ni, h, r, cc);
+          double v = T.alpha * acc[mi][ni][h];
+          if (c0 && r < m && cc < n) v += T.beta * __ldcg(c0 + (int64_t)r * T.c0.ld + cc);
+          acc[mi][ni][h] = v;
+        }
+  }
+  if (T.flags & TF_POST) {  // out = S op(R), S = the 128 x n result, R n x n
+    double *St = smem;
+    double *Rt = smem + WROWS * LDT;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int r, cc;
+          wide_rc(mi, ni, h, r, cc);
+          St[r * LDT + cc] = acc[mi][ni][h];
+          acc[mi][ni][h] = 0.0;
+        }
+    tile_to_smem(Rt, lptr(p, T.r), T.r.ld, n, n);
+    __syncthreads();
+    if (T.flags & TF_POST_T)
+      wide_steps<LDT, 1, LDT, 1>(St, Rt, acc, (n + 3) / 4);
+    else
+      wide_steps<LDT, 1, 1, LDT>(St, Rt, acc, (n + 3) / 4);
+    __syncthreads();
+  }
+  double *o = lptr(p, T.out);
+  const bool vec = ((T.out.off | T.out.ld) & 1) == 0;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      int r, cc;
+      wide_rc(mi, ni, 0, r, cc);
+      if (r >= m) continue;
+      double *dst = o + (int64_t)r * T.out.ld + cc;
+      if (vec && cc + 1 < n) {
+        *reinterpret_cast<double2 *>(dst) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      } else {
+        if (cc < n) dst[0] = acc[mi][ni][0];
+        if (cc + 1 < n) dst[1] = acc[mi][ni][1];
+      }
+    }
+  if (T.flags & TF_MIRROR) {
+    double *o2 = lptr(p, T.out2);
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int r, cc;
+          wide_rc(mi, ni, h, r, cc);
+          if (r < m && cc < n) o2[(int64_t)cc * T.out2.ld + r] = acc[mi][ni][h];
+        }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Tile tasks
 // ---------------------------------------------------------------------------
 __device__ void run_gemm(const Params &p, const Task &T, double *smem) {
@@ -1059,7 +1295,10 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
     if (p.trace && threadIdx.x == 0) t_start = globaltimer();
     __syncthreads();
     switch (T.type) {
-      case TK_GEMM: run_gemm(p, T, smem); break;
+      case TK_GEMM:
+        if (T.m > SERINV_TILE) run_gemm_wide(p, T, smem);
+        else run_gemm(p, T, smem);
+        break;
       case TK_POTRF: run_potrf_trtri(p, T, smem, true, t); break;
       case TK_TRTRI: run_potrf_trtri(p, T, smem, false, t); break;
       case TK_REDUCE: run_reduce(p, T); break;

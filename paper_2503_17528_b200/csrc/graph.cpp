@@ -241,6 +241,11 @@ struct Builder {
   std::map<std::tuple<int, int, int>, int> lam_task;
   std::vector<int32_t> input_waits;  // extra waits for tasks reading the problem's inputs
   int flush_queue = 0;               // claim queue of update tasks being flushed
+  int concurrency = 1;               // independent chains whose inversion waves overlap (twisted: 2)
+  // wide (128-row) tasks for a wave of `tiles` independent 64 x 64 output tiles
+  bool use_wide(int tiles) const {
+    return cx.opt.wide_min_wave > 0 && tiles * std::max(1, concurrency) >= cx.opt.wide_min_wave;
+  }
 
   Builder(Ctx &c, Problem &p) : cx(c), P(p) {}
 
@@ -611,12 +616,15 @@ struct Builder {
     for (int Z : P.rows[X]) {
       const BlkRef &bz = B(Z, X);
       Loc lc = P.Lchk.at({Z, X});
+      const int nqz = ntiles(P.size[Z]);
+      const bool wide = use_wide(nqz * nt);
       for (int c = 0; c < nt; ++c) {
         int32_t lcc = lcol_ctr(Z, X, c);
-        for (int q = 0; q < ntiles(P.size[Z]); ++q) {
+        for (int q = 0; q < nqz; q += (wide && q + 1 < nqz) ? 2 : 1) {
+          const bool two = wide && q + 1 < nqz;
           RawTask rt;
           rt.t.type = TK_GEMM;
-          rt.t.m = (int16_t)tdim(P.size[Z], q);
+          rt.t.m = (int16_t)(tdim(P.size[Z], q) + (two ? tdim(P.size[Z], q + 1) : 0));
           rt.t.n = (int16_t)tdim(P.size[X], c);
           rt.t.out = tileloc(lc, q, c);
           rt.t.alpha = 1.0;
@@ -700,6 +708,7 @@ struct Builder {
     int K = 0;
     for (auto &sg : rt.segs) K += sg.k;
     const int KS = cx.opt.si_split;
+    wave *= std::max(1, concurrency);  // independent chains inverted side by side
     const int want = (2 * std::max(1, cx.opt.grid) + wave - 1) / std::max(1, wave);
     int pieces = std::min({split_pieces, (K + KS - 1) / std::max(1, KS), want});
     if (split_base < 0 || KS <= 0 || pieces < 2 || tile >= split_tiles) {
@@ -768,38 +777,53 @@ struct Builder {
     int wave1 = 0;
     for (int Y : R) wave1 += ntiles(P.size[Y]) * nt;
     const int wave2 = nt * (nt + 1) / 2;
+    const bool wide = use_wide(wave1);
     for (int Y : R) {  // X_{Y,X}(q,c) = -sum_Z X_{Y,Z}(q,:) Lchk(Z,X)(:,c)
       const BlkRef &by = B(Y, X);
-      for (int q = 0; q < ntiles(P.size[Y]); ++q)
+      const int nq = ntiles(P.size[Y]);
+      for (int q = 0; q < nq; q += (wide && q + 1 < nq) ? 2 : 1) {
+        const bool two = wide && q + 1 < nq;  // rows q, q+1 in one wide task
         for (int c = 0; c < nt; ++c) {
           RawTask rt;
           rt.t.type = TK_GEMM;
-          rt.t.m = (int16_t)tdim(P.size[Y], q);
+          rt.t.m = (int16_t)(tdim(P.size[Y], q) + (two ? tdim(P.size[Y], q + 1) : 0));
           rt.t.n = (int16_t)tdim(P.size[X], c);
           rt.t.out = tileloc(by.base, q, c);
           rt.t.alpha = -1.0;
           rt.t.beta = 0.0;
           for (int Z : R) {
-            Loc a;
+            Loc a, a2;
             int tr, k;
             xrow(rt, Y, Z, q, a, tr, k);
+            if (two) xrow(rt, Y, Z, q + 1, a2, tr, k);
             rt.segs.push_back(mkseg(a, tr, tileloc(P.Lchk.at({Z, X}), 0, c), 0, k));
             rt.waits.push_back(lcol_ctr(Z, X, c));
           }
           rt.waits.push_back(pre);  // WAR: L_{Y,X} consumed by the precompute
           rt.sigs.push_back(XR(Y, X, q));
+          if (two) rt.sigs.push_back(XR(Y, X, q + 1));
           rt.sigs.push_back(XC(Y, X, c));
           if (fin_ctr >= 0) rt.sigs.push_back(fin_ctr);
-          emit_split(std::move(rt), tile++, wave1);
+          if (two) {
+            cx.emit(std::move(rt));
+            tile += 2;
+          } else {
+            emit_split(std::move(rt), tile++, wave1);
+          }
         }
+      }
     }
     // X_{X,X}(r,c) = Lambda(r,c) - sum_Y X_{Y,X}(:,r)^T Lchk(Y,X)(:,c), r >= c, mirrored
     const BlkRef &d = B(X, X);
-    for (int r = 0; r < nt; ++r)
-      for (int c = 0; c <= r; ++c) {
+    const bool wide2 = use_wide(wave2);
+    // X_XX tiles (r, c), r >= c; with wide tasks the off-diagonal rows of column c
+    // go in pairs (r, r+1), r > c (each mirrored), the diagonal tile alone
+    for (int c = 0; c < nt; ++c)
+      for (int r = c; r < nt;) {
+        const bool two = wide2 && r > c && r + 1 < nt;
         RawTask rt;
         rt.t.type = TK_GEMM;
-        rt.t.m = (int16_t)tdim(P.size[X], r);
+        rt.t.m = (int16_t)(tdim(P.size[X], r) + (two ? tdim(P.size[X], r + 1) : 0));
         rt.t.n = (int16_t)tdim(P.size[X], c);
         rt.t.out = tileloc(d.base, r, c);
         rt.t.c0 = tileloc(P.Lam[X], r, c);
@@ -808,22 +832,31 @@ struct Builder {
         for (int Y : R) {
           rt.segs.push_back(mkseg(tileloc(B(Y, X).base, 0, r), 1, tileloc(P.Lchk.at({Y, X}), 0, c), 0, P.size[Y]));
           rt.waits.push_back(XC(Y, X, r));
+          if (two) rt.waits.push_back(XC(Y, X, r + 1));
           rt.waits.push_back(lcol_ctr(Y, X, c));
         }
         rt.waits.push_back(cx.ctr_of(lam_task.at(std::make_tuple(X, r, c))));
+        if (two) rt.waits.push_back(cx.ctr_of(lam_task.at(std::make_tuple(X, r + 1, c))));
         rt.waits.push_back(pre);
         if (r != c) {
           rt.t.flags = TF_MIRROR;
           rt.t.out2 = tileloc(d.base, c, r);
         }
-        rt.sigs.push_back(XR(X, X, r));
-        rt.sigs.push_back(XC(X, X, c));
-        if (r != c) {
-          rt.sigs.push_back(XR(X, X, c));
-          rt.sigs.push_back(XC(X, X, r));
+        for (int rr = r; rr <= r + (two ? 1 : 0); ++rr) {
+          rt.sigs.push_back(XR(X, X, rr));
+          if (rr != c) rt.sigs.push_back(XC(X, X, rr));
         }
+        rt.sigs.push_back(XC(X, X, c));
+        if (r != c) rt.sigs.push_back(XR(X, X, c));
         if (fin_ctr >= 0) rt.sigs.push_back(fin_ctr);
-        emit_split(std::move(rt), tile++, wave2);
+        if (two) {
+          cx.emit(std::move(rt));
+          tile += 2;
+          r += 2;
+        } else {
+          emit_split(std::move(rt), tile++, wave2);
+          r += 1;
+        }
       }
     ++split_step;
   }
@@ -1119,8 +1152,12 @@ struct Twist {
   Fam T{};                        // T(j) at T.at(j - m - 1), j = m+1..n-1
 };
 
-bool use_twist(int kind, int64_t n, const BuildOptions &opt) {
-  return kind == 2 && opt.twist_min_n > 0 && n >= std::max(3, opt.twist_min_n);
+// The twisted order pays off where the dependent chain, not the FP64 work, bounds
+// the factorisation: the chain has n * b / 64 tile steps of ~30 us, the work
+// ~7/3 n b^3 flops (+ the overlapped inversion precompute).  For b >= 2048 the
+// one-sided chain already hides under the work (C3), so keep Alg. 1's order.
+bool use_twist(int kind, int64_t n, int64_t b, const BuildOptions &opt) {
+  return kind == 2 && opt.twist_min_n > 0 && n >= std::max(3, opt.twist_min_n) && b <= opt.twist_max_b;
 }
 
 void twisted_problem(Ctx &cx, Problem &P, Twist &tw, int64_t n, int64_t b, int64_t a) {
@@ -1176,6 +1213,7 @@ Graph build_twisted_selinv(Ctx &cx, int64_t n, int64_t b, int64_t a) {
   Twist tw;
   twisted_problem(cx, P, tw, n, b, a);
   Builder bld(cx, P);
+  bld.concurrency = 2;
   bld.allocate(true);
   const int nn = (int)P.size.size();
   std::vector<int32_t> tin(n, -1);
@@ -1204,7 +1242,7 @@ Graph build_twisted_selinv(Ctx &cx, int64_t n, int64_t b, int64_t a) {
 }
 
 Graph build_seq_ctx(Ctx &cx, int kind, int64_t n, int64_t b, int64_t a) {
-  if (use_twist(kind, n, cx.opt)) return build_twisted_selinv(cx, n, b, a);
+  if (use_twist(kind, n, b, cx.opt)) return build_twisted_selinv(cx, n, b, a);
   bool fact = kind != 1, inv = kind != 0;  // kinds 2 and 6 (selinv, streaming IO) do both
   cx.slot_cap = slot_bound(n, b, a);
   cx.slot_region = cx.alloc(cx.slot_cap);
@@ -1482,7 +1520,7 @@ int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a, const Bui
   cx.slot_cap = slot_bound(n, b, a);
   cx.slot_region = cx.alloc(cx.slot_cap);
   Problem P;
-  if (use_twist(kind, n, opt)) {
+  if (use_twist(kind, n, b, opt)) {
     Twist tw;
     twisted_problem(cx, P, tw, n, b, a);
     Builder bld(cx, P);
@@ -1531,6 +1569,8 @@ void BuildOptions::apply_env() {
       else if (k == "rts1_chain") rts1_chain = v != 0;
       else if (k == "max_crit") max_crit = (int)v;
       else if (k == "twist_min_n") twist_min_n = (int)v;
+      else if (k == "twist_max_b") twist_max_b = (int)v;
+      else if (k == "wide_min_wave") wide_min_wave = (int)v;
     }
     i = j + 1;
   }

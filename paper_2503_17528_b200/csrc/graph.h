@@ -96,6 +96,8 @@ struct BuildOptions {
   bool rts1_chain = false;      // the second sub-diagonal TRSM also on the chain's TRSM queue
   int max_crit = 16;            // partitioned solves: exclusive-SM chains only if 2P <= max_crit
   int twist_min_n = 4;          // selinv: two-sided (twisted) elimination if n >= twist_min_n (0: never)
+  int wide_min_wave = 512;      // 128 x 64 tasks for inversion waves of >= this many tiles (0: never)
+  int twist_max_b = 1024;       // ... and b <= twist_max_b (larger blocks: the one-sided chain hides under the work)
   // overrides from the environment (SERINV_OPT="key=value,..."), for tuning runs
   void apply_env();
 };

@@ -524,6 +524,40 @@ int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_
   return SERINV_OK;
 }
 
+// Diagnostic: the claimed task list of a cached sequential / partitioned graph.
+// rec (ntasks x 10 int32): type, flags, m, n, wait0, nwait, nlate, sig0, nsig, queue;
+// waits (nwaits int32 counter ids), sigs (nsigs int32).  Sizes via *nw, *ns.
+int serinv_graph_dump(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_t a, int P, double r, int32_t *rec,
+                      int32_t *waits, int64_t *nw, int32_t *sigs, int64_t *ns) {
+  if (!h) return SERINV_ERR_HANDLE;
+  if (kind < 0 || kind > 3) return -2;
+  int64_t rb = 0;
+  if (kind == 3) memcpy(&rb, &r, 8);
+  cudaSetDevice(h->device);
+  DevGraph *dg = nullptr;
+  int rc = get_graph(h, GKey(kind, n, b, a, kind == 3 ? P : 1, rb, 0, 0, 0), &dg);
+  if (rc) return rc;
+  const Graph &g = dg->g;
+  if (nw) *nw = (int64_t)g.waits.size();
+  if (ns) *ns = (int64_t)g.sigs.size();
+  if (rec) {
+    std::vector<int32_t> q(g.tasks.size(), 0);
+    for (size_t qq = 0; qq + 1 < g.qoff.size(); ++qq)
+      for (int32_t k = g.qoff[qq]; k < g.qoff[qq + 1]; ++k) q[g.qlist[k]] = (int32_t)qq;
+    for (size_t t = 0; t < g.tasks.size(); ++t) {
+      const Task &T = g.tasks[t];
+      int32_t *o = rec + 10 * t;
+      o[0] = T.type; o[1] = T.flags; o[2] = T.m; o[3] = T.n; o[4] = T.wait0; o[5] = T.nwait;
+      o[6] = T.nlate; o[7] = T.sig0; o[8] = T.nsig; o[9] = q[t];
+    }
+  }
+  if (waits)
+    for (size_t w = 0; w < g.waits.size(); ++w) waits[w] = g.waits[w].ctr;
+  if (sigs)
+    for (size_t s = 0; s < g.sigs.size(); ++s) sigs[s] = g.sigs[s];
+  return SERINV_OK;
+}
+
 int serinv_graph_stats_nested(serinv_handle_t h, int64_t n, int64_t b, int64_t a, int nlev, const int *Ps, double r,
                               serinv_graph_stats_t *out) {
   if (!h) return SERINV_ERR_HANDLE;

@@ -228,3 +228,20 @@ def test_twisted_selinv_graph(n, b, a, monkeypatch):
         assert abs(ldv.value - ld) <= 1e-12 * max(1, abs(ld))
         counts[mode] = nt.value
     assert counts["twisted"] != counts["one-sided"]
+
+
+@pytest.mark.parametrize("n,b,a", [(4, 200, 5), (5, 130, 70), (3, 256, 0), (6, 192, 3)])
+def test_wide_tasks(n, b, a, monkeypatch):
+    # 128-row GEMM tasks (paired row tiles) for the inversion waves and the L W
+    # precompute: forced on for every wave, same results (sequential, twisted, nested)
+    monkeypatch.setenv("SERINV_OPT", "wide_min_wave=1")
+    A0 = btagen.g2(7, n, b, a)
+    L, X, ld = seq.selinv(A0)
+    for kind, src, ref in ((2, A0, X), (1, L, X)):
+        R, ldr, info = run_seq(kind, src)
+        assert info == 0
+        assert inv.max_block_err(cut(R, ref), ref)[0] < 1e-12
+    if n >= 3:
+        rc, R, ldr, info = run_nested(A0, [2])
+        assert rc == 0 and info == 0
+        assert inv.max_block_err(cut(R, X), X)[0] < 1e-12

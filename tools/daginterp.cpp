@@ -31,7 +31,7 @@ inline double opget(Ctx &c, const Loc &l, int trans, int i, int j) {
 int run(const Graph &g, Ctx &c) {
   c.ctr.assign(g.nctr, 0);
   if (g.arr_ctr >= 0) c.ctr[g.arr_ctr] = 1 << 30;  // streaming IO: every block has arrived
-  std::vector<double> acc(SERINV_TILE * SERINV_TILE), tmp(SERINV_TILE * SERINV_TILE);
+  std::vector<double> acc(2 * SERINV_TILE * SERINV_TILE), tmp(2 * SERINV_TILE * SERINV_TILE);  // wide GEMM: m <= 128
   for (size_t t = 0; t < g.tasks.size(); ++t) {
     const Task &T = g.tasks[t];
     for (int w = 0; w < T.nwait; ++w) {
@@ -43,6 +43,11 @@ int run(const Graph &g, Ctx &c) {
       }
     }
     const int m = T.m, n = T.n;
+    if (m > SERINV_TILE && (T.type != TK_GEMM || m > 2 * SERINV_TILE || n > SERINV_TILE || T.nlate ||
+                            (T.flags & (TF_SYRK3 | TF_ZERO_MIRROR)))) {
+      fprintf(stderr, "task %zu: unsupported wide task (type %d, %d x %d, flags %d)\n", t, T.type, m, n, T.flags);
+      return -4;
+    }
     if (getenv("DAG_DUMP"))
       fprintf(stderr, "t%zu type %d m %d n %d out(%d,%lld) c0(%d,%lld) nseg %d nseg1 %d alpha %g beta %g flags %d out3(%d,%lld) m3 %d beta3 %g\n", t, T.type, m, n,
               T.out.buf, (long long)T.out.off, T.c0.buf, (long long)T.c0.off, T.nseg, T.nseg1, T.alpha, T.beta, T.flags,
@@ -257,6 +262,7 @@ int dag_run_pselinv_nested(int64_t n, int64_t b, int64_t a, int nlev, const int 
                            int64_t *ntasks) {
   BuildOptions opt;
   opt.grid = grid;
+  opt.apply_env();
   Graph g = build_pselinv(n, b, a, std::vector<int>(Ps, Ps + nlev), r, opt);
   if (!g.error.empty()) {
     fprintf(stderr, "graph error: %s\n", g.error.c_str());
@@ -306,6 +312,7 @@ int dag_run_distributed(int64_t n, int64_t b, int64_t a, int P, double r, double
   std::vector<Rank> R(P);
   BuildOptions opt;
   opt.grid = 8;
+  opt.apply_env();
   for (int p = 0; p < P; ++p) {
     Rank &k = R[p];
     int64_t s = st[p], e = st[p + 1], cnt = e - s;

@@ -94,6 +94,17 @@ def main():
         ov = np.clip(np.minimum(end, hi) - np.maximum(start, lo), 0, None).sum()
         util.append(ov / (st['grid'] * (hi - lo)))
     print("  utilisation per 5% of time:", " ".join(f"{u:.2f}" for u in util))
+    # the least-utilised 5% window (before the last one): what runs, what waits
+    k = int(np.argmin(util[:-1]))
+    lo, hi = edges[k], edges[k + 1]
+    run_ = (start < hi) & (end > lo)
+    wait_ = (claim < hi) & (start > lo)
+    print(f"  dip window {k}: {lo/1e6:.2f}-{hi/1e6:.2f} ms, util {util[k]:.2f}")
+    for t in sorted(set(typ[run_ | wait_].tolist())):
+        print(f"    {NAMES.get(t, t):8s} running {int((run_ & (typ == t)).sum()):6d}  claimed-waiting {int((wait_ & (typ == t)).sum()):6d}")
+    pw = np.where(wait_ & (typ == 2))[0]
+    if len(pw):
+        print(f"    POTRF in window: rows(m) {sorted(set(m[pw].tolist()))[:5]} start-claim {((start - claim)[pw]).mean()/1e3:.1f} us")
     if args.out:
         np.savez(args.out, claim=claim, start=start, end=end, typ=typ, sm=sm, m=m, n=nn)
 
