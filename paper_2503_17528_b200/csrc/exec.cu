@@ -891,6 +891,196 @@ __device__ __forceinline__ void leaf_chol16(double *St, double *Wt, double *dv, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// 8 x 8 block helpers (one warp).  A block is addressed by its top-left element
+// in a [64][LDT] smem tile.  Accumulator layout (DMMA m8n8): lane (g = lane >> 2,
+// q = lane & 3) holds row g, columns 2q, 2q + 1.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void blk_load(const double *B, double (&v)[2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  v[0] = B[g * LDT + 2 * q];
+  v[1] = B[g * LDT + 2 * q + 1];
+}
+__device__ __forceinline__ void blk_store(double *B, const double (&v)[2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  B[g * LDT + 2 * q] = v[0];
+  B[g * LDT + 2 * q + 1] = v[1];
+}
+// acc += X Y^T
+__device__ __forceinline__ void blk_mma_nt(double (&acc)[2], const double *X, const double *Y) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  dmma(acc, X[g * LDT + q], Y[g * LDT + q]);
+  dmma(acc, X[g * LDT + 4 + q], Y[g * LDT + 4 + q]);
+}
+// acc += X Y
+__device__ __forceinline__ void blk_mma_nn(double (&acc)[2], const double *X, const double *Y) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  dmma(acc, X[g * LDT + q], Y[q * LDT + g]);
+  dmma(acc, X[g * LDT + 4 + q], Y[(4 + q) * LDT + g]);
+}
+
+// acc -= X Y^T with acc holding C on entry: the DMMA accumulates onto C directly
+// (negated A operand), so no FP64 ALU op waits on the tensor-pipe result
+__device__ __forceinline__ void blk_mma_nt_sub(double (&acc)[2], const double *X, const double *Y) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  dmma(acc, -X[g * LDT + q], Y[g * LDT + q]);
+  dmma(acc, -X[g * LDT + 4 + q], Y[g * LDT + 4 + q]);
+}
+
+// Cholesky + inverse of one 8 x 8 block in place (one converged warp, registers +
+// shuffles): Ab <- L (strict upper zeroed), Zb <- Z = L^{-1}, dv8[j] <- pivot j.
+// Right-looking elimination with the row operations mirrored on Z = I (see
+// leaf_chol16 for the algebra: M A = L^T, Z = D^{-1/2} M = L^{-1}).  The next
+// pivot d' = A[p+1][p+1] - A[p+1][p]^2 / d is formed from two values shuffled
+// before pivot p's update, so the serial chain per pivot is one FMA and one
+// reciprocal; the column / Z updates run beside it.
+__device__ __forceinline__ void leaf_chol8(double *Ab, double *Zb, double *dv8) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  double a0 = Ab[g * LDT + 2 * q], a1 = Ab[g * LDT + 2 * q + 1];
+  double z0 = (g == 2 * q) ? 1.0 : 0.0, z1 = (g == 2 * q + 1) ? 1.0 : 0.0;
+  double dmine = 1.0;
+  double d = __shfl_sync(FULL, a0, 0);
+  double id = rcp_nr(d);
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int sq = p >> 1;
+    const double ap = (p & 1) ? a1 : a0;
+    double x = 0.0, y = 1.0;
+    if (p < 7) {  // compile-time
+      const int p1 = p + 1;
+      x = __shfl_sync(FULL, ap, 4 * p1 + sq);                               // A[p+1][p]
+      y = __shfl_sync(FULL, (p1 & 1) ? a1 : a0, 4 * p1 + (p1 >> 1));        // A[p+1][p+1]
+    }
+    const double ai = __shfl_sync(FULL, ap, 4 * g + sq);        // A[g][p]
+    const double aj0 = __shfl_sync(FULL, ap, 8 * q + sq);       // A[2q][p]
+    const double aj1 = __shfl_sync(FULL, ap, 8 * q + 4 + sq);   // A[2q+1][p]
+    const double zp0 = __shfl_sync(FULL, z0, 4 * p + q);        // Z[p][2q]
+    const double zp1 = __shfl_sync(FULL, z1, 4 * p + q);        // Z[p][2q+1]
+    const double dn = fma(-(x * x), id, y);
+    const double idn = rcp_nr(dn);
+    const double f = ai * id;
+    const bool below = g > p;
+    a0 = (below && 2 * q > p) ? fma(-f, aj0, a0) : a0;
+    a1 = (below && 2 * q + 1 > p) ? fma(-f, aj1, a1) : a1;
+    z0 = below ? fma(-f, zp0, z0) : z0;
+    z1 = below ? fma(-f, zp1, z1) : z1;
+    const double rs = rsqrt_nr(d);
+    const double lcol = below ? ai * rs : ((g == p) ? d * rs : 0.0);  // column p of L
+    if (p & 1) {
+      a1 = (q == sq) ? lcol : a1;
+    } else {
+      a0 = (q == sq) ? lcol : a0;
+    }
+    z0 = (g == p) ? z0 * rs : z0;
+    z1 = (g == p) ? z1 * rs : z1;
+    dmine = (lane == p) ? d : dmine;
+    d = dn;
+    id = idn;
+  }
+  Ab[g * LDT + 2 * q] = a0;
+  Ab[g * LDT + 2 * q + 1] = a1;
+  Zb[g * LDT + 2 * q] = z0;
+  Zb[g * LDT + 2 * q + 1] = z1;
+  if (lane < 8) dv8[lane] = dmine;
+}
+
+// Cholesky L and inverse W = L^{-1} of the 64 x 64 tile St (rows / columns >= m
+// padded with the identity) on 8 x 8 blocks, software-pipelined across warps so
+// the serial chain is just the 8 leaves.  Step k (k = 0..7), after a CTA barrier:
+//   warp 0 (critical): L(k,k-1) = A(k,k-1) Z_{k-1}^T (published to the workers
+//     through a named barrier), A(k,k) -= L(k,k-1) L(k,k-1)^T, leaf_chol8(k);
+//   warps 1-7: the panel L(i,k-1) = A(i,k-1) Z_{k-1}^T (i > k), then the
+//     trailing update A(i,j) -= L(i,k-1) L(j,k-1)^T (k <= j <= i, (i,j) != (k,k))
+//     and block row k-1 of W: W(k-1,j) = -Z_{k-1} sum_{l=j}^{k-2} L(k-1,l) W(l,j).
+// The last block row of W follows the final step.  Writes L (strict upper
+// zeroed) to St, W to Wt (must be zero on entry), pivots to dv[0..63].
+__device__ void chol8_pipelined(double *St, double *Wt, double *S2, double *dv, int m) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int idx = tid; idx < SERINV_TILE * SERINV_TILE; idx += NT) {
+    const int i = idx >> 6, j = idx & 63;
+    if (i >= m || j >= m) St[i * LDT + j] = (i == j) ? 1.0 : 0.0;
+  }
+  double *scr = S2 + 8 * warp * LDT;  // per-warp 8 x 8 scratch
+  auto blk = [](double *T, int i, int j) { return T + 8 * i * LDT + 8 * j; };
+  // W(r,j) = -Z_r sum_{l=j}^{r-1} L(r,l) W(l,j), one block per call
+  auto wblock = [&](int r, int j) {
+    double t[2] = {0.0, 0.0};
+    for (int l = j; l < r; ++l) blk_mma_nn(t, blk(St, r, l), blk(Wt, l, j));
+    blk_store(scr, t);
+    __syncwarp();
+    double w[2] = {0.0, 0.0};
+    {
+      const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+      const double *Z = blk(Wt, r, r);
+      dmma(w, -Z[g * LDT + q], scr[q * LDT + g]);
+      dmma(w, -Z[g * LDT + 4 + q], scr[(4 + q) * LDT + g]);
+    }
+    __syncwarp();
+    blk_store(blk(Wt, r, j), w);
+  };
+  for (int k = 0; k < 8; ++k) {
+    __syncthreads();
+    if (__all_sync(0xffffffffu, warp == 0)) {
+      double *Akk = blk(St, k, k);
+      if (k > 0) {
+        double l[2] = {0.0, 0.0};
+        blk_mma_nt(l, blk(St, k, k - 1), blk(Wt, k - 1, k - 1));
+        blk_store(blk(St, k, k - 1), l);
+        __syncwarp();
+        asm volatile("bar.arrive 1, 256;" ::: "memory");
+        double a[2];
+        blk_load(Akk, a);
+        blk_mma_nt_sub(a, blk(St, k, k - 1), blk(St, k, k - 1));
+        blk_store(Akk, a);
+        __syncwarp();
+      }
+      leaf_chol8(Akk, blk(Wt, k, k), dv + 8 * k);
+    } else if (k > 0) {
+      const int wk = warp - 1;  // 0..6
+      const int ip = k + 1 + wk;
+      if (ip < 8) {  // panel block (ip, k-1)
+        double l[2] = {0.0, 0.0};
+        blk_mma_nt(l, blk(St, ip, k - 1), blk(Wt, k - 1, k - 1));
+        blk_store(blk(St, ip, k - 1), l);
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      // trailing update by column k-1: blocks (i, j), k <= j <= i <= 7, except (k, k);
+      // this warp's (at most 4) blocks: all operands loaded, then all DMMAs, then stores
+      int bi[4], bj[4], nb = 0, idx = 0;
+      for (int j = k; j < 8; ++j)
+        for (int i = j; i < 8; ++i) {
+          if (i == k && j == k) continue;
+          if (idx++ % 7 == wk && nb < 4) {
+            bi[nb] = i;
+            bj[nb] = j;
+            ++nb;
+          }
+        }
+      double acc[4][2];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t < nb) blk_load(blk(St, bi[t], bj[t]), acc[t]);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t < nb) blk_mma_nt_sub(acc[t], blk(St, bi[t], k - 1), blk(St, bj[t], k - 1));
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t < nb) blk_store(blk(St, bi[t], bj[t]), acc[t]);
+      // block row k-1 of W (blocks j < k-1), round-robin after the updates
+      for (int j = 0; j < k - 1; ++j)
+        if ((idx + j) % 7 == wk) wblock(k - 1, j);
+    }
+  }
+  __syncthreads();
+  if (warp < 7) wblock(7, warp);  // last block row of W
+  for (int idx = tid; idx < SERINV_TILE * SERINV_TILE; idx += NT) {  // strict-upper blocks of L
+    const int i = idx >> 6, j = idx & 63;
+    if ((j >> 3) > (i >> 3)) St[i * LDT + j] = 0.0;
+  }
+  __syncthreads();
+}
+
 // Diagonal-tile task: optional fused pre-update (GEMM), Cholesky (factor) of the
 // 64 x 64 tile, its inverse W = L^{-1}, log-det partial, info, and the fused TRSM
 // of the sub-diagonal tile (next link of the critical chain).
@@ -934,7 +1124,12 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   if (tid == 0) s_bad = 1 << 30;
   __syncthreads();
   phase_mark(p, tsk, 0);
-  if (factor) {
+  const bool chol8 = factor && (T.flags & TF_CHOL8);
+  if (chol8) {
+    chol8_pipelined(St, Wt, S2, dv, m);
+    if (tid < m && !(dv[tid] > 0.0)) atomicMin(&s_bad, tid);
+    __syncthreads();
+  } else if (factor) {
     // Left-looking over 16-column blocks.  Per block: (1) DMMA update of the
     // block columns from the finished columns to the left, (2) one warp factors
     // and inverts the 16 x 16 diagonal block in registers (leaf_chol16, no CTA
@@ -1027,7 +1222,7 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   }
   __syncthreads();
   // ---- off-diagonal blocks, level d = i - j
-  for (int d = 1; d < 4; ++d) {
+  for (int d = 1; d < (chol8 ? 1 : 4); ++d) {  // chol8: W is complete
     const int bj = warp, bi = warp + d;
     if (bi < 4 && 16 * bi < m) {
       double acc[2][2][2] = {};

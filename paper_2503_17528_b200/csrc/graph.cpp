@@ -29,6 +29,8 @@
 
 namespace serinv {
 
+int reduced_size(int P, bool tw);
+
 namespace {
 
 constexpr int URGENT_QUEUE = 1 << 20;  // placeholder id, renumbered to ncrit + 1 in finalize
@@ -99,8 +101,11 @@ struct Ctx {
   std::map<std::tuple<int32_t, int64_t, int, int>, int32_t> xrc;  // final-X row/col tile counters by location
   std::vector<int32_t> potrf_ctrs;                                  // every factor-done counter (LOGDET waits)
   std::vector<Wait> ext_default;     // external waits added to every task emitted while set
-  std::vector<std::pair<int32_t, int>> fin;  // streaming IO: per node, counter of its final-X tasks
+  std::vector<std::pair<int32_t, int>> fin;  // streaming IO: per node, counter of its final-X tasks + block (-1 tip)
   int32_t arr_ctr = -1;                      // streaming IO: blocks-arrived counter (external)
+  int32_t arr_ctr2 = -1;                     // twisted streaming IO: bottom units arrived
+  int64_t twist_m = -1;
+  std::map<int32_t, double> ext_ns;          // scheduler model: ns per unit of an external counter
   std::vector<char> is_ext;          // counter written by a stream (no producer task)
 
   int32_t new_ctr() { return nctr++; }
@@ -405,7 +410,7 @@ struct Builder {
         rt.t.nseg1 = (int32_t)rt.segs.size();
         if (st.last >= 0) rt.waits.push_back(cx.ctr_of(st.last));
         for (int32_t iw : input_waits) rt.waits.push_back(iw);
-        rt.t.flags = TF_W_OUT;
+        rt.t.flags = TF_W_OUT | (cx.opt.chol8 ? TF_CHOL8 : 0);
         rt.t.out2 = tileloc(P.W[X], c, c);
         rt.t.aux0 = (int32_t)(P.slot[X] + c);
         rt.t.r = wsloc(cx.slot_region + P.slot[X] + c, 0);
@@ -930,13 +935,26 @@ Graph Ctx::finalize() {
     };
     std::priority_queue<int, std::vector<int>, decltype(cmp)> ready(cmp);
     typedef std::pair<double, int> Ev;
-    std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> ev;
+    std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> ev, rel;
+    // streaming IO: a task waiting on an external (stream-written) counter is not
+    // released before its input units can have arrived (target x ns per unit)
+    std::vector<double> release(N, 0.0);
+    if (!ext_ns.empty())
+      for (int i = 0; i < N; ++i)
+        for (const Wait &w : tasks[i].ext) {
+          auto it = ext_ns.find(w.ctr);
+          if (it != ext_ns.end()) release[i] = std::max(release[i], w.target * it->second);
+        }
+    double now = 0;
+    auto make_ready = [&](int t) {
+      if (release[t] > now) rel.push({release[t], t});
+      else ready.push(t);
+    };
     for (int i = 0; i < N; ++i) tdeg[i] = (int32_t)tasks[i].waits.size();
     cdeg = nprod;
     for (int i = 0; i < N; ++i)
-      if (!tdeg[i]) ready.push(i);
+      if (!tdeg[i]) make_ready(i);
     int free_w = std::max(1, opt.grid);
-    double now = 0;
     while ((int)order.size() < N) {
       while (free_w > 0 && !ready.empty()) {
         int t = ready.top();
@@ -945,7 +963,13 @@ Graph Ctx::finalize() {
         ev.push({now + tasks[t].cost, t});
         --free_w;
       }
-      if (ev.empty()) break;
+      if (ev.empty() && rel.empty()) break;
+      if (!rel.empty() && (ev.empty() || rel.top().first <= ev.top().first)) {
+        now = std::max(now, rel.top().first);
+        ready.push(rel.top().second);
+        rel.pop();
+        continue;
+      }
       Ev e = ev.top();
       ev.pop();
       now = e.first;
@@ -953,7 +977,7 @@ Graph Ctx::finalize() {
       for (int32_t s : tasks[e.second].sigs)
         if (--cdeg[s] == 0)
           for (int64_t k = wptr[s]; k < wptr[s + 1]; ++k)
-            if (--tdeg[wlist[k]] == 0) ready.push(wlist[k]);
+            if (--tdeg[wlist[k]] == 0) make_ready(wlist[k]);
     }
     if ((int)order.size() != N) {
       g.error = "schedule incomplete";
@@ -1009,8 +1033,13 @@ Graph Ctx::finalize() {
   g.grid = opt.grid;
   g.ws_doubles = ws_top;
   g.nslots = slot_count;
-  for (auto &f : fin) g.fin.push_back(Wait{f.first, nprod[f.first]});
+  for (auto &f : fin) {
+    g.fin.push_back(Wait{f.first, nprod[f.first]});
+    g.fin_blk.push_back(f.second);
+  }
   g.arr_ctr = arr_ctr;
+  g.arr_ctr2 = arr_ctr2;
+  g.twist_m = twist_m;
   return g;
 }
 
@@ -1156,8 +1185,12 @@ struct Twist {
 // the factorisation: the chain has n * b / 64 tile steps of ~30 us, the work
 // ~7/3 n b^3 flops (+ the overlapped inversion precompute).  For b >= 2048 the
 // one-sided chain already hides under the work (C3), so keep Alg. 1's order.
+// scheduler model of the host -> device stream: one unit (diag + lower + arrow
+// block) per ~unit bytes / 50 GB/s (PCIe 5 x16, pinned)
+double h2d_ns_per_unit(int64_t b, int64_t a) { return (double)(2 * b * b + a * b) * 8.0 / 50.0; }
+
 bool use_twist(int kind, int64_t n, int64_t b, const BuildOptions &opt) {
-  return kind == 2 && opt.twist_min_n > 0 && n >= std::max(3, opt.twist_min_n) && b <= opt.twist_max_b;
+  return (kind == 2 || kind == 6) && opt.twist_min_n > 0 && n >= std::max(3, opt.twist_min_n) && b <= opt.twist_max_b;
 }
 
 void twisted_problem(Ctx &cx, Problem &P, Twist &tw, int64_t n, int64_t b, int64_t a) {
@@ -1206,7 +1239,10 @@ void twisted_problem(Ctx &cx, Problem &P, Twist &tw, int64_t n, int64_t b, int64
   }
 }
 
-Graph build_twisted_selinv(Ctx &cx, int64_t n, int64_t b, int64_t a) {
+// stream_io (kind 6): the host streams units in from both ends (top units
+// 0..m on arr_ctr, bottom units n-1..m+1 on arr_ctr2) and each node's outputs
+// out as soon as its final-X counter completes (fin, in completion order).
+Graph build_twisted_selinv(Ctx &cx, int64_t n, int64_t b, int64_t a, bool stream_io) {
   cx.slot_cap = slot_bound(n, b, a);
   cx.slot_region = cx.alloc(cx.slot_cap);
   Problem P;
@@ -1216,33 +1252,68 @@ Graph build_twisted_selinv(Ctx &cx, int64_t n, int64_t b, int64_t a) {
   bld.concurrency = 2;
   bld.allocate(true);
   const int nn = (int)P.size.size();
+  const int64_t m = tw.m;
+  if (stream_io) {
+    cx.arr_ctr = cx.new_ext_ctr();
+    cx.arr_ctr2 = cx.new_ext_ctr();
+    cx.twist_m = m;
+    cx.ext_ns[cx.arr_ctr] = cx.ext_ns[cx.arr_ctr2] = 2.0 * h2d_ns_per_unit(b, a);  // the two sides alternate
+  }
+  // arrival waits: top block i (<= m) present iff arr_ctr >= i + 1, bottom block j
+  // (> m, with lower[j-1]) iff arr_ctr2 >= n - j
+  auto need = [&](std::vector<Wait> &w, int64_t blk) {
+    if (!stream_io) return;
+    if (blk <= m) w.push_back(Wait{cx.arr_ctr, (int32_t)(blk + 1)});
+    else w.push_back(Wait{cx.arr_ctr2, (int32_t)(n - blk)});
+  };
   std::vector<int32_t> tin(n, -1);
-  for (int64_t j = tw.m + 1; j < n; ++j) {  // T(j) = A_{j,j-1}^T
+  for (int64_t j = m + 1; j < n; ++j) {  // T(j) = A_{j,j-1}^T
     tin[j] = cx.new_ctr();
-    cx.copy_block(tw.T.at(j - tw.m - 1), famL(b).at(j - 1), (int)b, (int)b, true, {}, {tin[j]});
+    cx.ext_default.clear();
+    need(cx.ext_default, j);
+    cx.copy_block(tw.T.at(j - m - 1), famL(b).at(j - 1), (int)b, (int)b, true, {}, {tin[j]});
   }
   std::vector<int64_t> blk_of(nn, -1);
   for (int64_t i = 0; i < n; ++i) blk_of[tw.pos[i]] = i;
   for (int X = 0; X < nn; ++X) {
     bld.input_waits.clear();
-    if (blk_of[X] > tw.m) bld.input_waits.push_back(tin[blk_of[X]]);
+    cx.ext_default.clear();
+    const int64_t i = blk_of[X];
+    if (i > m) bld.input_waits.push_back(tin[i]);
+    if (i >= 0) {  // the column of block i reads blocks i and its chain successor
+      need(cx.ext_default, i);
+      if (i < m) need(cx.ext_default, i + 1);
+      if (i > m) need(cx.ext_default, i - 1);
+    } else {
+      need(cx.ext_default, m);
+    }
     bld.factor_node(X);
   }
+  cx.ext_default.clear();
   bld.input_waits.clear();
   cx.logdet(Loc{BUF_LOGDET, 0, 0}, 0, cx.slot_count, Loc{BUF_WS, 0, 0}, 0, 0, {});
   for (int X = 0; X < nn; ++X) bld.precompute_node(X, true);
-  for (int X = nn - 1; X >= 0; --X) bld.invert_node(X);
-  for (int64_t j = tw.m + 1; j < n; ++j) {  // X_{j,j-1} = T(j)^T
-    const Loc src = tw.T.at(j - tw.m - 1);
-    std::vector<int32_t> w;
-    for (int q = 0; q < ntiles(b); ++q) w.push_back(cx.XRC(src, q, 0));
-    cx.copy_block(famL(b).at(j - 1), src, (int)b, (int)b, true, w, {});
+  for (int X = nn - 1; X >= 0; --X) {
+    const int64_t i = blk_of[X];
+    if (stream_io) {
+      bld.fin_ctr = cx.new_ctr();
+      cx.fin.push_back({bld.fin_ctr, (int)i});
+    }
+    bld.invert_node(X);
+    if (i > m) {  // X_{i,i-1} = T(i)^T
+      const Loc src = tw.T.at(i - m - 1);
+      std::vector<int32_t> w;
+      for (int q = 0; q < ntiles(b); ++q) w.push_back(cx.XRC(src, q, 0));
+      std::vector<int32_t> s;
+      if (bld.fin_ctr >= 0) s.push_back(bld.fin_ctr);
+      cx.copy_block(famL(b).at(i - 1), src, (int)b, (int)b, true, w, s);
+    }
   }
   return cx.finalize();
 }
 
 Graph build_seq_ctx(Ctx &cx, int kind, int64_t n, int64_t b, int64_t a) {
-  if (use_twist(kind, n, b, cx.opt)) return build_twisted_selinv(cx, n, b, a);
+  if (use_twist(kind, n, b, cx.opt)) return build_twisted_selinv(cx, n, b, a, kind == 6);
   bool fact = kind != 1, inv = kind != 0;  // kinds 2 and 6 (selinv, streaming IO) do both
   cx.slot_cap = slot_bound(n, b, a);
   cx.slot_region = cx.alloc(cx.slot_cap);
@@ -1257,7 +1328,10 @@ Graph build_seq_ctx(Ctx &cx, int kind, int64_t n, int64_t b, int64_t a) {
   bld.allocate(inv);
   int nn = (int)P.size.size();
   const bool stream_io = kind == 6;
-  if (stream_io) cx.arr_ctr = cx.new_ext_ctr();
+  if (stream_io) {
+    cx.arr_ctr = cx.new_ext_ctr();
+    cx.ext_ns[cx.arr_ctr] = h2d_ns_per_unit(b, a);
+  }
   if (fact) {
     for (int X = 0; X < nn; ++X) {
       // streaming IO: the column of node X reads blocks X and X+1 (counted in blocks arrived)
@@ -1272,7 +1346,7 @@ Graph build_seq_ctx(Ctx &cx, int kind, int64_t n, int64_t b, int64_t a) {
     for (int X = nn - 1; X >= 0; --X) {
       if (stream_io) {
         bld.fin_ctr = cx.new_ctr();
-        cx.fin.push_back({bld.fin_ctr, X});
+        cx.fin.push_back({bld.fin_ctr, X < (int)n ? X : -1});
       }
       bld.invert_node(X);
     }
@@ -1296,7 +1370,48 @@ struct PartState {
   int queue = 1;              // critical claim queue of this partition's chain (0: bulk)
   View V;                     // the matrix this partition belongs to
   std::vector<int32_t> inw;   // counters after which the partition's input blocks are ready
+  bool bottom = false;        // twisted last partition: eliminated bottom-up, no fill-in (reading R14)
+  Fam Tbuf{};                 // bottom: T(j) = A_{j,j-1}^T at Tbuf.at(j - s - 1), j = s+1..e-1
 };
+
+// The last partition, eliminated bottom-up (reading R14): the block-reversed
+// BTA chain of blocks e-1, e-2, ..., s+1, with block s (its first block) left as
+// the boundary node and the arrow node accumulating U_p.  Node k <-> block e-1-k
+// (k < cnt-1), node cnt-1 <-> block s, node cnt = arrow.  Couplings A_{j-1,j} =
+// A_{j,j-1}^T live transposed in Tbuf (row-major factor / inverse storage).
+void bottom_problem(Problem &P, const View &V, int64_t ls, int64_t cnt, int64_t b, int64_t a, Loc U, const Fam &Tb,
+                    int64_t glob_s) {
+  const int nb = (int)cnt;  // nodes 0..cnt-1 = blocks e-1 .. s
+  const int A = nb;
+  const int nn = nb + (a > 0 ? 1 : 0);
+  P.size.assign(nn, (int)b);
+  if (a > 0) P.size[A] = (int)a;
+  P.elim.assign(nn, 0);
+  for (int k = 0; k + 1 < nb; ++k) P.elim[k] = 1;
+  P.accum.assign(nn, 0);
+  if (a > 0) P.accum[A] = 1;
+  P.rowbase.resize(nn);
+  P.rows.assign(nn, {});
+  for (int k = 0; k < nb; ++k) {
+    const int64_t j = glob_s + (cnt - 1 - k);   // global block of node k
+    const int64_t lj = ls + (cnt - 1 - k);      // local index
+    P.rowbase[k] = V.row(j);
+    P.blk[{k, k}] = blkref(V.D.at(lj), (int)b, (int)b);
+    const bool el = k + 1 < nb;
+    if (el) {  // successor: block j-1 = node k+1, coupling A_{j-1,j} = T(j)
+      P.blk[{k + 1, k}] = blkref(Tb.at(j - glob_s - 1), (int)b, (int)b);
+      P.rows[k].push_back(k + 1);
+    }
+    if (a > 0) {
+      P.blk[{A, k}] = blkref(V.Ar.at(lj), (int)a, (int)b);
+      if (el) P.rows[k].push_back(A);
+    }
+  }
+  if (a > 0) {
+    P.rowbase[A] = -1;
+    P.blk[{A, A}] = blkref(U, (int)a, (int)a, true);
+  }
+}
 
 // PPOBTAF for one partition (Alg. 3 line 3 / line 5): factor the interior and
 // flush the Schur updates into the boundary blocks, U_p and (middle) B_{e-1}.
@@ -1304,7 +1419,10 @@ void ppobtaf_part(Ctx &cx, PartState &ps, int64_t b, int64_t a) {
   bool top = ps.p == 0;
   int64_t cnt = ps.e - ps.s;
   ps.U = wsloc(cx.alloc(std::max<int64_t>(a * a, 1)), std::max<int64_t>(a, 1));
-  if (top) {
+  if (ps.bottom) {
+    ps.Tbuf = Fam{BUF_WS, cx.alloc(std::max<int64_t>(cnt - 1, 1) * b * b), b * b, (int32_t)b};
+    bottom_problem(ps.prob, ps.V, ps.ls, cnt, b, a, ps.U, ps.Tbuf, ps.s);
+  } else if (top) {
     int64_t ls = ps.ls;
     const View &V = ps.V;
     chain_problem(
@@ -1321,7 +1439,15 @@ void ppobtaf_part(Ctx &cx, PartState &ps, int64_t b, int64_t a) {
   Builder &B = *ps.bld;
   B.input_waits = ps.inw;
   B.allocate(true);
-  if (!top) {  // B_{s+1} = A_{s+1,s}^T (Alg. 4 line 1, reading R7)
+  std::vector<int32_t> tin;
+  if (ps.bottom) {  // T(j) = A_{j,j-1}^T, j = s+1..e-1 (node k = e-1-j needs T(j))
+    for (int64_t j = ps.s + 1; j < ps.e; ++j) {
+      int32_t c = cx.new_ctr();
+      cx.copy_block(ps.Tbuf.at(j - ps.s - 1), ps.V.Lo.at(ps.ls + (j - 1 - ps.s)), (int)b, (int)b, true, ps.inw, {c});
+      tin.push_back(c);
+      ps.done.push_back(c);
+    }
+  } else if (!top) {  // B_{s+1} = A_{s+1,s}^T (Alg. 4 line 1, reading R7)
     int32_t c = cx.new_ctr();
     cx.copy_block(ps.Bbuf.at(0), ps.V.Lo.at(ps.ls), (int)b, (int)b, true, ps.inw, {c});
     B.input_waits.push_back(c);
@@ -1329,9 +1455,14 @@ void ppobtaf_part(Ctx &cx, PartState &ps, int64_t b, int64_t a) {
   }
   for (size_t X = 0; X < ps.prob.size.size(); ++X)
     if (ps.prob.elim[X]) {
+      if (ps.bottom) {  // node X = block e-1-X reads T(e-1-X)
+        B.input_waits = ps.inw;
+        B.input_waits.push_back(tin[(size_t)(ps.e - 1 - (int64_t)X - ps.s - 1)]);
+      }
       B.factor_node((int)X);
       ++ps.nelim;
     }
+  if (ps.bottom) B.input_waits = ps.inw;
   B.flush_boundary(ps.done);
   if (a > 0 && ps.nelim == 0) {  // U_p = 0 when nothing is eliminated
     int32_t z = cx.new_ctr();
@@ -1364,6 +1495,9 @@ void pack_part(Ctx &cx, PartState &ps, int P, int64_t b, int64_t a, int32_t rbuf
   if (ps.p == 0) {
     cx.copy_block(rec(x.bd0(), b), V.D.at(ls + cnt - 1), (int)b, (int)b, false, w, {sig});
     if (a > 0) cx.copy_block(rec(x.ar0(), b), V.Ar.at(ls + cnt - 1), (int)a, (int)b, false, w, {sig});
+  } else if (ps.bottom) {  // boundary block s only
+    cx.copy_block(rec(x.bd0(), b), V.D.at(ls), (int)b, (int)b, false, w, {sig});
+    if (a > 0) cx.copy_block(rec(x.ar0(), b), V.Ar.at(ls), (int)a, (int)b, false, w, {sig});
   } else {
     cx.copy_block(rec(x.bd0(), b), V.D.at(ls), (int)b, (int)b, false, w, {sig});
     cx.copy_block(rec(x.bd1(), b), V.D.at(ls + cnt - 1), (int)b, (int)b, false, w, {sig});
@@ -1389,11 +1523,12 @@ struct Reduced {
 // Assemble A_r (2P-1 blocks, reading R9) from the P records at (rbuf, rec0 +
 // p*recsz), then POBTARSSI = POBTAF + POBTASI on it (Sec. 3.3).  The reduced tip
 // A_nn + U_0 + ... + U_{P-1} (reading R8) is formed in place in BUF_TIP.
+
 void assemble_reduced(Ctx &cx, const View &V0, int P, int64_t b, int64_t a, int32_t rbuf, int64_t rec0,
                       int64_t recsz, const std::vector<int64_t> &starts, const std::vector<int32_t> &inwaits,
-                      Reduced &R) {
+                      Reduced &R, bool tw) {
   XRec x{b, a};
-  int nr = 2 * P - 1;
+  int nr = reduced_size(P, tw);
   R.D = Fam{BUF_WS, cx.alloc(nr * b * b), b * b, (int32_t)b};
   R.Lo = Fam{BUF_WS, cx.alloc(std::max(nr - 1, 1) * b * b), b * b, (int32_t)b};
   R.Ar = Fam{BUF_WS, cx.alloc(std::max<int64_t>(nr * a * b, 1)), a * b, (int32_t)b};
@@ -1403,6 +1538,12 @@ void assemble_reduced(Ctx &cx, const View &V0, int P, int64_t b, int64_t a, int3
   cx.copy_block(R.D.at(0), rec(0, x.bd0(), b), (int)b, (int)b, false, inwaits, {cr});
   if (a > 0) cx.copy_block(R.Ar.at(0), rec(0, x.ar0(), b), (int)a, (int)b, false, inwaits, {cr});
   for (int p = 1; p < P; ++p) {
+    if (tw && p == P - 1) {  // twisted last partition: its boundary block s only (reading R14)
+      cx.copy_block(R.D.at(2 * p - 1), rec(p, x.bd0(), b), (int)b, (int)b, false, inwaits, {cr});
+      if (a > 0) cx.copy_block(R.Ar.at(2 * p - 1), rec(p, x.ar0(), b), (int)a, (int)b, false, inwaits, {cr});
+      cx.copy_block(R.Lo.at(2 * p - 2), rec(p - 1, x.lw0(), b), (int)b, (int)b, false, inwaits, {cr});
+      continue;
+    }
     cx.copy_block(R.D.at(2 * p - 1), rec(p, x.bd0(), b), (int)b, (int)b, false, inwaits, {cr});
     cx.copy_block(R.D.at(2 * p), rec(p, x.bd1(), b), (int)b, (int)b, false, inwaits, {cr});
     if (a > 0) {
@@ -1454,9 +1595,9 @@ void solve_reduced_chain(Ctx &cx, int64_t b, int64_t a, int nr, Reduced &R) {
 
 void reduced_from_records(Ctx &cx, const View &V0, int P, int64_t b, int64_t a, int32_t rbuf, int64_t rec0,
                           int64_t recsz, const std::vector<int64_t> &starts, const std::vector<int32_t> &inwaits,
-                          Reduced &R) {
-  assemble_reduced(cx, V0, P, b, a, rbuf, rec0, recsz, starts, inwaits, R);
-  solve_reduced_chain(cx, b, a, 2 * P - 1, R);
+                          Reduced &R, bool tw) {
+  assemble_reduced(cx, V0, P, b, a, rbuf, rec0, recsz, starts, inwaits, R, tw);
+  solve_reduced_chain(cx, b, a, reduced_size(P, tw), R);
 }
 
 // Copy the true-inverse boundary blocks of partition ps from X_r into its
@@ -1477,6 +1618,10 @@ void scatter_xr(Ctx &cx, PartState &ps, int P, int64_t b, int64_t a, const Reduc
     int T = (int)(ps.e - ps.s) - 1;
     cp(Q.blk.at({T, T}).base, R.D.at(0), (int)b, (int)b, false);
     if (a > 0) cp(Q.blk.at({nn - 1, T}).base, R.Ar.at(0), (int)a, (int)b, false);
+  } else if (ps.bottom) {  // boundary block s = node cnt-1
+    int S = (int)(ps.e - ps.s) - 1;
+    cp(Q.blk.at({S, S}).base, R.D.at(2 * p - 1), (int)b, (int)b, false);
+    if (a > 0) cp(Q.blk.at({nn - 1, S}).base, R.Ar.at(2 * p - 1), (int)a, (int)b, false);
   } else {
     int k = (int)(ps.e - ps.s) - 1, F = k, L = k - 1;
     cp(Q.blk.at({F, F}).base, R.D.at(2 * p - 1), (int)b, (int)b, false);
@@ -1501,7 +1646,16 @@ void ppobtasi_part(Ctx &cx, PartState &ps, int64_t b, bool have_wdiag) {
     if (ps.prob.elim[X]) B.precompute_node(X, have_wdiag);
   for (int X = nn - 1; X >= 0; --X)
     if (ps.prob.elim[X]) B.invert_node(X);
-  if (ps.p > 0) {  // X_{s+1,s} = Q_{s+1}^T (reading R10)
+  if (ps.bottom) {  // X_{j,j-1} = T(j)^T, j = s+1..e-1
+    for (int64_t j = ps.s + 1; j < ps.e; ++j) {
+      const Loc src = ps.Tbuf.at(j - ps.s - 1);
+      std::vector<int32_t> w;
+      for (int q = 0; q < ntiles(b); ++q) w.push_back(cx.XRC(src, q, 0));
+      const Loc dst = ps.V.Lo.at(ps.ls + (j - 1 - ps.s));
+      cx.copy_block(dst, src, (int)b, (int)b, true, w, {},
+                    [&](RawTask &rt, int q, int c) { cx.sig_xblock(rt, dst, q, c); });
+    }
+  } else if (ps.p > 0) {  // X_{s+1,s} = Q_{s+1}^T (reading R10)
     std::vector<int32_t> w;
     for (int q = 0; q < ntiles(b); ++q) w.push_back(cx.XRC(ps.Bbuf.at(0), q, 0));
     const Loc dst = ps.V.Lo.at(ps.ls);
@@ -1571,6 +1725,8 @@ void BuildOptions::apply_env() {
       else if (k == "twist_min_n") twist_min_n = (int)v;
       else if (k == "twist_max_b") twist_max_b = (int)v;
       else if (k == "wide_min_wave") wide_min_wave = (int)v;
+      else if (k == "chol8") chol8 = v != 0;
+      else if (k == "twist_last") twist_last = v != 0;
     }
     i = j + 1;
   }
@@ -1600,6 +1756,8 @@ Graph build_gemm_bench(int ntasks, int k, int nseg, const BuildOptions &opt) {
   }
   return cx.finalize();
 }
+
+int reduced_size(int P, bool tw) { return tw && P >= 2 ? 2 * P - 2 : 2 * P - 1; }
 
 bool plan_partitions(int64_t n, int P, double r, std::vector<int64_t> &starts) {
   starts.clear();
@@ -1639,6 +1797,7 @@ bool psolve_level(Ctx &cx, const View &V, int64_t n, int64_t b, int64_t a, const
   std::vector<PartState> parts(P);
   // exclusive-SM chains only for a few top-level partitions (each takes two SMs)
   const bool crit = lvl == 0 && 2 * P <= cx.opt.max_crit;
+  const bool tw = cx.opt.twist_last && P >= 2;
   for (int p = 0; p < P; ++p) {
     parts[p].p = p;
     parts[p].s = starts[p];
@@ -1647,13 +1806,14 @@ bool psolve_level(Ctx &cx, const View &V, int64_t n, int64_t b, int64_t a, const
     parts[p].queue = crit ? 2 * p + 1 : 0;
     parts[p].V = V;
     parts[p].inw = inw;
+    parts[p].bottom = tw && p == P - 1;
     ppobtaf_part(cx, parts[p], b, a);
   }
   int32_t packed = cx.new_ctr();
   for (int p = 0; p < P; ++p) pack_part(cx, parts[p], P, b, a, BUF_WS, recs + p * recsz, packed);
   Reduced R;
-  assemble_reduced(cx, V, P, b, a, BUF_WS, recs, recsz, starts, {packed}, R);
-  const int nr = 2 * P - 1;
+  assemble_reduced(cx, V, P, b, a, BUF_WS, recs, recsz, starts, {packed}, R, tw);
+  const int nr = reduced_size(P, tw);
   bool nested = lvl + 1 < Ps.size() && psolve_level(cx, R.V, nr, b, a, Ps, lvl + 1, r, R.ready);
   if (!nested) solve_reduced_chain(cx, b, a, nr, R);
   for (int p = 0; p < P; ++p) {
@@ -1686,6 +1846,7 @@ Graph build_pselinv(int64_t n, int64_t b, int64_t a, int P, double r, const Buil
 
 int64_t pselinv_ws_bytes(int64_t n, int64_t b, int64_t a, const std::vector<int> &Ps, double r) {
   BuildOptions opt;
+  opt.apply_env();  // the layout depends on options (twist_last, wide_min_wave, ...)
   opt.schedule = false;
   Graph g = build_pselinv(n, b, a, Ps, r, opt);
   return g.error.empty() ? g.ws_doubles * 8 : -1;
@@ -1708,7 +1869,7 @@ std::vector<int> auto_partitions(int64_t n, int64_t b) {
     if (P < 2) break;
     P = std::min<int64_t>(P, 4096);
     Ps.push_back((int)P);
-    m = 2 * P - 1;
+    m = reduced_size((int)P, BuildOptions().twist_last);
   }
   if (Ps.empty()) Ps.push_back(1);
   return Ps;
@@ -1734,6 +1895,8 @@ Graph build_distributed(int phase, int P, int rank, int64_t n, int64_t start, in
   ps.e = start + count;
   ps.ls = 0;
   ps.V = top_view(n, b, a);  // local storage (block `start` at index ls = 0), global rows
+  const bool tw = opt.twist_last && P >= 2;
+  ps.bottom = tw && rank == P - 1;
   ppobtaf_part(cx, ps, b, a);
   if (phase == 0) {
     int32_t packed = cx.new_ctr();
@@ -1760,7 +1923,7 @@ Graph build_distributed(int phase, int P, int rank, int64_t n, int64_t start, in
   st[0] = 0;
   st[P] = n;
   Reduced R;
-  reduced_from_records(cx, ps.V, P, b, a, BUF_EXT1, 0, recsz, st, {}, R);
+  reduced_from_records(cx, ps.V, P, b, a, BUF_EXT1, 0, recsz, st, {}, R, tw);
   scatter_xr(cx, ps, P, b, a, R);
   ppobtasi_part(cx, ps, b, false);  // W tiles recomputed by TRTRI (no fused POTRF here)
   // log det = sum of the ranks' partials (rank order) + 2 sum log diag of POBTAF(A_r)
@@ -1770,6 +1933,7 @@ Graph build_distributed(int phase, int P, int rank, int64_t n, int64_t start, in
 
 int64_t distributed_ws_bytes(int P, int rank, int64_t n, int64_t start, int64_t count, int64_t b, int64_t a) {
   BuildOptions opt;
+  opt.apply_env();
   opt.schedule = false;
   Graph g0 = build_distributed(0, P, rank, n, start, count, b, a, opt);
   Graph g1 = build_distributed(1, P, rank, n, start, count, b, a, opt);

@@ -45,6 +45,12 @@ struct Graph {
   // the nodes finish (tip first, then blocks n-1 .. 0)
   int32_t arr_ctr = -1;
   std::vector<Wait> fin;
+  std::vector<int32_t> fin_blk;   // block of fin[k] (-1: the tip)
+  // twisted streaming IO: arr_ctr counts top units (blocks 0, 1, ..., m) and
+  // arr_ctr2 bottom units (blocks n-1, n-2, ..., m+1; unit j holds diag[j],
+  // arrow[j] and lower[j-1]); twist_m = m (-1: one-sided, units in block order)
+  int32_t arr_ctr2 = -1;
+  int64_t twist_m = -1;
   int ncrit = 0;     // queues 1..ncrit: one CTA each, alone on its SM
   int nurgent = 0;   // queue ncrit+1 (if any): served by nurgent CTAs (near-critical tasks)
   std::string error;         // non-empty if building failed
@@ -96,6 +102,8 @@ struct BuildOptions {
   bool rts1_chain = false;      // the second sub-diagonal TRSM also on the chain's TRSM queue
   int max_crit = 16;            // partitioned solves: exclusive-SM chains only if 2P <= max_crit
   int twist_min_n = 4;          // selinv: two-sided (twisted) elimination if n >= twist_min_n (0: never)
+  bool twist_last = true;       // partitioned solves: the last partition eliminates bottom-up (no fill-in)
+  bool chol8 = true;            // POTRF tasks: 8 x 8-block warp-pipelined Cholesky (else 16 x 16 leaves)
   int wide_min_wave = 512;      // 128 x 64 tasks for inversion waves of >= this many tiles (0: never)
   int twist_max_b = 1024;       // ... and b <= twist_max_b (larger blocks: the one-sided chain hides under the work)
   // overrides from the environment (SERINV_OPT="key=value,..."), for tuning runs
@@ -129,6 +137,10 @@ int64_t exchange_doubles(int64_t b, int64_t a);
 
 // Diagnostic: independent tile GEMMs (engine throughput).
 Graph build_gemm_bench(int ntasks, int k, int nseg, const BuildOptions &opt);
+
+// Blocks of the reduced system of P partitions: 2P-1 (paper), 2P-2 with the
+// twisted last partition (reading R14).
+int reduced_size(int P, bool twisted_last);
 
 // Partition plan (reading R6).  Returns false if infeasible.
 bool plan_partitions(int64_t n, int P, double r, std::vector<int64_t> &starts);

@@ -40,7 +40,7 @@ struct DevGraph {
   int nq = 1;
   int ncrit = 0, nurgent = 0;
   int64_t nctr_alloc = 0;
-  int64_t ntasks = 0;
+  int64_t ntasks = 0, nwaits = 0, nsigs = 0;
   ~DevGraph() {
     if (blob) cudaFree(blob);
     if (ctr) cudaFree(ctr);
@@ -99,6 +99,8 @@ int upload(DevGraph &dg, int grid) {
   dg.nctr_alloc = (int64_t)g.nctr + dg.nq + 2 + grid;
   if (cudaMalloc(&dg.ctr, (size_t)dg.nctr_alloc * sizeof(int32_t)) != cudaSuccess) return SERINV_ERR_CUDA;
   dg.ntasks = (int64_t)g.tasks.size();
+  dg.nwaits = (int64_t)g.waits.size();
+  dg.nsigs = (int64_t)g.sigs.size();
   if (cudaGetLastError() != cudaSuccess) return SERINV_ERR_CUDA;
   // keep stats, drop the big host arrays
   std::vector<Task>().swap(g.tasks);
@@ -278,22 +280,28 @@ int serinv_destroy(serinv_handle_t h) {
   return SERINV_OK;
 }
 
+static BuildOptions env_opt() {
+  BuildOptions o;
+  o.apply_env();
+  return o;
+}
+
 int serinv_pobtaf_ws(int64_t n, int64_t b, int64_t a, size_t *bytes) {
   if (!bytes) return -4;
   if (n < 1 || b < 1 || a < 0) return SERINV_ERR_SHAPE;
-  *bytes = (size_t)sequential_ws_bytes(0, n, b, a);
+  *bytes = (size_t)sequential_ws_bytes(0, n, b, a, env_opt());
   return SERINV_OK;
 }
 int serinv_pobtasi_ws(int64_t n, int64_t b, int64_t a, size_t *bytes) {
   if (!bytes) return -4;
   if (n < 1 || b < 1 || a < 0) return SERINV_ERR_SHAPE;
-  *bytes = (size_t)sequential_ws_bytes(1, n, b, a);
+  *bytes = (size_t)sequential_ws_bytes(1, n, b, a, env_opt());
   return SERINV_OK;
 }
 int serinv_selinv_ws(int64_t n, int64_t b, int64_t a, size_t *bytes) {
   if (!bytes) return -4;
   if (n < 1 || b < 1 || a < 0) return SERINV_ERR_SHAPE;
-  *bytes = (size_t)sequential_ws_bytes(2, n, b, a);
+  *bytes = (size_t)sequential_ws_bytes(2, n, b, a, env_opt());
   return SERINV_OK;
 }
 
@@ -377,12 +385,14 @@ static int nested_key(int64_t n, int nlev, const int *Ps, double r, int64_t *mor
   if (nlev < 1 || nlev > SERINV_MAX_LEVELS || !Ps) return SERINV_ERR_PLAN;
   int64_t m = n;
   *more = 0;
+  BuildOptions opt;
+  opt.apply_env();
   for (int l = 0; l < nlev; ++l) {
     std::vector<int64_t> s;
     if (Ps[l] < 1 || Ps[l] > 0xffff || (l > 0 && Ps[l] < 2) || !plan_partitions(m, Ps[l], r, s))
       return SERINV_ERR_PLAN;
     if (l > 0) *more |= (int64_t)Ps[l] << (16 * (l - 1));
-    m = 2 * (int64_t)Ps[l] - 1;
+    m = reduced_size(Ps[l], opt.twist_last);
   }
   if (nlev > 1 && Ps[0] < 2) return SERINV_ERR_PLAN;
   return SERINV_OK;
@@ -537,24 +547,31 @@ int serinv_graph_dump(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_t
   DevGraph *dg = nullptr;
   int rc = get_graph(h, GKey(kind, n, b, a, kind == 3 ? P : 1, rb, 0, 0, 0), &dg);
   if (rc) return rc;
+  // the host arrays were dropped after upload: read the device copies back
   const Graph &g = dg->g;
-  if (nw) *nw = (int64_t)g.waits.size();
-  if (ns) *ns = (int64_t)g.sigs.size();
+  if (nw) *nw = dg->nwaits;
+  if (ns) *ns = dg->nsigs;
   if (rec) {
-    std::vector<int32_t> q(g.tasks.size(), 0);
+    std::vector<Task> tasks(dg->ntasks);
+    std::vector<int32_t> ql(dg->ntasks);
+    cudaMemcpy(tasks.data(), dg->d_tasks, tasks.size() * sizeof(Task), cudaMemcpyDeviceToHost);
+    cudaMemcpy(ql.data(), dg->d_qlist, ql.size() * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    std::vector<int32_t> q(tasks.size(), 0);
     for (size_t qq = 0; qq + 1 < g.qoff.size(); ++qq)
-      for (int32_t k = g.qoff[qq]; k < g.qoff[qq + 1]; ++k) q[g.qlist[k]] = (int32_t)qq;
-    for (size_t t = 0; t < g.tasks.size(); ++t) {
-      const Task &T = g.tasks[t];
+      for (int32_t k = g.qoff[qq]; k < g.qoff[qq + 1]; ++k) q[ql[k]] = (int32_t)qq;
+    for (size_t t = 0; t < tasks.size(); ++t) {
+      const Task &T = tasks[t];
       int32_t *o = rec + 10 * t;
       o[0] = T.type; o[1] = T.flags; o[2] = T.m; o[3] = T.n; o[4] = T.wait0; o[5] = T.nwait;
       o[6] = T.nlate; o[7] = T.sig0; o[8] = T.nsig; o[9] = q[t];
     }
   }
-  if (waits)
-    for (size_t w = 0; w < g.waits.size(); ++w) waits[w] = g.waits[w].ctr;
-  if (sigs)
-    for (size_t s = 0; s < g.sigs.size(); ++s) sigs[s] = g.sigs[s];
+  if (waits) {
+    std::vector<Wait> w(dg->nwaits);
+    cudaMemcpy(w.data(), dg->d_waits, w.size() * sizeof(Wait), cudaMemcpyDeviceToHost);
+    for (size_t k = 0; k < w.size(); ++k) waits[k] = w[k].ctr;
+  }
+  if (sigs) cudaMemcpy(sigs, dg->d_sigs, dg->nsigs * sizeof(int32_t), cudaMemcpyDeviceToHost);
   return SERINV_OK;
 }
 
@@ -603,6 +620,88 @@ static bool load_stream_memops() {
 // in order and bumps the graph's arrival counter (cuStreamWriteValue32); the
 // D2H stream waits on each node's final-X counter (cuStreamWaitValue32) and
 // copies the node's blocks back while the kernel works on earlier blocks.
+// Streaming host IO for the twisted selinv graph: units stream in from both ends
+// (top units 0..m on the arrival counter arr_ctr, bottom units n-1..m+1 on
+// arr_ctr2; bottom unit j carries lower[j-1]) and each node's outputs stream out
+// as soon as its final-X counter completes (the graph's fin list, in completion
+// order: tip, m, then both chains outwards), in contiguous per-side chunks.
+static int selinv_host_twisted(serinv_handle_t h, DevGraph &dg, const serinv_bta_t *A_host, const serinv_bta_t *X_host,
+                               const serinv_bta_t *A_dev, void *d_ws, int *d_info, double *d_logdet, cudaStream_t st,
+                               int64_t chunk) {
+  const int64_t n = A_dev->n, b = A_dev->b, a = A_dev->a, m = dg.g.twist_m;
+  const size_t bb = (size_t)b * b, ab = (size_t)a * b;
+  auto cp = [&](double *dst, const double *src, size_t doubles, cudaMemcpyKind k, cudaStream_t s) {
+    return doubles ? cudaMemcpyAsync(dst, src, doubles * 8, k, s) == cudaSuccess : true;
+  };
+  // blocks [j0, j1) of one side with their lower blocks (top: lower[j], bottom: lower[j-1])
+  auto unit_range = [&](const serinv_bta_t *dst, const serinv_bta_t *src, int64_t j0, int64_t j1, bool top,
+                        cudaMemcpyKind k, cudaStream_t s) {
+    if (j1 <= j0) return true;
+    bool ok = cp(dst->diag + j0 * bb, src->diag + j0 * bb, (j1 - j0) * bb, k, s);
+    if (a > 0) ok = ok && cp(dst->arrow + j0 * ab, src->arrow + j0 * ab, (j1 - j0) * ab, k, s);
+    const int64_t l0 = top ? j0 : j0 - 1, l1 = top ? std::min(j1, m) : j1 - 1;
+    if (l1 > l0) ok = ok && cp(dst->lower + l0 * bb, src->lower + l0 * bb, (l1 - l0) * bb, k, s);
+    return ok;
+  };
+  CUdeviceptr arr = (CUdeviceptr)(dg.ctr + dg.g.arr_ctr), arr2 = (CUdeviceptr)(dg.ctr + dg.g.arr_ctr2);
+  const int64_t nbot = n - 1 - m;
+  for (int64_t t = 0, s = 0; t <= m || s < nbot;) {
+    if (t <= m) {
+      const int64_t t1 = std::min(m + 1, t + chunk);
+      if (!unit_range(A_dev, A_host, t, t1, true, cudaMemcpyHostToDevice, h->s_in) ||
+          p_writeValue32((CUstream)h->s_in, arr, (cuuint32_t)t1, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        return SERINV_ERR_CUDA;
+      t = t1;
+    }
+    if (s < nbot) {
+      const int64_t s1 = std::min(nbot, s + chunk);
+      if (!unit_range(A_dev, A_host, n - s1, n - s, false, cudaMemcpyHostToDevice, h->s_in) ||
+          p_writeValue32((CUstream)h->s_in, arr2, (cuuint32_t)s1, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        return SERINV_ERR_CUDA;
+      s = s1;
+    }
+  }
+  double *bufs[BUF_COUNT] = {A_dev->diag, A_dev->lower, A_dev->arrow, A_dev->tip, (double *)d_ws, nullptr, nullptr,
+                             d_logdet ? d_logdet : h->dummy};
+  int rc = launch(h, dg, bufs, d_info, st, false);
+  if (rc) return rc;
+  // D2H in completion order; per side a pending contiguous range, flushed per chunk
+  int64_t tlo = -1, thi = -1, blo = -1, bhi = -1;  // top [tlo, thi), bottom [blo, bhi)
+  auto flush_top = [&]() {
+    bool ok = unit_range(X_host, A_dev, tlo, thi, true, cudaMemcpyDeviceToHost, h->s_out);
+    tlo = thi = -1;
+    return ok;
+  };
+  auto flush_bot = [&]() {
+    bool ok = unit_range(X_host, A_dev, blo, bhi, false, cudaMemcpyDeviceToHost, h->s_out);
+    blo = bhi = -1;
+    return ok;
+  };
+  for (size_t k = 0; k < dg.g.fin.size(); ++k) {
+    const Wait &w = dg.g.fin[k];
+    if (p_waitValue32((CUstream)h->s_out, (CUdeviceptr)(dg.ctr + w.ctr), (cuuint32_t)w.target,
+                      CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return SERINV_ERR_CUDA;
+    const int64_t i = dg.g.fin_blk[k];
+    if (i < 0) {
+      if (!cp(X_host->tip, A_dev->tip, (size_t)a * a, cudaMemcpyDeviceToHost, h->s_out)) return SERINV_ERR_CUDA;
+    } else if (i <= m) {  // top side finishes m, m-1, ..., 0
+      if (tlo < 0) tlo = thi = i + 1;
+      tlo = i;
+      if (thi - tlo >= chunk && !flush_top()) return SERINV_ERR_CUDA;
+    } else {  // bottom side finishes m+1, m+2, ..., n-1
+      if (blo < 0) blo = bhi = i;
+      bhi = i + 1;
+      if (bhi - blo >= chunk && !flush_bot()) return SERINV_ERR_CUDA;
+    }
+  }
+  if ((tlo >= 0 && !flush_top()) || (blo >= 0 && !flush_bot())) return SERINV_ERR_CUDA;
+  if (cudaEventRecord(h->ev_in, h->s_in) != cudaSuccess || cudaEventRecord(h->ev_out, h->s_out) != cudaSuccess ||
+      cudaStreamWaitEvent(st, h->ev_in, 0) != cudaSuccess || cudaStreamWaitEvent(st, h->ev_out, 0) != cudaSuccess)
+    return SERINV_ERR_CUDA;
+  return SERINV_OK;
+}
+
 int serinv_selinv_host(serinv_handle_t h, const serinv_bta_t *A_host, const serinv_bta_t *X_host,
                        const serinv_bta_t *A_dev, void *d_ws, size_t ws_bytes, int *d_info, double *d_logdet,
                        void *stream) {
@@ -653,6 +752,7 @@ int serinv_selinv_host(serinv_handle_t h, const serinv_bta_t *A_host, const seri
   };
   CUdeviceptr arr = (CUdeviceptr)(dg->ctr + dg->g.arr_ctr);
   if (a > 0 && h2d(A_dev->tip, A_host->tip, (size_t)a * a * 8) != cudaSuccess) return SERINV_ERR_CUDA;
+  if (dg->g.twist_m >= 0) return selinv_host_twisted(h, *dg, A_host, X_host, A_dev, d_ws, d_info, d_logdet, st, chunk);
   for (int64_t i0 = 0; i0 < n; i0 += chunk) {
     const int64_t i1 = std::min(n, i0 + chunk);
     if (h2d(A_dev->diag + i0 * b * b, A_host->diag + i0 * b * b, (size_t)(i1 - i0) * bb) != cudaSuccess)

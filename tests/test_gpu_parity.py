@@ -132,7 +132,7 @@ def test_launch_count_is_one_kernel():
     assert h.last_launches() == 1
 
 
-@pytest.mark.parametrize("n,b,a", [(9, 128, 8), (40, 64, 4), (5, 200, 0), (1, 64, 3)])
+@pytest.mark.parametrize("n,b,a", [(9, 128, 8), (40, 64, 4), (5, 200, 0), (1, 64, 3), (10, 1024, 16)])
 def test_selinv_host_streaming(n, b, a):
     """serinv_selinv_host: H2D / D2H stream with the computation (arrival / final counters)."""
     import torch

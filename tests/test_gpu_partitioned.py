@@ -125,20 +125,56 @@ def test_distributed_entry_points(P, n, b, a):
 
 def test_partitioned_factor_blocks_match_oracle_permuted_factor():
     """The eliminated blocks after the partitioned run's factor phase equal the
-    oracle's PERMUTED_POBTAF factor (same algorithm, Alg. 4)."""
+    oracle's PERMUTED_POBTAF factor (same algorithm, Alg. 4) for a middle partition."""
     sb = _sb()
     import torch
     from paper_2503_17528_b200 import distributed as sd
     A = btagen.g2(8, 14, 32, 3)
-    R = par.pselinv(A, 2)
-    ranks_parts = sb.plan(14, 2, 1.0)
-    s, e = ranks_parts[1]
-    loc = sd.local_blocks(A, s, e, last=True)
+    R = par.pselinv(A, 3)
+    s, e = sb.plan(14, 3, 1.0)[1]
+    loc = sd.local_blocks(A, s, e, last=False)
     D = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in loc.items()}
-    ctx = sd.DistContext(sb.default_handle(), 2, 1, 14, s, e - s, 32, 3)
+    ctx = sd.DistContext(sb.default_handle(), 3, 1, 14, s, e - s, 32, 3)
     sd.ppobtaf(ctx, D)
     torch.cuda.synchronize()
     G = {k: v.cpu().numpy() for k, v in D.items()}
     for i in range(s + 1, e - 1):   # interior blocks of the middle partition: factor L
         assert inv.rel_err(G["diag"][i - s], R["L"]["diag"][i]) <= TOL
         assert inv.rel_err(G["arrow"][i - s], R["L"]["arrow"][i]) <= TOL
+
+
+def test_twisted_last_partition_factor_is_reversed_pobtaf():
+    """Reading R14: the last partition eliminates blocks e-1, ..., s+1 bottom-up, i.e.
+    Alg. 1 on the block-reversed BTA matrix (again BTA); its diagonal and arrow factor
+    blocks equal the oracle's POBTAF of the reversed matrix."""
+    sb = _sb()
+    import torch
+    from paper_2503_17528_b200 import distributed as sd
+    n, b, a, P = 14, 32, 3, 3
+    A = btagen.g2(9, n, b, a)
+    s, e = sb.plan(n, P, 1.0)[P - 1]
+    assert e == n
+    # block-reversed matrix of blocks e-1 .. s (plus the tip): lower_rev[k] = A_{j-1,j} = lower[j-1]^T
+    blocks = list(range(e - 1, s - 1, -1))
+    Rv = {"diag": np.stack([A["diag"][j] for j in blocks]),
+          "lower": np.stack([A["lower"][j - 1].T for j in blocks[:-1]]),
+          "arrow": np.stack([A["arrow"][j] for j in blocks]),
+          "tip": np.zeros((a, a))}
+    loc = sd.local_blocks(A, s, e, last=True)
+    D = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in loc.items()}
+    ctx = sd.DistContext(sb.default_handle(), P, P - 1, n, s, e - s, b, a)
+    sd.ppobtaf(ctx, D)
+    torch.cuda.synchronize()
+    G = {k: v.cpu().numpy() for k, v in D.items()}
+    # the factor of the reversed chain: L_kk = chol(...) in the same elimination order
+    import scipy.linalg as sla
+    Dw = {k: v.copy() for k, v in Rv.items()}
+    for k in range(len(blocks) - 1):   # Alg. 1 l.2-6 on the reversed matrix (no tip needed)
+        Lkk = np.linalg.cholesky(Dw["diag"][k])
+        Lnext = sla.solve_triangular(Lkk, Dw["lower"][k].T, lower=True).T
+        Larr = sla.solve_triangular(Lkk, Dw["arrow"][k].T, lower=True).T
+        Dw["diag"][k + 1] -= Lnext @ Lnext.T
+        Dw["arrow"][k + 1] -= Larr @ Lnext.T
+        j = blocks[k]
+        assert inv.rel_err(np.tril(G["diag"][j - s]), Lkk) <= TOL
+        assert inv.rel_err(G["arrow"][j - s], Larr) <= TOL

@@ -118,9 +118,13 @@ def test_info_first_bad_pivot():
     assert np.isnan(ld)
 
 
+@pytest.mark.parametrize("twist_last", [1, 0])
 @pytest.mark.parametrize("P", [2, 3, 4, 8])
 @pytest.mark.parametrize("n,b,a", [(17, 4, 2), (24, 70, 5), (30, 8, 0), (16, 65, 3)])
-def test_pselinv_and_distributed_graphs(P, n, b, a):
+def test_pselinv_and_distributed_graphs(P, n, b, a, twist_last, monkeypatch):
+    # twist_last=1: the last partition eliminates bottom-up (reading R14), the
+    # reduced system has 2P-2 blocks; 0: the paper's scheme (2P-1)
+    monkeypatch.setenv("SERINV_OPT", f"twist_last={twist_last}")
     if n < 2 * P - 1:
         pytest.skip("too few blocks")
     A0 = btagen.g2(7, n, b, a)

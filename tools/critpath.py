@@ -33,8 +33,8 @@ def main():
     L = _lib.lib()
     nw, ns = ctypes.c_int64(0), ctypes.c_int64(0)
     L.serinv_graph_dump.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
-                                    ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                                    ctypes.c_void_p, ctypes.c_void_p]
+                                    ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]
     assert L.serinv_graph_dump(h._h, kid, n, b, a, 1, 1.0, None, None, ctypes.byref(nw), None, ctypes.byref(ns)) == 0
     rec = np.zeros((T, 10), np.int32); waits = np.zeros(nw.value, np.int32); sigs = np.zeros(ns.value, np.int32)
     assert L.serinv_graph_dump(h._h, kid, n, b, a, 1, 1.0, rec.ctypes.data, waits.ctypes.data, None,

@@ -31,6 +31,7 @@ inline double opget(Ctx &c, const Loc &l, int trans, int i, int j) {
 int run(const Graph &g, Ctx &c) {
   c.ctr.assign(g.nctr, 0);
   if (g.arr_ctr >= 0) c.ctr[g.arr_ctr] = 1 << 30;  // streaming IO: every block has arrived
+  if (g.arr_ctr2 >= 0) c.ctr[g.arr_ctr2] = 1 << 30;
   std::vector<double> acc(2 * SERINV_TILE * SERINV_TILE), tmp(2 * SERINV_TILE * SERINV_TILE);  // wide GEMM: m <= 128
   for (size_t t = 0; t < g.tasks.size(); ++t) {
     const Task &T = g.tasks[t];
