@@ -49,6 +49,17 @@ def flops_pobtasi(n, b, a):
             + 2 * b ** 3 / 3 + 2 * a * b * b + 2 * a * a * b + 2 * a ** 3 / 3)
 
 
+def ncu_traffic(config):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the executor from the
+    committed ncu --set full capture of this config (profiles/r01/ncu_<C>/summary.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r01", f"ncu_{config}", "summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f)["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def bta_bytes(n, b, a):
     return 8 * (n * b * b + (n - 1) * b * b + n * a * b + a * a)
 
@@ -319,7 +330,8 @@ def main():
             "tflops_pobtaf_plus_pobtasi": round(value, 4),
             "fraction_of_fp64_peak": round(value / (FP64_PEAK_TFLOPS * N), 4),
             "roofline": {"bound": "tensor", "achieved": round(value / N, 4), "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": round(value / N / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                         "unit": "TFLOP/s", "frac": round(value / N / FP64_PEAK_TFLOPS, 4),
+                         "traffic": ncu_traffic(args.config) if world == 1 else None,
                          "kernel": "serinv_exec_kernel (persistent, 1 launch per step)",
                          "peak_source": "measured DMMA f64 peak, profiles/fp64_peaks_r01.json"},
             "clocks": clocks,
