@@ -71,6 +71,11 @@ __device__ __forceinline__ unsigned smid() {
 
 __device__ __forceinline__ double *lptr(const Params &p, const Loc &l) { return p.bufs[l.buf] + l.off; }
 
+__device__ __forceinline__ void phase_mark(const Params &p, int t, int k) {
+  if (p.trace && threadIdx.x == 0) p.trace[4 * (size_t)p.ntasks + 8 * (size_t)t + k] = globaltimer();
+}
+
+
 // thread 0 spins until waits [w0, w1) of the task list are satisfied (20 s watchdog)
 __device__ void wait_range(const Params &p, int w0, int w1) {
   for (int w = w0; w < w1; ++w) {
@@ -231,10 +236,23 @@ __device__ __forceinline__ void mma_chunk_lay(bool akm, bool bkm, const double *
 // Main loop over one or two segment lists sharing ONE cp.async pipeline:
 //   acc  = sum_{s in [s0, s0+ns)}  op(A_s) op(B_s)   (output m  x n)
 //   acc2 = sum_{s in [s0b, s0b+nsb)} op(A_s) op(B_s)  (output mb x n)   [if acc2 != nullptr]
+// full 64 x 64 tile (row-major, ld, 16-byte aligned) -> smem [64][LDT] via cp.async
+__device__ __forceinline__ void tile_async(double *s, const double *g, int ld) {
+#pragma unroll
+  for (int it = 0; it < (SERINV_TILE * SERINV_TILE / 2) / NT; ++it) {
+    const int idx = threadIdx.x + it * NT, r = idx >> 5, c2 = (idx & 31) * 2;
+    cp_async16(s + r * LDT + c2, g + (int64_t)r * ld + c2, 16);
+  }
+}
+
+// pf0 / pf1 (optional, full aligned 64 x 64 tiles): staged with cp.async into the
+// pipeline stages freed after the last k-chunk is issued -- pf0 lands in stage
+// nchunks % STAGES, pf1 in (nchunks + 1) % STAGES (complete when this returns).
 template <bool DUAL>
 __device__ __forceinline__ void gemm_mainloop2(const Params &p, int s0, int ns, int m, int s0b, int nsb, int mb,
                                                int n, double *smem, double (&acc)[2][4][2],
-                                               double (&acc2)[2][4][2]) {
+                                               double (&acc2)[2][4][2], const double *pf0 = nullptr, int ld0 = 0,
+                                               const double *pf1 = nullptr, int ld1 = 0) {
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -296,15 +314,23 @@ __device__ __forceinline__ void gemm_mainloop2(const Params &p, int s0, int ns, 
   // compute-side cursor
   int cs = 0, ck = 0;
   Cur C = L;
+  // issue slot `slot` (>= nchunks): the prefetch tiles
+  auto issue_extra = [&](int slot) {
+    double *st = smem + (slot % STAGES) * 2 * OPSZ;
+    if (slot == nchunks && pf0) tile_async(st, pf0, ld0);
+    if (slot == nchunks + 1 && pf1) tile_async(st, pf1, ld1);
+  };
 #pragma unroll
   for (int j = 0; j < STAGES - 1; ++j) {
     if (j < nchunks) issue(j);
+    else issue_extra(j);
     cp_commit();
   }
   for (int j = 0; j < nchunks; ++j) {
     cp_wait<STAGES - 2>();
     __syncthreads();
     if (j + STAGES - 1 < nchunks) issue((j + STAGES - 1) % STAGES);
+    else issue_extra(j + STAGES - 1);
     cp_commit();
     const bool inB = j >= nchA;
     const double *As = smem + (j % STAGES) * 2 * OPSZ;
@@ -370,16 +396,35 @@ __device__ __forceinline__ void frag_rc(int mi, int ni, int h, int &r, int &c) {
 __device__ __forceinline__ void apply_c0(const Params &p, double alpha, double beta, const Loc &loc, int m, int n,
                                          double (&acc)[2][4][2]) {
   const double *c0 = (beta != 0.0) ? lptr(p, loc) : nullptr;
+  if (c0 && m == SERINV_TILE && n == SERINV_TILE && ((loc.off | loc.ld) & 1) == 0) {
+    // full tile: 16-byte loads, four in flight per fragment row
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      double2 cv[4];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        int r, cc;
+        frag_rc(mi, ni, 0, r, cc);
+        cv[ni] = __ldcg(reinterpret_cast<const double2 *>(c0 + (int64_t)r * loc.ld + cc));
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        acc[mi][ni][0] = fma(alpha, acc[mi][ni][0], beta * cv[ni].x);
+        acc[mi][ni][1] = fma(alpha, acc[mi][ni][1], beta * cv[ni].y);
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        int r, c;
-        frag_rc(mi, ni, h, r, c);
+        int r, cc;
+        frag_rc(mi, ni, h, r, cc);
         double v = alpha * acc[mi][ni][h];
-        if (c0 && r < m && c < n) v += beta * __ldcg(c0 + (int64_t)r * loc.ld + c);
+        if (c0 && r < m && cc < n) v += beta * __ldcg(c0 + (int64_t)r * loc.ld + cc);
         acc[mi][ni][h] = v;
       }
 }
@@ -626,7 +671,24 @@ __device__ void run_gemm_wide(const Params &p, const Task &T, double *smem) {
     __syncthreads();
   }
   // acc = alpha * acc + beta * C0
-  {
+  if (T.beta != 0.0 && m == WROWS && n == SERINV_TILE && ((T.c0.off | T.c0.ld) & 1) == 0) {
+    const double *c0 = lptr(p, T.c0);  // full tile: 16-byte loads, four in flight per row group
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      double2 cv[4];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        int r, cc;
+        wide_rc(mi, ni, 0, r, cc);
+        cv[ni] = __ldcg(reinterpret_cast<const double2 *>(c0 + (int64_t)r * T.c0.ld + cc));
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        acc[mi][ni][0] = fma(T.alpha, acc[mi][ni][0], T.beta * cv[ni].x);
+        acc[mi][ni][1] = fma(T.alpha, acc[mi][ni][1], T.beta * cv[ni].y);
+      }
+    }
+  } else {
     const double *c0 = (T.beta != 0.0) ? lptr(p, T.c0) : nullptr;
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
@@ -698,19 +760,49 @@ __device__ void run_gemm_wide(const Params &p, const Task &T, double *smem) {
 // ---------------------------------------------------------------------------
 // Tile tasks
 // ---------------------------------------------------------------------------
-__device__ void run_gemm(const Params &p, const Task &T, double *smem) {
+__device__ void run_gemm(const Params &p, const Task &T, double *smem, int tsk) {
   double acc[2][4][2];
-  gemm_mainloop(p, T.seg0, T.nseg, T.m, T.n, smem, acc);
-  apply_c0(p, T.alpha, T.beta, T.c0, T.m, T.n, acc);
+  // C0 and the post-multiply tile ride in the pipeline's freed stages when the
+  // task has k-chunks and the tiles are full and 16-byte aligned (the post tile
+  // only if it is not a late input)
+  int nch = 0;
+  for (int s = 0; s < T.nseg; ++s) nch += (p.segs[T.seg0 + s].k + KC - 1) / KC;
+  const bool full = T.m == SERINV_TILE && T.n == SERINV_TILE && nch > 0;
+  const bool pfc = full && T.beta != 0.0 && ((T.c0.off | T.c0.ld) & 1) == 0;
+  const bool pfr = full && (T.flags & TF_POST) && T.nlate == 0 && ((T.r.off | T.r.ld) & 1) == 0;
+  const double *pc = pfc ? lptr(p, T.c0) : nullptr;
+  const double *pr = pfr ? lptr(p, T.r) : nullptr;
+  // stage assignment: pf0 -> nch % 3, pf1 -> (nch + 1) % 3; with only R, R takes pf0's slot
+  gemm_mainloop2<false>(p, T.seg0, T.nseg, T.m, 0, 0, 0, T.n, smem, acc, acc, pfc ? pc : pr,
+                        pfc ? T.c0.ld : T.r.ld, pfc ? pr : nullptr, T.r.ld);
+  phase_mark(p, tsk, 5);
+  double *Cs = smem + (nch % STAGES) * 2 * OPSZ;
+  double *Rs = pfc ? smem + ((nch + 1) % STAGES) * 2 * OPSZ : Cs;
+  if (pfc) {
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int r, cc;
+          frag_rc(mi, ni, h, r, cc);
+          acc[mi][ni][h] = fma(T.alpha, acc[mi][ni][h], T.beta * Cs[r * LDT + cc]);
+        }
+  } else {
+    apply_c0(p, T.alpha, T.beta, T.c0, T.m, T.n, acc);
+  }
   if (T.nlate > 0) {  // late inputs (the post-multiply tile, the SYRK target's updates)
     if (threadIdx.x == 0) wait_range(p, T.wait0 + T.nwait - T.nlate, T.wait0 + T.nwait);
     __syncthreads();
   }
   if (T.flags & TF_POST) {
-    double *St = smem;
-    double *Rt = smem + SERINV_TILE * LDT;
+    // S (this result) goes to the stage after the prefetched ones; R from its stage
+    double *St = pfr ? smem + ((nch + 2) % STAGES) * 2 * OPSZ : smem;
+    double *Rt = pfr ? Rs : smem + SERINV_TILE * LDT;
+    if (!pfr && pfc) __syncthreads();  // C0 (read above) may overlap St / Rt
     acc_to_smem(St, acc);
-    tile_to_smem(Rt, lptr(p, T.r), T.r.ld, T.n, T.n);
+    if (!pfr) tile_to_smem(Rt, lptr(p, T.r), T.r.ld, T.n, T.n);
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -721,7 +813,9 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem) {
     mma_steps(St, LDT, 1, Rt, rt ? LDT : 1, rt ? 1 : LDT, acc, (T.n + 3) / 4);
     __syncthreads();
   }
+  phase_mark(p, tsk, 6);
   store_acc(p, T, acc);
+  phase_mark(p, tsk, 7);
   if (T.flags & TF_SYRK3) {
     // the next diagonal tile of the chain: out3 -= L L^T (L = this result, m x n);
     // stage the target tile into smem with cp.async while the SYRK runs
@@ -767,9 +861,6 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem) {
   }
 }
 
-__device__ __forceinline__ void phase_mark(const Params &p, int t, int k) {
-  if (p.trace && threadIdx.x == 0) p.trace[4 * (size_t)p.ntasks + 8 * (size_t)t + k] = globaltimer();
-}
 
 // select row[kk] for runtime kk without dynamic register indexing
 __device__ __forceinline__ double sel4(const double (&row)[4], int kk) {
@@ -1251,6 +1342,22 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   }
   phase_mark(p, tsk, 2);
   if (tid == 0 && s_bad < (1 << 30)) record_info(p.info, T.aux1 + s_bad + 1);
+  const bool early = factor && (T.flags & TF_EARLY_SIG) && (T.flags & TF_W_OUT);
+  if (early) {
+    // W = L^{-1} is what the chain's next TRSM waits for: store it and publish the
+    // task's own counter now; the log-det partial and L follow (their readers wait
+    // on the factor-done counter, signalled at the end)
+    double *wo = lptr(p, T.out2);
+    for (int idx = tid; idx < SERINV_TILE * SERINV_TILE; idx += NT) {
+      const int i = idx >> 6, k = idx & 63;
+      if (i < m && k < m) wo[(int64_t)i * T.out2.ld + k] = Wt[i * LDT + k];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(p.ctr + p.sigs[T.sig0], 1);
+    }
+  }
   if (factor) {
     // log det partial: sum_j 0.5 log d_j, fixed-order tree over 64 values
     double *lg = lb;
@@ -1307,7 +1414,7 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   phase_mark(p, tsk, 3);
   // ---- store L (factor) and W
   {
-    const bool wout = !factor || (T.flags & TF_W_OUT);
+    const bool wout = (!factor || (T.flags & TF_W_OUT)) && !early;
     const Loc &wl = factor ? T.out2 : T.out;
     double *o = factor ? lptr(p, T.out) : nullptr;
     double *wo = wout ? lptr(p, wl) : nullptr;
@@ -1492,7 +1599,7 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
     switch (T.type) {
       case TK_GEMM:
         if (T.m > SERINV_TILE) run_gemm_wide(p, T, smem);
-        else run_gemm(p, T, smem);
+        else run_gemm(p, T, smem, t);
         break;
       case TK_POTRF: run_potrf_trtri(p, T, smem, true, t); break;
       case TK_TRTRI: run_potrf_trtri(p, T, smem, false, t); break;
@@ -1502,19 +1609,24 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
       default: break;
     }
     // publish: barrier (CTA-scope ordering of every thread's stores) then one
-    // gpu-scope fence by the signalling thread (cumulative) and the increments
+    // gpu-scope fence by the signalling thread (cumulative) and the increments.
+    // The last warp publishes while thread 0 already claims the next task.
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == NT - 32) {
       __threadfence();
-      for (int s = 0; s < T.nsig; ++s) atomicAdd(p.ctr + p.sigs[T.sig0 + s], 1);
+      const int s0 = (T.type == TK_POTRF && (T.flags & TF_EARLY_SIG) && (T.flags & TF_W_OUT)) ? 1 : 0;
+      for (int s = s0; s < T.nsig; ++s) atomicAdd(p.ctr + p.sigs[T.sig0 + s], 1);
       if (p.trace) {
         unsigned long long *rec = p.trace + 4 * (size_t)t;
-        rec[0] = t_claim;
-        rec[1] = t_start;
         rec[2] = globaltimer();
         rec[3] = (unsigned long long)(unsigned)T.type | ((unsigned long long)smid() << 16) |
                  ((unsigned long long)(unsigned)T.m << 32) | ((unsigned long long)(unsigned)T.flags << 48);
       }
+    }
+    if (threadIdx.x == 0 && p.trace) {
+      unsigned long long *rec = p.trace + 4 * (size_t)t;
+      rec[0] = t_claim;
+      rec[1] = t_start;
     }
   }
 }

@@ -453,6 +453,9 @@ struct Builder {
           first_trsm = 2;
         }
         rt.queue = cx.opt.critical_queues ? P.q1(X) : 0;
+        // the own counter (first signal) only guards W = L^{-1}: readers of the
+        // factor tile and the log-det slot wait on the factor-done counter fd
+        if (!(rt.t.flags & (TF_TRSM2 | TF_TRSM3)) && cx.opt.early_sig) rt.t.flags |= TF_EARLY_SIG;
         int id = cx.emit(std::move(rt));
         st.pending.clear();
         st.last = id;
@@ -1727,6 +1730,7 @@ void BuildOptions::apply_env() {
       else if (k == "wide_min_wave") wide_min_wave = (int)v;
       else if (k == "chol8") chol8 = v != 0;
       else if (k == "twist_last") twist_last = v != 0;
+      else if (k == "early_sig") early_sig = v != 0;
     }
     i = j + 1;
   }

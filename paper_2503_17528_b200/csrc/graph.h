@@ -103,7 +103,8 @@ struct BuildOptions {
   int max_crit = 16;            // partitioned solves: exclusive-SM chains only if 2P <= max_crit
   int twist_min_n = 4;          // selinv: two-sided (twisted) elimination if n >= twist_min_n (0: never)
   bool twist_last = true;       // partitioned solves: the last partition eliminates bottom-up (no fill-in)
-  bool chol8 = true;            // POTRF tasks: 8 x 8-block warp-pipelined Cholesky (else 16 x 16 leaves)
+  bool chol8 = true;
+  bool early_sig = true;        // POTRF publishes W before its log-det partial and L (TF_EARLY_SIG)            // POTRF tasks: 8 x 8-block warp-pipelined Cholesky (else 16 x 16 leaves)
   int wide_min_wave = 512;      // 128 x 64 tasks for inversion waves of >= this many tiles (0: never)
   int twist_max_b = 1024;       // ... and b <= twist_max_b (larger blocks: the one-sided chain hides under the work)
   // overrides from the environment (SERINV_OPT="key=value,..."), for tuning runs

@@ -45,6 +45,7 @@ enum TaskFlags : uint16_t {
   TF_TRSM3 = 128,     // TK_POTRF: fused TRSM of the second sub-diagonal tile (out4)
   TF_SYRK3 = 256,     // TK_GEMM (+TF_POST): then out3 (m x m) -= L L^T with L the result
   TF_CHOL8 = 512,     // TK_POTRF: warp-pipelined 8 x 8-block Cholesky + inverse (chol8_pipelined)
+  TF_EARLY_SIG = 1024,  // TK_POTRF (+TF_W_OUT, no TF_TRSM2): own counter signalled once W is stored
 };
 
 // Buffer ids (kernel argument `bufs[]`, offsets in doubles).
