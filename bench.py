@@ -60,6 +60,13 @@ def ncu_traffic(config):
         return None
 
 
+def bench_config(name, cfg):
+    """The workload both arms report (per GPU for N > 1: weak scaling)."""
+    n, b, a = cfg["n"], cfg["b"], cfg["a"]
+    return {"workload": f"{name} n={n} b={b} a={a} per GPU", "n": n, "b": b, "a": a, "generator": "g1 seed 0",
+            "l2": f"inputs {bta_bytes(n, b, a) / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"}
+
+
 def bta_bytes(n, b, a):
     return 8 * (n * b * b + (n - 1) * b * b + n * a * b + a * a)
 
@@ -170,8 +177,7 @@ def reference_arm(args, cfg):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(med * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} n={n} b={b} a={a}", "n": n, "b": b, "a": a,
-                   "generator": "g1 seed 0", "sample_blocks": nprime},
+        "config": bench_config(args.config, cfg),
         "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
                          "sample": f"oracle selinv (numpy/scipy FP64) on n'={nprime} of the {n} blocks, same b, a"},
         "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -319,13 +325,12 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec_per_step * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"{args.config} n={n_loc} b={b} a={a} per GPU", "n_global": n, "b": b, "a": a,
-                       "generator": "g1 seed 0", "parallelism": f"partitions{world}" if world > 1 else
-                       ("single" if Ps == [1] else "intra-GPU partitions " + "x".join(map(str, Ps))),
-                       "l2": f"inputs {bta_bytes(n_loc, b, a) / 1e9:.2f} GB per GPU > 126 MB L2",
-                       "step": ("POBTAF+POBTASI (serinv_selinv)" if Ps == [1] else
-                                "PPOBTAF+POBTARSSI+PPOBTASI in one launch (serinv_pselinv_nested)")
-                               if world == 1 else "PPOBTAF + NCCL all-gather + PPOBTASI"},
+            "config": bench_config(args.config, cfg),
+            "plan": {"n_global": n, "parallelism": f"partitions{world}" if world > 1 else
+                     ("single" if Ps == [1] else "intra-GPU partitions " + "x".join(map(str, Ps))),
+                     "step": ("POBTAF+POBTASI (serinv_selinv)" if Ps == [1] else
+                              "PPOBTAF+POBTARSSI+PPOBTASI in one launch (serinv_pselinv_nested)")
+                             if world == 1 else "PPOBTAF + NCCL all-gather + PPOBTASI"},
             "seconds_per_step": round(sec_per_step, 6),
             "tflops_pobtaf_plus_pobtasi": round(value, 4),
             "fraction_of_fp64_peak": round(value / (FP64_PEAK_TFLOPS * N), 4),
