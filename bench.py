@@ -64,7 +64,8 @@ def bench_config(name, cfg):
     """The workload both arms report (per GPU for N > 1: weak scaling)."""
     n, b, a = cfg["n"], cfg["b"], cfg["a"]
     return {"workload": f"{name} n={n} b={b} a={a} per GPU", "n": n, "b": b, "a": a, "generator": "g1 seed 0",
-            "l2": f"inputs {bta_bytes(n, b, a) / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"}
+            "l2": (f"inputs {bta_bytes(n, b, a) / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"
+                   if bta_bytes(n, b, a) > L2_BYTES else "inputs fit in L2 (parity-size case)")}
 
 
 def bta_bytes(n, b, a):

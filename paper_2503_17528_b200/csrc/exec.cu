@@ -1076,6 +1076,11 @@ __device__ __forceinline__ void leaf_chol8(double *Ab, double *Zb, double *dv8) 
   if (lane < 8) dv8[lane] = dmine;
 }
 
+// the 36 blocks (i, j), j <= i < 8, of an 8 x 8-block lower triangle, column-major: (i << 4) | j
+__constant__ unsigned char c_lower8[36] = {
+    0x00, 0x10, 0x20, 0x30, 0x40, 0x50, 0x60, 0x70, 0x11, 0x21, 0x31, 0x41, 0x51, 0x61, 0x71, 0x22, 0x32, 0x42,
+    0x52, 0x62, 0x72, 0x33, 0x43, 0x53, 0x63, 0x73, 0x44, 0x54, 0x64, 0x74, 0x55, 0x65, 0x75, 0x66, 0x76, 0x77};
+
 // Cholesky L and inverse W = L^{-1} of the 64 x 64 tile St (rows / columns >= m
 // padded with the identity) on 8 x 8 blocks, software-pipelined across warps so
 // the serial chain is just the 8 leaves.  Step k (k = 0..7), after a CTA barrier:
@@ -1136,28 +1141,29 @@ __device__ void chol8_pipelined(double *St, double *Wt, double *S2, double *dv, 
         blk_store(blk(St, ip, k - 1), l);
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      // trailing update by column k-1: blocks (i, j), k <= j <= i <= 7, except (k, k);
-      // this warp's (at most 4) blocks: all operands loaded, then all DMMAs, then stores
-      int bi[4], bj[4], nb = 0, idx = 0;
-      for (int j = k; j < 8; ++j)
-        for (int i = j; i < 8; ++i) {
-          if (i == k && j == k) continue;
-          if (idx++ % 7 == wk && nb < 4) {
-            bi[nb] = i;
-            bj[nb] = j;
-            ++nb;
-          }
-        }
+      // trailing update by column k-1: blocks (i, j), k <= j <= i <= 7, except (k, k)
+      // (entries off(k)+1 .. 35 of the column-major lower-triangle table); this warp
+      // takes every 7th: all operands loaded, then all DMMAs, then the stores
+      const int off = k * 8 - (k * (k - 1)) / 2;          // entries with j < k
+      const int idx = 36 - off - 1;                        // blocks this step
+      int bi[4], bj[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int e = off + 1 + wk + 7 * t;
+        const int v = (e < 36) ? c_lower8[e] : 0;
+        bi[t] = v >> 4;
+        bj[t] = v & 15;
+      }
       double acc[4][2];
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (t < nb) blk_load(blk(St, bi[t], bj[t]), acc[t]);
+        if (wk + 7 * t < idx) blk_load(blk(St, bi[t], bj[t]), acc[t]);
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (t < nb) blk_mma_nt_sub(acc[t], blk(St, bi[t], k - 1), blk(St, bj[t], k - 1));
+        if (wk + 7 * t < idx) blk_mma_nt_sub(acc[t], blk(St, bi[t], k - 1), blk(St, bj[t], k - 1));
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (t < nb) blk_store(blk(St, bi[t], bj[t]), acc[t]);
+        if (wk + 7 * t < idx) blk_store(blk(St, bi[t], bj[t]), acc[t]);
       // block row k-1 of W (blocks j < k-1), round-robin after the updates
       for (int j = 0; j < k - 1; ++j)
         if ((idx + j) % 7 == wk) wblock(k - 1, j);

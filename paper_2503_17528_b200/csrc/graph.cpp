@@ -234,6 +234,11 @@ struct Builder {
   Ctx &cx;
   Problem &P;
   std::unordered_map<uint64_t, int> Lprod;  // L tile producers
+  std::unordered_map<uint64_t, int32_t> Lctr;  // L tiles published on a counter other than their producer's own
+  int32_t lwait(uint64_t key) {
+    auto it = Lctr.find(key);
+    return it != Lctr.end() ? it->second : cx.ctr_of(Lprod.at(key));
+  }
   struct TileState {
     std::vector<std::pair<int, int>> pending;  // columns (X, c) not yet applied
     int last = -1;
@@ -346,8 +351,8 @@ struct Builder {
       rt.segs.push_back(mkseg(tileloc(bi.base, qi, c0), 0, tileloc(bj.base, qj, c0), 1, k));
       for (size_t u = s; u < e; ++u) {
         int c = cols[u].second;
-        rt.waits.push_back(cx.ctr_of(Lprod.at(key4(Yi, qi, X, c))));
-        rt.waits.push_back(cx.ctr_of(Lprod.at(key4(Yj, qj, X, c))));
+        rt.waits.push_back(lwait(key4(Yi, qi, X, c)));
+        rt.waits.push_back(lwait(key4(Yj, qj, X, c)));
       }
       s = e;
     }
@@ -454,9 +459,18 @@ struct Builder {
         }
         rt.queue = cx.opt.critical_queues ? P.q1(X) : 0;
         // the own counter (first signal) only guards W = L^{-1}: readers of the
-        // factor tile and the log-det slot wait on the factor-done counter fd
-        if (!(rt.t.flags & (TF_TRSM2 | TF_TRSM3)) && cx.opt.early_sig) rt.t.flags |= TF_EARLY_SIG;
+        // factor tile and the log-det slot wait on the factor-done counter fd, and
+        // readers of a fused TRSM's tile on its own counter (published at the end)
+        int32_t sctr = -1;
+        if (!(rt.t.flags & TF_TRSM3) && cx.opt.early_sig) {
+          rt.t.flags |= TF_EARLY_SIG;
+          if (rt.t.flags & TF_TRSM2) {
+            sctr = cx.new_ctr();
+            rt.sigs.push_back(sctr);
+          }
+        }
         int id = cx.emit(std::move(rt));
+        if (sctr >= 0) Lctr[key4(rts[0].Y, rts[0].q, X, c)] = sctr;
         st.pending.clear();
         st.last = id;
         st.written = true;

@@ -63,28 +63,29 @@ __device__ void chol8_dbg(double *St, double *Wt, double *S2, double *dv, int m,
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if ((threadIdx.x & 31) == 0) ts[(threadIdx.x >> 5) * 40 + 4 * k + 1] = clock64();
       if (!(mode & 2)) {
-      // trailing update by column k-1: blocks (i, j), k <= j <= i <= 7, except (k, k);
-      // this warp's (at most 4) blocks: all operands loaded, then all DMMAs, then stores
-      int bi[4], bj[4], nb = 0, idx = 0;
-      for (int j = k; j < 8; ++j)
-        for (int i = j; i < 8; ++i) {
-          if (i == k && j == k) continue;
-          if (idx++ % 7 == wk && nb < 4) {
-            bi[nb] = i;
-            bj[nb] = j;
-            ++nb;
-          }
-        }
+      // trailing update by column k-1: blocks (i, j), k <= j <= i <= 7, except (k, k)
+      // (entries off(k)+1 .. 35 of the column-major lower-triangle table); this warp
+      // takes every 7th: all operands loaded, then all DMMAs, then the stores
+      const int off = k * 8 - (k * (k - 1)) / 2;          // entries with j < k
+      const int idx = 36 - off - 1;                        // blocks this step
+      int bi[4], bj[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int e = off + 1 + wk + 7 * t;
+        const int v = (e < 36) ? c_lower8[e] : 0;
+        bi[t] = v >> 4;
+        bj[t] = v & 15;
+      }
       double acc[4][2];
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (t < nb) blk_load(blk(St, bi[t], bj[t]), acc[t]);
+        if (wk + 7 * t < idx) blk_load(blk(St, bi[t], bj[t]), acc[t]);
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (t < nb) blk_mma_nt_sub(acc[t], blk(St, bi[t], k - 1), blk(St, bj[t], k - 1));
+        if (wk + 7 * t < idx) blk_mma_nt_sub(acc[t], blk(St, bi[t], k - 1), blk(St, bj[t], k - 1));
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (t < nb) blk_store(blk(St, bi[t], bj[t]), acc[t]);
+        if (wk + 7 * t < idx) blk_store(blk(St, bi[t], bj[t]), acc[t]);
       // block row k-1 of W (blocks j < k-1), round-robin after the updates
       for (int j = 0; j < k - 1; ++j)
         if ((idx + j) % 7 == wk) wblock(k - 1, j);
@@ -146,7 +147,7 @@ int main() {
   cudaFuncSetAttribute(kchol, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char *names[3] = {"chol8_pipelined (64x64 L + W)", "leaf_chol8 (one 8x8 block)", "leaf_chol16 (one 16x16 block)"};
   long long *hts = new long long[400];
-  for (int mode = 0; mode < 4; ++mode) {
+  for (int mode : {0, 1, 2}) {
     cudaMemset(dc, 0, 8 * 400);
     kchol<<<1, 256, smem>>>(dA, dL, dW, dc, 3 + mode);
     kchol<<<1, 256, smem>>>(dA, dL, dW, dc, 3 + mode);
