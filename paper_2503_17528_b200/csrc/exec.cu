@@ -1018,17 +1018,18 @@ __device__ __forceinline__ void blk_mma_nt_sub(double (&acc)[2], const double *X
   dmma(acc, -X[g * LDT + 4 + q], Y[g * LDT + 4 + q]);
 }
 
-// Cholesky + inverse of one 8 x 8 block in place (one converged warp, registers +
-// shuffles): Ab <- L (strict upper zeroed), Zb <- Z = L^{-1}, dv8[j] <- pivot j.
+// Cholesky + inverse of one 8 x 8 block (one converged warp, registers +
+// shuffles), the block given in accumulator layout (a0, a1 = A[g][2q], A[g][2q+1]):
+// Ab <- L (strict upper zeroed), Zb <- Z = L^{-1}, dv8[j] <- pivot j.
 // Right-looking elimination with the row operations mirrored on Z = I (see
-// leaf_chol16 for the algebra: M A = L^T, Z = D^{-1/2} M = L^{-1}).  The next
-// pivot d' = A[p+1][p+1] - A[p+1][p]^2 / d is formed from two values shuffled
-// before pivot p's update, so the serial chain per pivot is one FMA and one
-// reciprocal; the column / Z updates run beside it.
-__device__ __forceinline__ void leaf_chol8(double *Ab, double *Zb, double *dv8) {
+// leaf_chol16 for the algebra: M A = L^T, Z = D^{-1/2} M = L^{-1}).  The column
+// scaling by 1/sqrt(d_p) (L) and the row scaling of Z are postponed to the end
+// (the updates only read the unscaled current column), and the next pivot
+// d' = A[p+1][p+1] - A[p+1][p]^2 / d is formed from two values shuffled before
+// pivot p's update, so the serial chain per pivot is one FMA and one reciprocal.
+__device__ __forceinline__ void leaf_chol8r(double a0, double a1, double *Ab, double *Zb, double *dv8) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  double a0 = Ab[g * LDT + 2 * q], a1 = Ab[g * LDT + 2 * q + 1];
   double z0 = (g == 2 * q) ? 1.0 : 0.0, z1 = (g == 2 * q + 1) ? 1.0 : 0.0;
   double dmine = 1.0;
   double d = __shfl_sync(FULL, a0, 0);
@@ -1056,24 +1057,26 @@ __device__ __forceinline__ void leaf_chol8(double *Ab, double *Zb, double *dv8) 
     a1 = (below && 2 * q + 1 > p) ? fma(-f, aj1, a1) : a1;
     z0 = below ? fma(-f, zp0, z0) : z0;
     z1 = below ? fma(-f, zp1, z1) : z1;
-    const double rs = rsqrt_nr(d);
-    const double lcol = below ? ai * rs : ((g == p) ? d * rs : 0.0);  // column p of L
-    if (p & 1) {
-      a1 = (q == sq) ? lcol : a1;
-    } else {
-      a0 = (q == sq) ? lcol : a0;
-    }
-    z0 = (g == p) ? z0 * rs : z0;
-    z1 = (g == p) ? z1 * rs : z1;
     dmine = (lane == p) ? d : dmine;
     d = dn;
     id = idn;
   }
+  // postponed scaling: L[g][j] = A[g][j] / sqrt(d_j) (g > j), sqrt(d_j) on the
+  // diagonal, 0 above; Z[g][:] /= sqrt(d_g)
+  const double dj0 = __shfl_sync(FULL, dmine, 2 * q), dj1 = __shfl_sync(FULL, dmine, 2 * q + 1);
+  const double dg = __shfl_sync(FULL, dmine, g);
+  const double r0 = rsqrt_nr(dj0), r1 = rsqrt_nr(dj1), rg = rsqrt_nr(dg);
+  a0 = (g > 2 * q) ? a0 * r0 : ((g == 2 * q) ? dj0 * r0 : 0.0);
+  a1 = (g > 2 * q + 1) ? a1 * r1 : ((g == 2 * q + 1) ? dj1 * r1 : 0.0);
   Ab[g * LDT + 2 * q] = a0;
   Ab[g * LDT + 2 * q + 1] = a1;
-  Zb[g * LDT + 2 * q] = z0;
-  Zb[g * LDT + 2 * q + 1] = z1;
+  Zb[g * LDT + 2 * q] = z0 * rg;
+  Zb[g * LDT + 2 * q + 1] = z1 * rg;
   if (lane < 8) dv8[lane] = dmine;
+}
+__device__ __forceinline__ void leaf_chol8(double *Ab, double *Zb, double *dv8) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  leaf_chol8r(Ab[g * LDT + 2 * q], Ab[g * LDT + 2 * q + 1], Ab, Zb, dv8);
 }
 
 // the 36 blocks (i, j), j <= i < 8, of an 8 x 8-block lower triangle, column-major: (i << 4) | j
@@ -1128,10 +1131,10 @@ __device__ void chol8_pipelined(double *St, double *Wt, double *S2, double *dv, 
         double a[2];
         blk_load(Akk, a);
         blk_mma_nt_sub(a, blk(St, k, k - 1), blk(St, k, k - 1));
-        blk_store(Akk, a);
-        __syncwarp();
+        leaf_chol8r(a[0], a[1], Akk, blk(Wt, k, k), dv + 8 * k);  // the updated block stays in registers
+      } else {
+        leaf_chol8(Akk, blk(Wt, k, k), dv + 8 * k);
       }
-      leaf_chol8(Akk, blk(Wt, k, k), dv + 8 * k);
     } else if (k > 0) {
       const int wk = warp - 1;  // 0..6
       const int ip = k + 1 + wk;

@@ -46,12 +46,10 @@ __device__ void chol8_dbg(double *St, double *Wt, double *S2, double *dv, int m,
         double a[2];
         blk_load(Akk, a);
         blk_mma_nt_sub(a, blk(St, k, k - 1), blk(St, k, k - 1));
-        blk_store(Akk, a);
-        __syncwarp();
+        leaf_chol8r(a[0], a[1], Akk, blk(Wt, k, k), dv + 8 * k);  // the updated block stays in registers
+      } else {
+        leaf_chol8(Akk, blk(Wt, k, k), dv + 8 * k);
       }
-      if ((threadIdx.x & 31) == 0) ts[4 * k + 1] = clock64();
-      if (!(mode & 1)) leaf_chol8(Akk, blk(Wt, k, k), dv + 8 * k);
-      if ((threadIdx.x & 31) == 0) ts[4 * k + 2] = clock64();
     } else if (k > 0) {
       const int wk = warp - 1;  // 0..6
       const int ip = k + 1 + wk;
@@ -61,8 +59,6 @@ __device__ void chol8_dbg(double *St, double *Wt, double *S2, double *dv, int m,
         blk_store(blk(St, ip, k - 1), l);
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      if ((threadIdx.x & 31) == 0) ts[(threadIdx.x >> 5) * 40 + 4 * k + 1] = clock64();
-      if (!(mode & 2)) {
       // trailing update by column k-1: blocks (i, j), k <= j <= i <= 7, except (k, k)
       // (entries off(k)+1 .. 35 of the column-major lower-triangle table); this warp
       // takes every 7th: all operands loaded, then all DMMAs, then the stores
@@ -89,8 +85,6 @@ __device__ void chol8_dbg(double *St, double *Wt, double *S2, double *dv, int m,
       // block row k-1 of W (blocks j < k-1), round-robin after the updates
       for (int j = 0; j < k - 1; ++j)
         if ((idx + j) % 7 == wk) wblock(k - 1, j);
-      }
-      if ((threadIdx.x & 31) == 0) ts[(threadIdx.x >> 5) * 40 + 4 * k + 2] = clock64();
     }
   }
   __syncthreads();
