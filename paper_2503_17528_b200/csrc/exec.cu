@@ -444,9 +444,45 @@ __device__ __forceinline__ void acc_to_smem(double *St, const double (&acc)[2][4
 
 // load an m x n tile (row-major, ld) into smem [64][LDT], zero padded
 __device__ __forceinline__ void tile_to_smem(double *St, const double *g, int ld, int m, int n) {
+  if (m == SERINV_TILE && n == SERINV_TILE && (((uintptr_t)g | (uintptr_t)ld) & 1) == 0 &&
+      ((uintptr_t)g & 15) == 0) {
+    // full aligned tile: all 16-byte loads in flight together (cp.async), one wait
+#pragma unroll
+    for (int it = 0; it < (SERINV_TILE * SERINV_TILE / 2) / NT; ++it) {
+      const int idx = threadIdx.x + it * NT, r = idx >> 5, c2 = (idx & 31) * 2;
+      unsigned s = (unsigned)__cvta_generic_to_shared(St + r * LDT + c2);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g + (int64_t)r * ld + c2) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    return;
+  }
   for (int idx = threadIdx.x; idx < SERINV_TILE * SERINV_TILE; idx += NT) {
     int r = idx >> 6, c = idx & 63;
     St[r * LDT + c] = (r < m && c < n) ? __ldcg(g + (int64_t)r * ld + c) : 0.0;
+  }
+}
+
+// acc(16 x 32 warp slab of a 64 x 64 result) += A B over K = 64 from two [64][LDT]
+// smem tiles, compile-time strides, fully unrolled: A(r,k) = As[r][k];
+// B(k,c) = Bs[c][k] (BT) or Bs[k][c]
+template <bool BT>
+__device__ __forceinline__ void mma_smem64(const double *As, const double *Bs, double (&acc)[2][4][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kq = lane & 3;
+  const double *Ap = As + ((warp >> 1) * 16 + (lane >> 2)) * LDT + kq;
+  const double *Bp = BT ? Bs + ((warp & 1) * 32 + (lane >> 2)) * LDT + kq : Bs + kq * LDT + (warp & 1) * 32 + (lane >> 2);
+#pragma unroll
+  for (int ks = 0; ks < SERINV_TILE / 4; ++ks) {
+    const double a0 = Ap[ks * 4], a1 = Ap[8 * LDT + ks * 4];
+    double b[4];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = BT ? Bp[ni * 8 * LDT + ks * 4] : Bp[ks * 4 * LDT + ni * 8];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      dmma(acc[0][ni], a0, b[ni]);
+      dmma(acc[1][ni], a1, b[ni]);
+    }
   }
 }
 
@@ -810,7 +846,12 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem, int tsk) 
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const bool rt = (T.flags & TF_POST_T) != 0;
     // out = S * op(R): B(k, j) = R[j][k] (POST_T) or R[k][j]
-    mma_steps(St, LDT, 1, Rt, rt ? LDT : 1, rt ? 1 : LDT, acc, (T.n + 3) / 4);
+    if (T.n == SERINV_TILE) {
+      if (rt) mma_smem64<true>(St, Rt, acc);
+      else mma_smem64<false>(St, Rt, acc);
+    } else {
+      mma_steps(St, LDT, 1, Rt, rt ? LDT : 1, rt ? 1 : LDT, acc, (T.n + 3) / 4);
+    }
     __syncthreads();
   }
   phase_mark(p, tsk, 6);
@@ -843,7 +884,13 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem, int tsk) 
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    mma_steps(Lt, LDT, 1, Lt, LDT, 1, acc, (T.n + 3) / 4);
+    if (T.n == SERINV_TILE) {
+      // only the lower triangle of L L^T is used downstream: the warp whose slab is
+      // strictly upper (rows 0-15, columns 32-63) skips its products
+      if (!((threadIdx.x >> 5) == 1)) mma_smem64<true>(Lt, Lt, acc);
+    } else {
+      mma_steps(Lt, LDT, 1, Lt, LDT, 1, acc, (T.n + 3) / 4);
+    }
     cp_wait<0>();
     __syncthreads();
 #pragma unroll
