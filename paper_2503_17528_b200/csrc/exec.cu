@@ -486,6 +486,22 @@ __device__ __forceinline__ void mma_smem64(const double *As, const double *Bs, d
   }
 }
 
+// smem [64][LDT] tile -> global (m x n at g, row stride ld); 16-byte stores when full and aligned
+__device__ __forceinline__ void smem_to_global(double *g, int64_t ld, const double *S, int m, int n) {
+  if (m == SERINV_TILE && n == SERINV_TILE && (((uintptr_t)g & 15) | (ld & 1)) == 0) {
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < SERINV_TILE * SERINV_TILE / 2; idx += NT) {
+      const int i = idx >> 5, k2 = (idx & 31) * 2;
+      *reinterpret_cast<double2 *>(g + (int64_t)i * ld + k2) = make_double2(S[i * LDT + k2], S[i * LDT + k2 + 1]);
+    }
+    return;
+  }
+  for (int idx = threadIdx.x; idx < SERINV_TILE * SERINV_TILE; idx += NT) {
+    const int i = idx >> 6, k = idx & 63;
+    if (i < m && k < n) g[(int64_t)i * ld + k] = S[i * LDT + k];
+  }
+}
+
 __device__ void store_tile(const Params &p, const Loc &loc, int m, int n, const double (&acc)[2][4][2]) {
   double *o = lptr(p, loc);
   const bool vec = ((loc.off | loc.ld) & 1) == 0;
@@ -834,11 +850,14 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem, int tsk) 
   }
   if (T.flags & TF_POST) {
     // S (this result) goes to the stage after the prefetched ones; R from its stage
-    double *St = pfr ? smem + ((nch + 2) % STAGES) * 2 * OPSZ : smem;
-    double *Rt = pfr ? Rs : smem + SERINV_TILE * LDT;
-    if (!pfr && pfc) __syncthreads();  // C0 (read above) may overlap St / Rt
+    // carried chain: W is the previous task's (the POTRF's) Wt; smem[0..) stays free
+    // for the SYRK target that the next POTRF consumes
+    const bool carry = (T.flags & TF_CARRY) != 0;
+    double *St = carry ? smem + 2 * SERINV_TILE * LDT : (pfr ? smem + ((nch + 2) % STAGES) * 2 * OPSZ : smem);
+    double *Rt = carry ? smem + SERINV_TILE * LDT : (pfr ? Rs : smem + SERINV_TILE * LDT);
+    if (!pfr && pfc && !carry) __syncthreads();  // C0 (read above) may overlap St / Rt
     acc_to_smem(St, acc);
-    if (!pfr) tile_to_smem(Rt, lptr(p, T.r), T.r.ld, T.n, T.n);
+    if (!pfr && !carry) tile_to_smem(Rt, lptr(p, T.r), T.r.ld, T.n, T.n);
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -860,8 +879,9 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem, int tsk) 
   if (T.flags & TF_SYRK3) {
     // the next diagonal tile of the chain: out3 -= L L^T (L = this result, m x n);
     // stage the target tile into smem with cp.async while the SYRK runs
-    double *Lt = smem;
-    double *Ct = smem + SERINV_TILE * LDT;
+    const bool carry = (T.flags & TF_CARRY) != 0;
+    double *Lt = carry ? smem + 2 * SERINV_TILE * LDT : smem;
+    double *Ct = carry ? smem : smem + SERINV_TILE * LDT;
     {
       const double *g = lptr(p, T.out3);
       const bool vec = ((T.out3.off | T.out3.ld) & 1) == 0;
@@ -904,6 +924,10 @@ __device__ void run_gemm(const Params &p, const Task &T, double *smem, int tsk) 
           acc[mi][ni][h] = Ct[r * LDT + c] - acc[mi][ni][h];
         }
     store_tile(p, T.out3, T.m, T.m, acc);
+    if (carry) {  // the updated diagonal tile stays in smem[0..) for the next POTRF (same CTA)
+      __syncthreads();
+      acc_to_smem(Ct, acc);
+    }
     __syncthreads();
   }
 }
@@ -1252,7 +1276,10 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   __shared__ int s_bad;
   const bool trsm2 = factor && (T.flags & TF_TRSM2);
   double acc2[2][4][2];
-  if (factor) {
+  if (factor && (T.flags & TF_CARRY)) {
+    // carried chain: the previous task on this CTA (the chain TRSM+SYRK) left the
+    // fully updated tile in St
+  } else if (factor) {
     double acc1[2][4][2];
     // both fused updates (diagonal tile, sub-diagonal tile) through one pipeline
     if (trsm2)
@@ -1403,11 +1430,7 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
     // W = L^{-1} is what the chain's next TRSM waits for: store it and publish the
     // task's own counter now; the log-det partial and L follow (their readers wait
     // on the factor-done counter, signalled at the end)
-    double *wo = lptr(p, T.out2);
-    for (int idx = tid; idx < SERINV_TILE * SERINV_TILE; idx += NT) {
-      const int i = idx >> 6, k = idx & 63;
-      if (i < m && k < m) wo[(int64_t)i * T.out2.ld + k] = Wt[i * LDT + k];
-    }
+    smem_to_global(lptr(p, T.out2), T.out2.ld, Wt, m, m);
     __syncthreads();
     if (tid == 0) {
       __threadfence();
@@ -1472,15 +1495,8 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   {
     const bool wout = (!factor || (T.flags & TF_W_OUT)) && !early;
     const Loc &wl = factor ? T.out2 : T.out;
-    double *o = factor ? lptr(p, T.out) : nullptr;
-    double *wo = wout ? lptr(p, wl) : nullptr;
-    for (int idx = tid; idx < SERINV_TILE * SERINV_TILE; idx += NT) {
-      const int i = idx >> 6, k = idx & 63;
-      if (i < m && k < m) {
-        if (o) o[(int64_t)i * T.out.ld + k] = St[i * LDT + k];
-        if (wo) wo[(int64_t)i * wl.ld + k] = Wt[i * LDT + k];
-      }
-    }
+    if (factor) smem_to_global(lptr(p, T.out), T.out.ld, St, m, m);
+    if (wout) smem_to_global(lptr(p, wl), wl.ld, Wt, m, m);
   }
   phase_mark(p, tsk, 4);
 }

@@ -252,6 +252,7 @@ struct Builder {
   std::vector<int32_t> input_waits;  // extra waits for tasks reading the problem's inputs
   int flush_queue = 0;               // claim queue of update tasks being flushed
   int concurrency = 1;               // independent chains whose inversion waves overlap (twisted: 2)
+  std::map<int, int> last_chain_ts;  // carried chain: last chain TRSM+SYRK task per claim queue
   // wide (128-row) tasks for a wave of `tiles` independent 64 x 64 output tiles
   bool use_wide(int tiles) const {
     return cx.opt.wide_min_wave > 0 && tiles * std::max(1, concurrency) >= cx.opt.wide_min_wave;
@@ -401,8 +402,17 @@ struct Builder {
       int w = tdim(P.size[X], c);
       std::vector<RT> rts = column_rows(X, c);
       size_t first_trsm = 0;
+      // carried chain only for large blocks: there the FP64 work hides the serialised
+      // TRSM+SYRK and the freed SM helps (C3 954 -> 937 ms); for b <= 1024 the split
+      // chain's overlap wins (C2 57.1 vs 58.2 ms)
+      const bool carry = cx.opt.carry_chain && cx.opt.critical_queues && cx.opt.split_chain && cx.opt.chain_syrk &&
+                         !cx.opt.fuse_trsm && P.q1(X) > 0 && P.size[X] >= cx.opt.carry_min_b;
       {  // POTRF of the diagonal tile with the last update fused in (+ the sub-diagonal TRSM)
         TileState &st = tstate[tkey(X, X, c, c)];
+        // carried chain: the tile's last writer is the chain TRSM+SYRK that ran just
+        // before on this claim queue (same CTA), which left the tile in shared memory
+        const bool carry_in = carry && st.pending.empty() && st.last >= 0 && last_chain_ts.count(P.q1(X)) &&
+                              last_chain_ts[P.q1(X)] == st.last;
         flush(X, c, X, c, d, st, 1);
         RawTask rt;
         rt.t.type = TK_POTRF;
@@ -415,7 +425,7 @@ struct Builder {
         rt.t.nseg1 = (int32_t)rt.segs.size();
         if (st.last >= 0) rt.waits.push_back(cx.ctr_of(st.last));
         for (int32_t iw : input_waits) rt.waits.push_back(iw);
-        rt.t.flags = TF_W_OUT | (cx.opt.chol8 ? TF_CHOL8 : 0);
+        rt.t.flags = TF_W_OUT | (cx.opt.chol8 ? TF_CHOL8 : 0) | (carry_in ? TF_CARRY : 0);
         rt.t.out2 = tileloc(P.W[X], c, c);
         rt.t.aux0 = (int32_t)(P.slot[X] + c);
         rt.t.r = wsloc(cx.slot_region + P.slot[X] + c, 0);
@@ -497,7 +507,15 @@ struct Builder {
         // updates feeding the chain's next two tiles are near-critical: urgent queue
         const bool near = cx.opt.critical_queues && cx.opt.split_chain && cx.opt.urgent_ctas > 0 && ri < 2;
         flush_queue = near ? URGENT_QUEUE : 0;
-        flush(r.Y, r.q, X, c, tb, st, 1);
+        // carried chain TRSM+SYRK: runs on the POTRF's CTA right after it (W in shared
+        // memory), so all of its tile's earlier updates are flushed to bulk tasks
+        bool chain_carry = false;
+        if (carry && ri == 0 && first_trsm == 0 && has(r.Y, r.Y)) {
+          const BlkRef &bd = B(r.Y, r.Y);
+          const TileState &sd0 = tstate[tkey(r.Y, r.Y, r.q, r.q)];
+          chain_carry = !(bd.zero_init && !sd0.written) && r.h == TILE && w == TILE;
+        }
+        flush(r.Y, r.q, X, c, tb, st, chain_carry ? 0 : 1);
         RawTask rt;
         rt.t.type = TK_GEMM;
         rt.t.m = (int16_t)r.h;
@@ -543,13 +561,18 @@ struct Builder {
         rt.sigs.push_back(fd);
         // the sub-diagonal TRSMs feed the next POTRF: critical queues too
         flush_queue = 0;
+        if (chain_carry && sdp) rt.t.flags |= TF_CARRY;
         if (cx.opt.critical_queues) {
-          if (cx.opt.split_chain && first_trsm == 0 && ri == 0) rt.queue = P.q2(X);
+          if (chain_carry && sdp) rt.queue = P.q1(X);
+          else if (cx.opt.split_chain && first_trsm == 0 && ri == 0) rt.queue = P.q2(X);
           else if (cx.opt.split_chain && first_trsm == 0 && ri == 1 && cx.opt.rts1_chain) rt.queue = P.q2(X);
           else if (cx.opt.split_chain && first_trsm == 0 && ri == 1 && cx.opt.urgent_ctas > 0) rt.queue = URGENT_QUEUE;
           else if (ri == first_trsm && first_trsm == 1) rt.queue = P.q1(X);
         }
+        const bool is_carry = (rt.t.flags & TF_CARRY) != 0;
+        const int rq = rt.queue;
         int id = cx.emit(std::move(rt));
+        if (is_carry) last_chain_ts[rq] = id;
         st.pending.clear();
         st.last = id;
         st.written = true;
@@ -1023,6 +1046,15 @@ Graph Ctx::finalize() {
     for (int32_t s : rt.sigs) g.sigs.push_back(s);
     g.tasks.push_back(task);
     g.flops += rt.flops;
+  }
+  {  // compact the critical queue ids (a carried chain leaves its TRSM queue empty)
+    std::map<int, int> qmap;
+    for (int t : order)
+      if (tasks[t].queue > 0 && tasks[t].queue != URGENT_QUEUE) qmap[tasks[t].queue] = 0;
+    int k = 0;
+    for (auto &kv : qmap) kv.second = ++k;
+    for (int t : order)
+      if (tasks[t].queue > 0 && tasks[t].queue != URGENT_QUEUE) tasks[t].queue = qmap[tasks[t].queue];
   }
   int ncrit = 0;
   bool has_urgent = false;
@@ -1745,6 +1777,8 @@ void BuildOptions::apply_env() {
       else if (k == "chol8") chol8 = v != 0;
       else if (k == "twist_last") twist_last = v != 0;
       else if (k == "early_sig") early_sig = v != 0;
+      else if (k == "carry_chain") carry_chain = v != 0;
+      else if (k == "carry_min_b") carry_min_b = (int)v;
     }
     i = j + 1;
   }

@@ -46,6 +46,8 @@ enum TaskFlags : uint16_t {
   TF_SYRK3 = 256,     // TK_GEMM (+TF_POST): then out3 (m x m) -= L L^T with L the result
   TF_CHOL8 = 512,     // TK_POTRF: warp-pipelined 8 x 8-block Cholesky + inverse (chol8_pipelined)
   TF_EARLY_SIG = 1024,  // TK_POTRF (+TF_W_OUT, no TF_TRSM2): own counter signalled once W is stored
+  TF_CARRY = 2048,    // carried chain (same CTA, consecutive tasks): TK_POTRF reads its tile from smem St;
+                      // TK_GEMM (+TF_POST|TF_SYRK3) reads W from smem Wt and leaves the SYRK result in St
 };
 
 // Buffer ids (kernel argument `bufs[]`, offsets in doubles).

@@ -148,3 +148,23 @@ def test_selinv_host_streaming(n, b, a):
         e, where = inv.max_block_err(G, X)
         assert e <= TOL, (e, where)
         assert abs(ldg - ld) <= 1e-12 * max(1.0, abs(ld))
+
+
+@pytest.mark.parametrize("opt", ["carry_min_b=64", "carry_min_b=64,twist_min_n=0", "chol8=0", "early_sig=0",
+                                 "wide_min_wave=1", "fuse_trsm=1,split_chain=0"])
+def test_scheduling_variants_parity(opt, monkeypatch):
+    """Graph-build options (SERINV_OPT, read when a handle builds a graph) change the
+    task structure -- carried chain, one-sided order, 16x16-leaf POTRF, late
+    publication, wide tasks, fused TRSM -- never the results."""
+    sb = _sb()
+    monkeypatch.setenv("SERINV_OPT", opt)
+    h = sb.Handle(0)
+    A = btagen.g2(31, 6, 192, 5)
+    L, X, ld = seq.selinv(A)
+    D = to_dev(A)
+    ldg = sb.selinv(*args(D), handle=h)
+    assert inv.max_block_err(to_host(D), X)[0] <= TOL
+    assert abs(ldg - ld) <= 1e-12 * abs(ld)
+    D = to_dev(A)
+    sb.pselinv(*args(D), 3, handle=h)
+    assert inv.max_block_err(to_host(D), X)[0] <= TOL
