@@ -81,7 +81,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--r", type=float, default=1.0, help="load-balance ratio for N > 1")
+    ap.add_argument("--r", type=float, default=1.7,
+                    help="N > 1: blocks of the first / last rank relative to a middle rank (serinv_plan_ends)")
     ap.add_argument("--partitions", default="auto",
                     help="N = 1: intra-GPU partitions, e.g. 1 (sequential), 8, 256x16 (nested); "
                          "'auto' = the library's plan (serinv_auto_partitions)")
@@ -231,7 +232,9 @@ def main():
                               check=False, info=info, logdet=logdet)
     else:
         from paper_2503_17528_b200 import distributed as sd
-        parts = sb.plan(n, world, args.r)
+        # twisted scheme (reading R14): first and last rank are fill-in free, so they
+        # take r x a middle rank's blocks (flop/chain balance)
+        parts = sb.plan_ends(n, world, args.r)
         s, e = parts[rank]
         pristine = btagen.g1_torch(0, n, b, a, device=f"cuda:{local}", start=s, end=e)
         if pristine["lower"].shape[0] == 0:

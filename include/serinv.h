@@ -149,6 +149,14 @@ int serinv_selinv_host(serinv_handle_t h, const serinv_bta_t *A_host, const seri
  */
 int serinv_plan(int64_t n, int P, double r, int64_t *starts);
 
+/* Partition plan for the twisted scheme (reading R14: the last partition
+ * is eliminated bottom-up, so the first and the last partition are fill-in free):
+ * both ends get r times a middle partition's blocks, middles split the rest evenly
+ * (each >= 2), the remainder to the earliest; P = 2 gives equal halves, r = 1 the
+ * same partition as serinv_plan.  starts: host int64[P + 1], caller-owned.
+ * Returns 0, -3 (r not positive/finite), -4 (NULL), SERINV_ERR_PLAN (infeasible). */
+int serinv_plan_ends(int64_t n, int P, double r, int64_t *starts);
+
 /*
  * In-process partitioned selected inversion on ONE device: PPOBTAF (Alg. 3-4)
  * over P partitions, POBTARSSI on the reduced system of 2P-1 blocks (Sec. 3.3),

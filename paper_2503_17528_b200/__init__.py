@@ -232,6 +232,14 @@ def plan(n: int, P: int, r: float = 1.0):
     return [(starts[p], starts[p + 1]) for p in range(P)]
 
 
+def plan_ends(n: int, P: int, r: float = 1.0):
+    """Twisted-scheme partition plan (reading R14, serinv_plan_ends): the first and
+    the last partition get r times a middle partition's blocks.  [(start, end)]."""
+    starts = (ctypes.c_int64 * (P + 1))()
+    _check(_lib.lib().serinv_plan_ends(n, P, float(r), starts), "serinv_plan_ends")
+    return [(starts[p], starts[p + 1]) for p in range(P)]
+
+
 def auto_partitions(n: int, b: int) -> list[int]:
     """The library's default one-device nesting plan (serinv_auto_partitions)."""
     out = (ctypes.c_int * 8)()

@@ -52,6 +52,7 @@ def lib():
     L.serinv_pobtasi.argtypes = [c_p, ctypes.POINTER(BTA), c_p, ctypes.c_size_t, c_p, c_p]
     L.serinv_selinv.argtypes = [c_p, ctypes.POINTER(BTA), c_p, ctypes.c_size_t, c_p, c_p, c_p]
     L.serinv_plan.argtypes = [c_i64, ctypes.c_int, ctypes.c_double, ctypes.POINTER(c_i64)]
+    L.serinv_plan_ends.argtypes = [c_i64, ctypes.c_int, ctypes.c_double, ctypes.POINTER(c_i64)]
     L.serinv_pselinv_ws.argtypes = [c_i64, c_i64, c_i64, ctypes.c_int, ctypes.c_double, sz]
     L.serinv_pselinv.argtypes = [c_p, ctypes.POINTER(BTA), ctypes.c_int, ctypes.c_double, c_p,
                                  ctypes.c_size_t, c_p, c_p, c_p]
@@ -82,7 +83,7 @@ def lib():
 EXPORTED = [
     "serinv_version", "serinv_status_string", "serinv_create", "serinv_destroy",
     "serinv_pobtaf_ws", "serinv_pobtasi_ws", "serinv_selinv_ws", "serinv_prepare",
-    "serinv_pobtaf", "serinv_pobtasi", "serinv_selinv", "serinv_plan",
+    "serinv_pobtaf", "serinv_pobtasi", "serinv_selinv", "serinv_plan", "serinv_plan_ends",
     "serinv_pselinv_ws", "serinv_pselinv", "serinv_exchange_bytes", "serinv_ppobtaf_ws",
     "serinv_ppobtaf", "serinv_ppobtasi", "serinv_graph_stats", "serinv_last_launches", "serinv_set_trace", "serinv_selinv_host", "serinv_bench_gemm",
     "serinv_auto_partitions", "serinv_pselinv_nested_ws", "serinv_pselinv_nested", "serinv_graph_stats_nested",

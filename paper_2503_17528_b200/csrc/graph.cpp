@@ -1832,6 +1832,36 @@ bool plan_partitions(int64_t n, int P, double r, std::vector<int64_t> &starts) {
   return s == n;
 }
 
+// Plan for the twisted scheme (reading R14): the first and the last partition
+// have no fill-in, so both get r times a middle partition's blocks; middles split
+// the rest evenly (each >= 2), the remainder to the earliest.  r = 1 gives the
+// same partition as plan_partitions.
+bool plan_partitions_ends(int64_t n, int P, double r, std::vector<int64_t> &starts) {
+  starts.clear();
+  if (P < 1 || n < 1) return false;
+  if (P == 2 && n >= 2) {  // both partitions are chain ends: equal halves
+    starts = {0, n / 2, n};
+    return true;
+  }
+  if (P == 1 || r == 1.0) return plan_partitions(n, P, 1.0, starts);
+  if (n < 2 * (int64_t)P - 2) return false;
+  const double mid = (double)n / (2.0 * r + (double)(P - 2));
+  int64_t end = std::max<int64_t>(1, (int64_t)std::llround(r * mid));
+  end = std::min<int64_t>(end, (n - 2 * (int64_t)(P - 2)) / 2);
+  if (end < 1) return false;
+  int64_t rest = n - 2 * end, base = rest / (P - 2), rem = rest % (P - 2);
+  if (base < 2) return false;
+  starts.push_back(0);
+  int64_t s = end;
+  starts.push_back(s);
+  for (int p = 1; p < P - 1; ++p) {
+    s += base + ((p - 1) < rem ? 1 : 0);
+    starts.push_back(s);
+  }
+  starts.push_back(n);
+  return s + end == n;
+}
+
 int64_t exchange_doubles(int64_t b, int64_t a) { return (4 * b * b + 2 * a * b + a * a + 1 + 31) / 32 * 32; }
 
 // One level of the (nested) partitioned solve of the BTA matrix V (n blocks, tip
@@ -1843,7 +1873,8 @@ bool psolve_level(Ctx &cx, const View &V, int64_t n, int64_t b, int64_t a, const
                   double r, const std::vector<int32_t> &inw) {
   const int P = Ps[lvl];
   std::vector<int64_t> starts;
-  if (P < 1 || (lvl > 0 && P < 2) || !plan_partitions(n, P, r, starts)) return false;
+  const bool ok = cx.opt.twist_last ? plan_partitions_ends(n, P, r, starts) : plan_partitions(n, P, r, starts);
+  if (P < 1 || (lvl > 0 && P < 2) || !ok) return false;
   const int64_t recsz = exchange_doubles(b, a);
   const int64_t recs = cx.alloc(recsz * P);
   std::vector<PartState> parts(P);

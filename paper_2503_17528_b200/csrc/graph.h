@@ -147,6 +147,8 @@ int reduced_size(int P, bool twisted_last);
 
 // Partition plan (reading R6).  Returns false if infeasible.
 bool plan_partitions(int64_t n, int P, double r, std::vector<int64_t> &starts);
+// Twisted-scheme plan (reading R14): first and last partition r x a middle one.
+bool plan_partitions_ends(int64_t n, int P, double r, std::vector<int64_t> &starts);
 
 // Bytes reserved at the end of the workspace for counters (+1 claim counter).
 int64_t counter_bytes(int32_t nctr);

@@ -338,6 +338,15 @@ int serinv_plan(int64_t n, int P, double r, int64_t *starts) {
   return SERINV_OK;
 }
 
+int serinv_plan_ends(int64_t n, int P, double r, int64_t *starts) {
+  if (!starts) return -4;
+  if (!(r > 0.0) || !std::isfinite(r)) return -3;
+  std::vector<int64_t> s;
+  if (!plan_partitions_ends(n, P, r, s)) return SERINV_ERR_PLAN;
+  for (size_t i = 0; i < s.size(); ++i) starts[i] = s[i];
+  return SERINV_OK;
+}
+
 // workspace queries of the partitioned graphs build the graph: memoise them
 static std::mutex g_ws_mu;
 static std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int64_t, int, int64_t, int64_t>, int64_t> g_ws_cache;

@@ -249,3 +249,38 @@ def test_wide_tasks(n, b, a, monkeypatch):
         rc, R, ldr, info = run_nested(A0, [2])
         assert rc == 0 and info == 0
         assert inv.max_block_err(cut(R, X), X)[0] < 1e-12
+
+
+def test_plan_ends_policy():
+    # serinv_plan_ends (reading R14): both chain ends take r x a middle's blocks
+    from paper_2503_17528_b200 import plan, plan_ends
+    for n in range(2, 70):
+        for P in range(1, 9):
+            for r in (0.5, 1.0, 1.7, 3.0):
+                if n < 2 * P - 1:
+                    continue
+                pe = plan_ends(n, P, r)
+                assert pe[0][0] == 0 and pe[-1][1] == n
+                assert all(pe[i][1] == pe[i + 1][0] for i in range(P - 1))
+                assert all(e - s >= 1 for s, e in pe)
+                assert all(e - s >= 2 for s, e in pe[1:-1])
+                if r == 1.0 and P != 2:
+                    assert pe == plan(n, P, 1.0)
+                if P == 2:
+                    assert pe == [(0, n // 2), (n // 2, n)]
+    pe = plan_ends(1024, 8, 1.7)
+    assert pe[0][1] - pe[0][0] == pe[-1][1] - pe[-1][0] > pe[1][1] - pe[1][0]
+
+
+@pytest.mark.parametrize("r", [0.5, 1.7, 2.5])
+@pytest.mark.parametrize("P", [3, 4, 6])
+def test_pselinv_graph_ends_plan(P, r):
+    A0 = btagen.g2(8, 30, 20, 3)
+    L, X, ld = seq.selinv(A0)
+    A, n, b, a = prep(A0)
+    ldv, info, nt = ctypes.c_double(0), ctypes.c_int(0), ctypes.c_int64(0)
+    rc = lib().dag_run_pselinv(ctypes.c_int64(n), ctypes.c_int64(b), ctypes.c_int64(a), P, ctypes.c_double(r),
+                               *ptrs(A), ctypes.byref(ldv), ctypes.byref(info), 16, ctypes.byref(nt))
+    assert rc == 0 and info.value == 0
+    assert inv.max_block_err(cut(A, X), X)[0] < 1e-11
+    assert abs(ldv.value - ld) <= 1e-12 * max(1, abs(ld))

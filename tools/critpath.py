@@ -77,6 +77,17 @@ def main():
     for key, v in sorted(stats.items(), key=lambda kv: -len(kv[1])):
         v = np.array(v) / 1e3
         print(f"{key[0]:14s} {key[1]:14s} {len(v):6d} {v[:, 0].mean():8.2f} {v[:, 1].mean():10.2f} {v[:, 2].mean():8.2f}")
+    # timeline of a few consecutive chain steps (queues 1 and 2), relative to the first
+    ph = buf[4 * T:].view(T, 8).cpu().numpy().astype(np.int64) - t0
+    sel = [t for t in chain if q[t] in (1, 2)]
+    sel.sort(key=lambda t: start[t])
+    mid = len(sel) // 2
+    base = claim[sel[mid]]
+    print("timeline (us, relative): queue role claim start [phases] end")
+    for t in sel[mid:mid + 8]:
+        p = [f"{(v - base) / 1e3:7.2f}" for v in ph[t] if v > 0]
+        print(f"  q{q[t]} {role(typ[t], fl[t], q[t]):10s} {(claim[t] - base) / 1e3:7.2f} {(start[t] - base) / 1e3:7.2f} "
+              f"[{' '.join(p)}] {(end[t] - base) / 1e3:7.2f}")
     # period of each critical queue
     for qq in (1, 2, 3, 4):
         sel = [t for t in chain if q[t] == qq]

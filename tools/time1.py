@@ -10,6 +10,7 @@ from tools.sweep import CFG, flops
 name = sys.argv[1]
 P = sys.argv[2] if len(sys.argv) > 2 else "1"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+r = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
 n, b, a = CFG[name]
 Ps = sb.auto_partitions(n, b) if P == "auto" else [int(x) for x in P.split("x")]
 A0 = btagen.g1_torch(0, n, b, a)
@@ -24,9 +25,9 @@ for r in range(reps + 1):
     if Ps == [1]:
         sb.selinv(D["diag"], D["lower"], D["arrow"], D["tip"], check=False)
     else:
-        sb.pselinv(D["diag"], D["lower"], D["arrow"], D["tip"], Ps, check=False)
+        sb.pselinv(D["diag"], D["lower"], D["arrow"], D["tip"], Ps, r, check=False)
     e1.record(); torch.cuda.synchronize()
     if r:
         ts.append(e0.elapsed_time(e1))
 ms = min(ts)
-print(f"{name} P={P} opt={os.environ.get('SERINV_OPT', '')}: {ms:.2f} ms {flops(n, b, a) / ms / 1e9:.2f} TF/s (all {[round(t, 2) for t in ts]})", flush=True)
+print(f"{name} P={P} r={r} opt={os.environ.get('SERINV_OPT', '')}: {ms:.2f} ms {flops(n, b, a) / ms / 1e9:.2f} TF/s (all {[round(t, 2) for t in ts]})", flush=True)
