@@ -81,7 +81,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--r", type=float, default=1.7,
+    ap.add_argument("--r", type=float, default=1.0,
                     help="N > 1: blocks of the first / last rank relative to a middle rank (serinv_plan_ends)")
     ap.add_argument("--partitions", default="auto",
                     help="N = 1: intra-GPU partitions, e.g. 1 (sequential), 8, 256x16 (nested); "

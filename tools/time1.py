@@ -16,7 +16,7 @@ Ps = sb.auto_partitions(n, b) if P == "auto" else [int(x) for x in P.split("x")]
 A0 = btagen.g1_torch(0, n, b, a)
 D = {k: v.clone() for k, v in A0.items()}
 ts = []
-for r in range(reps + 1):
+for it in range(reps + 1):
     for k in D:
         D[k].copy_(A0[k])
     torch.cuda.synchronize()
@@ -27,7 +27,7 @@ for r in range(reps + 1):
     else:
         sb.pselinv(D["diag"], D["lower"], D["arrow"], D["tip"], Ps, r, check=False)
     e1.record(); torch.cuda.synchronize()
-    if r:
+    if it:
         ts.append(e0.elapsed_time(e1))
 ms = min(ts)
 print(f"{name} P={P} r={r} opt={os.environ.get('SERINV_OPT', '')}: {ms:.2f} ms {flops(n, b, a) / ms / 1e9:.2f} TF/s (all {[round(t, 2) for t in ts]})", flush=True)
