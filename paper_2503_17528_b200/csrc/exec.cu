@@ -1434,8 +1434,59 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
     __syncthreads();
     if (tid == 0) {
       __threadfence();
-      atomicAdd(p.ctr + p.sigs[T.sig0], 1);
+      atomicAdd(p.ctr + p.sigs[T.sig0 + ((T.flags & TF_CHAINSTEP) ? 1 : 0)], 1);
     }
+  }
+  const bool chainstep = factor && (T.flags & TF_CHAINSTEP) && early;
+  if (chainstep) {
+    // fused chain step: E's and the next tile's earlier updates (bulk tasks) are the
+    // late inputs; W stays in Wt, E W^T and the next tile are formed in smem
+    if (tid == 0) wait_range(p, T.wait0 + T.nwait - T.nlate, T.wait0 + T.nwait);
+    __syncthreads();
+    tile_to_smem(S2, lptr(p, T.out3), T.out3.ld, T.m3, m);
+    __syncthreads();
+    double acc[2][4][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    mma_smem64<true>(S2, Wt, acc);  // L(K+1,K) = E W^T
+    store_tile(p, T.out3, T.m3, m, acc);
+    if (T.zmask & 1) {  // strict-upper tile (c, c+1) of the diagonal block
+      double *z = lptr(p, T.out) + SERINV_TILE;
+      for (int idx = tid; idx < m * T.m3; idx += NT) {
+        const int rr = idx / T.m3, cc = idx - rr * T.m3;
+        z[(int64_t)rr * T.out.ld + cc] = 0.0;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {  // publish the sub-diagonal tile (sigs[1]) for the bulk updates
+      __threadfence();
+      atomicAdd(p.ctr + p.sigs[T.sig0 + 2], 1);
+    }
+    smem_to_global(lptr(p, T.out), T.out.ld, St, m, m);  // L(K,K); St is reused below
+    acc_to_smem(S2, acc);
+    __syncthreads();
+    tile_to_smem(St, lptr(p, T.out4), T.out4.ld, T.m4, T.m4);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    if (warp != 1) mma_smem64<true>(S2, S2, acc);  // lower triangle of L L^T (warp 1's slab is upper)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int rr, cc;
+          frag_rc(mi, ni, h, rr, cc);
+          acc[mi][ni][h] = St[rr * LDT + cc] - acc[mi][ni][h];
+        }
+    store_tile(p, T.out4, T.m4, T.m4, acc);
+    __syncthreads();
+    acc_to_smem(St, acc);  // carried into the next POTRF on this CTA
   }
   if (factor) {
     // log det partial: sum_j 0.5 log d_j, fixed-order tree over 64 values
@@ -1495,7 +1546,7 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   {
     const bool wout = (!factor || (T.flags & TF_W_OUT)) && !early;
     const Loc &wl = factor ? T.out2 : T.out;
-    if (factor) smem_to_global(lptr(p, T.out), T.out.ld, St, m, m);
+    if (factor && !chainstep) smem_to_global(lptr(p, T.out), T.out.ld, St, m, m);
     if (wout) smem_to_global(lptr(p, wl), wl.ld, Wt, m, m);
   }
   phase_mark(p, tsk, 4);
@@ -1686,8 +1737,11 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
     __syncthreads();
     if (threadIdx.x == NT - 32) {
       __threadfence();
-      const int s0 = (T.type == TK_POTRF && (T.flags & TF_EARLY_SIG) && (T.flags & TF_W_OUT)) ? 1 : 0;
-      for (int s = s0; s < T.nsig; ++s) atomicAdd(p.ctr + p.sigs[T.sig0 + s], 1);
+      const bool ew = T.type == TK_POTRF && (T.flags & TF_EARLY_SIG) && (T.flags & TF_W_OUT);
+      const bool cs = ew && (T.flags & TF_CHAINSTEP);
+      // early-published signals: sigs[0] (W), or sigs[1] (W) and sigs[2] (sub-diagonal tile) of a chain step
+      for (int s = (ew && !cs) ? 1 : 0; s < T.nsig; ++s)
+        if (!(cs && (s == 1 || s == 2))) atomicAdd(p.ctr + p.sigs[T.sig0 + s], 1);
       if (p.trace) {
         unsigned long long *rec = p.trace + 4 * (size_t)t;
         rec[2] = globaltimer();

@@ -406,7 +406,8 @@ struct Builder {
       // TRSM+SYRK and the freed SM helps (C3 954 -> 937 ms); for b <= 1024 the split
       // chain's overlap wins (C2 57.1 vs 58.2 ms)
       const bool carry = cx.opt.carry_chain && cx.opt.critical_queues && cx.opt.split_chain && cx.opt.chain_syrk &&
-                         !cx.opt.fuse_trsm && P.q1(X) > 0 && P.size[X] >= cx.opt.carry_min_b;
+                         !cx.opt.fuse_trsm && P.q1(X) > 0 && (P.size[X] >= cx.opt.carry_min_b || cx.opt.chain_step);
+      uint64_t step_dk = ~0ull;  // next diagonal tile updated inside a fused chain step
       {  // POTRF of the diagonal tile with the last update fused in (+ the sub-diagonal TRSM)
         TileState &st = tstate[tkey(X, X, c, c)];
         // carried chain: the tile's last writer is the chain TRSM+SYRK that ran just
@@ -447,6 +448,35 @@ struct Builder {
           first_trsm = 1;
         }
         rt.t.nseg2 = (int32_t)rt.segs.size();
+        // fused carried chain step (TF_CHAINSTEP): this task also computes the first
+        // sub-diagonal tile E W^T and applies its SYRK to the next diagonal tile,
+        // keeping W, E and the updated next tile in shared memory (same CTA); E's and
+        // the next tile's earlier updates are bulk tasks, awaited late
+        TileState *stE = nullptr, *stD = nullptr;
+        int32_t step_sctr = -1;
+        if (carry && cx.opt.chain_step && first_trsm == 0 && !rts.empty() && rts[0].h == TILE && w == TILE &&
+            has(rts[0].Y, rts[0].Y)) {
+          const RT &r0 = rts[0];
+          const BlkRef &tbE = (r0.Y == X) ? d : B(r0.Y, X);
+          const BlkRef &bd = B(r0.Y, r0.Y);
+          const uint64_t dk = tkey(r0.Y, r0.Y, r0.q, r0.q);
+          if (!(bd.zero_init && !tstate[dk].written) && !(tbE.zero_init && !tstate[tkey(r0.Y, X, r0.q, c)].written)) {
+            stE = &tstate[tkey(r0.Y, X, r0.q, c)];
+            flush(r0.Y, r0.q, X, c, tbE, *stE, 0);
+            stD = &tstate[dk];
+            flush(r0.Y, r0.q, r0.Y, r0.q, bd, *stD, 0);
+            if (stE->last >= 0) rt.late.push_back(cx.ctr_of(stE->last));
+            if (stD->last >= 0) rt.late.push_back(cx.ctr_of(stD->last));
+            rt.t.flags |= TF_CHAINSTEP;
+            rt.t.out3 = r0.loc;
+            rt.t.m3 = r0.h;
+            rt.t.out4 = tileloc(bd.base, r0.q, r0.q);
+            rt.t.m4 = r0.h;
+            if (r0.Y == X) rt.t.zmask |= 1;  // zero tile (c, c+1) = out + TILE columns
+            step_dk = dk;
+            first_trsm = 1;  // rts[0] is done here
+          }
+        }
         TileState *st1 = nullptr;
         if (first_trsm == 1 && cx.opt.fuse_trsm3 && rts.size() >= 2) {
           // the second sub-diagonal tile: its own inputs (a bulk TRSM of the previous
@@ -471,16 +501,38 @@ struct Builder {
         // the own counter (first signal) only guards W = L^{-1}: readers of the
         // factor tile and the log-det slot wait on the factor-done counter fd, and
         // readers of a fused TRSM's tile on its own counter (published at the end)
-        int32_t sctr = -1;
-        if (!(rt.t.flags & TF_TRSM3) && cx.opt.early_sig) {
+        int32_t sctr = -1, wctr = -1;
+        const bool is_step = (rt.t.flags & TF_CHAINSTEP) != 0;
+        if (is_step) {
+          // chain step: sigs[0] (own) at the end -- it guards the next diagonal tile --
+          // sigs[1] = W (early), sigs[2] = the sub-diagonal tile (mid-task)
+          rt.t.flags |= TF_EARLY_SIG;
+          wctr = cx.new_ctr();
+          sctr = cx.new_ctr();
+          rt.sigs.insert(rt.sigs.begin(), sctr);
+          rt.sigs.insert(rt.sigs.begin(), wctr);
+        } else if (!(rt.t.flags & TF_TRSM3) && cx.opt.early_sig) {
           rt.t.flags |= TF_EARLY_SIG;
           if (rt.t.flags & TF_TRSM2) {
             sctr = cx.new_ctr();
             rt.sigs.push_back(sctr);
           }
         }
-        int id = cx.emit(std::move(rt));
+        step_sctr = sctr;
+        int id = cx.emit(std::move(rt));  // emit puts the own counter first: [own, wctr, sctr, ...]
         if (sctr >= 0) Lctr[key4(rts[0].Y, rts[0].q, X, c)] = sctr;
+        if (wctr >= 0) Lctr[key4(X, c, X, c)] = wctr;
+        if (is_step) {
+          last_chain_ts[P.q1(X)] = id;
+          stE->pending.clear();
+          stE->last = id;
+          stE->written = true;
+          Lprod[key4(rts[0].Y, rts[0].q, X, c)] = id;
+          stD->pending.clear();
+          stD->last = id;
+          stD->written = true;
+        }
+        (void)step_sctr;
         st.pending.clear();
         st.last = id;
         st.written = true;
@@ -499,7 +551,7 @@ struct Builder {
           Lprod[key4(rts[1].Y, rts[1].q, X, c)] = id;
         }
       }
-      uint64_t fused_diag = ~0ull;  // next diagonal tile whose column-(X,c) update is fused below
+      uint64_t fused_diag = step_dk;  // next diagonal tile whose column-(X,c) update is fused (step or chain TRSM)
       for (size_t ri = first_trsm; ri < rts.size(); ++ri) {  // TRSM = (A - last update) W(c,c)^T
         const RT &r = rts[ri];
         const BlkRef &tb = (r.Y == X) ? d : B(r.Y, X);
@@ -545,13 +597,13 @@ struct Builder {
             rt.t.flags = TF_SYRK3;
             rt.t.out3 = tileloc(bd.base, r.q, r.q);
             rt.t.m3 = r.h;
-            rt.late.push_back(cx.ctr_of(Lprod.at(key4(X, c, X, c))));
+            rt.late.push_back(lwait(key4(X, c, X, c)));
             if (sd.last >= 0) rt.late.push_back(cx.ctr_of(sd.last));
             sdp = &sd;
             fused_diag = dk;
           }
         }
-        if (!sdp) rt.waits.push_back(cx.ctr_of(Lprod.at(key4(X, c, X, c))));
+        if (!sdp) rt.waits.push_back(lwait(key4(X, c, X, c)));  // W(c,c)
         rt.t.flags |= TF_POST | TF_POST_T;
         rt.t.r = tileloc(P.W[X], c, c);
         if (r.Y == X) {
@@ -567,7 +619,7 @@ struct Builder {
           else if (cx.opt.split_chain && first_trsm == 0 && ri == 0) rt.queue = P.q2(X);
           else if (cx.opt.split_chain && first_trsm == 0 && ri == 1 && cx.opt.rts1_chain) rt.queue = P.q2(X);
           else if (cx.opt.split_chain && first_trsm == 0 && ri == 1 && cx.opt.urgent_ctas > 0) rt.queue = URGENT_QUEUE;
-          else if (ri == first_trsm && first_trsm == 1) rt.queue = P.q1(X);
+          else if (ri == first_trsm && first_trsm == 1 && cx.opt.fuse_trsm) rt.queue = P.q1(X);
         }
         const bool is_carry = (rt.t.flags & TF_CARRY) != 0;
         const int rq = rt.queue;
@@ -1779,6 +1831,7 @@ void BuildOptions::apply_env() {
       else if (k == "early_sig") early_sig = v != 0;
       else if (k == "carry_chain") carry_chain = v != 0;
       else if (k == "carry_min_b") carry_min_b = (int)v;
+      else if (k == "chain_step") chain_step = v != 0;
     }
     i = j + 1;
   }

@@ -106,7 +106,9 @@ struct BuildOptions {
   bool chol8 = true;
   bool early_sig = true;
   bool carry_chain = true;      // chain TRSM+SYRK on the POTRF's CTA, operands carried in shared memory
-  int carry_min_b = 2048;       // ... for nodes of at least this size        // POTRF publishes W before its log-det partial and L (TF_EARLY_SIG)            // POTRF tasks: 8 x 8-block warp-pipelined Cholesky (else 16 x 16 leaves)
+  int carry_min_b = 2048;       // ... for nodes of at least this size
+  bool chain_step = false;      // POTRF + sub-diagonal TRSM + next-tile SYRK as ONE carried task (all sizes;
+                                // measured slower: E's last update becomes a bulk round trip on the chain)        // POTRF publishes W before its log-det partial and L (TF_EARLY_SIG)            // POTRF tasks: 8 x 8-block warp-pipelined Cholesky (else 16 x 16 leaves)
   int wide_min_wave = 512;      // 128 x 64 tasks for inversion waves of >= this many tiles (0: never)
   int twist_max_b = 1024;       // ... and b <= twist_max_b (larger blocks: the one-sided chain hides under the work)
   // overrides from the environment (SERINV_OPT="key=value,..."), for tuning runs

@@ -48,6 +48,8 @@ enum TaskFlags : uint16_t {
   TF_EARLY_SIG = 1024,  // TK_POTRF (+TF_W_OUT, no TF_TRSM2): own counter signalled once W is stored
   TF_CARRY = 2048,    // carried chain (same CTA, consecutive tasks): TK_POTRF reads its tile from smem St;
                       // TK_GEMM (+TF_POST|TF_SYRK3) reads W from smem Wt and leaves the SYRK result in St
+  TF_CHAINSTEP = 4096,  // TK_POTRF: then E W^T for the sub-diagonal tile out3 (sigs[1] after its store) and
+                        // the next diagonal tile out4 -= (E W^T)(E W^T)^T, left in St (carry); late inputs
 };
 
 // Buffer ids (kernel argument `bufs[]`, offsets in doubles).

@@ -151,7 +151,7 @@ def test_selinv_host_streaming(n, b, a):
 
 
 @pytest.mark.parametrize("opt", ["carry_min_b=64", "carry_min_b=64,twist_min_n=0", "chol8=0", "early_sig=0",
-                                 "wide_min_wave=1", "fuse_trsm=1,split_chain=0"])
+                                 "wide_min_wave=1", "fuse_trsm=1,split_chain=0", "chain_step=1"])
 def test_scheduling_variants_parity(opt, monkeypatch):
     """Graph-build options (SERINV_OPT, read when a handle builds a graph) change the
     task structure -- carried chain, one-sided order, 16x16-leaf POTRF, late

@@ -183,6 +183,23 @@ int run(const Graph &g, Ctx &c) {
             for (int j = 0; j < T.m3; ++j) z[(int64_t)i * T.out.ld + j] = 0.0;
         }
       }
+      if (T.type == TK_POTRF && (T.flags & TF_CHAINSTEP)) {
+        // E <- E W^T (no update segments: E's updates were bulk tasks), zero the mirror
+        // tile, then the next diagonal tile out4 -= E E^T
+        trsm_tile(0, 0, T.out3, T.m3, 1.0);
+        if (T.zmask & 1) {
+          double *z = ptr(c, T.out) + SERINV_TILE;
+          for (int i = 0; i < m; ++i)
+            for (int j = 0; j < T.m3; ++j) z[(int64_t)i * T.out.ld + j] = 0.0;
+        }
+        double *o4 = ptr(c, T.out4);
+        for (int i = 0; i < T.m4; ++i)
+          for (int j = 0; j < T.m4; ++j) {
+            double s = 0;
+            for (int k = 0; k < m; ++k) s += get(c, T.out3, i, k) * get(c, T.out3, j, k);
+            o4[(int64_t)i * T.out4.ld + j] -= s;
+          }
+      }
       if (T.type == TK_POTRF && (T.flags & TF_TRSM3)) {
         trsm_tile(T.nseg2, T.nseg, T.out4, T.m4, T.beta4);
         if (T.zmask & 2) {
