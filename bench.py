@@ -13,6 +13,9 @@ device-timed with CUDA events; fraction of the measured FP64 DMMA peak.
 
 --impl reference times the CPU oracle (oracle/, numpy/scipy FP64) on a bounded
 sample of the same workload (the paper's code does not exist).
+--impl library times the paper's own GPU design on the same B200 and input: one
+cuSOLVER / cuBLAS call per block operation (tools/library_arm.py, SURVEY §8(f) f4);
+a bench-only comparator, N = 1.
 """
 from __future__ import annotations
 
@@ -78,11 +81,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference", "library"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--r", type=float, default=1.0,
                     help="N > 1: blocks of the first / last rank relative to a middle rank (serinv_plan_ends)")
+    ap.add_argument("--q", default="auto",
+                    help="N > 1: sub-partitions per rank (serinv_ppobtaf_q); 'auto' = serinv_dist_auto_q")
     ap.add_argument("--partitions", default="auto",
                     help="N = 1: intra-GPU partitions, e.g. 1 (sequential), 8, 256x16 (nested); "
                          "'auto' = the library's plan (serinv_auto_partitions)")
@@ -163,14 +168,12 @@ def reference_arm(args, cfg):
         return 0
     n, b, a = cfg["n"], cfg["b"], cfg["a"]
     times = []
-    tf = None
     nprime = None
     cores = len(os.sched_getaffinity(0))
     for it in range(args.warmup + args.steps):
-        rate, dt, nprime, cores = cpu_oracle_rate(cfg, budget_s=8.0)
+        _, dt, nprime, cores = cpu_oracle_rate(cfg, budget_s=8.0)
         if it >= args.warmup:
             times.append(dt)
-            tf = rate if tf is None else min(tf, rate) if False else rate
     fl = flops_pobtaf(nprime, b, a) + flops_pobtasi(nprime, b, a)
     med = statistics.median(times)
     value = fl / med / 1e12
@@ -188,12 +191,82 @@ def reference_arm(args, cfg):
     return 0
 
 
+def library_arm(args, cfg):
+    """The paper's per-block cuSOLVER/cuBLAS design on this B200, same input,
+    same timing rules as our arm; reports its max block error against our library."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+    import btagen
+    import paper_2503_17528_b200 as sb
+    from tools import library_arm as la
+    n, b, a = cfg["n"], cfg["b"], cfg["a"]
+    torch.cuda.set_device(0)
+    fl = flops_pobtaf(n, b, a) + flops_pobtasi(n, b, a)
+    pristine = btagen.g1_torch(0, n, b, a, device="cuda:0")
+    work = {k: v.clone() for k, v in pristine.items()}
+
+    def restore():
+        for k in work:
+            work[k].copy_(pristine[k])
+
+    def step():
+        ld = la.pobtaf(work)
+        la.pobtasi(work)
+        return ld
+
+    for _ in range(args.warmup):
+        restore()
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    times = []
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            restore()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ld_lib = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    sec = statistics.median(times)
+    # agreement with our library on the same input (relative Frobenius, per sampled block)
+    ours = {k: v.clone() for k, v in pristine.items()}
+    ld_ours = sb.selinv(ours["diag"], ours["lower"], ours["arrow"], ours["tip"])
+    errs = []
+    for k, idx in (("diag", [0, n // 2, n - 1]), ("lower", [0, (n - 1) // 2, n - 2]), ("arrow", [0, n - 1]),
+                   ("tip", [None])):
+        for i in idx:
+            if (k == "lower" and n < 2) or (k in ("arrow", "tip") and a == 0):
+                continue
+            x, y = (work[k], ours[k]) if i is None else (work[k][i], ours[k][i])
+            errs.append(float(torch.linalg.norm(x - y) / torch.linalg.norm(y)))
+    line = {
+        "impl": "library", "metric": METRIC, "value": round(fl / sec / 1e12, 4), "unit": "TFLOP/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": bench_config(args.config, cfg),
+        "design": "per-block cusolverDnDpotrf / cublasDtrsm / cublasDgemm via torch.linalg (paper P:646-650)",
+        "fraction_of_fp64_peak": round(fl / sec / 1e12 / FP64_PEAK_TFLOPS, 4),
+        "max_rel_block_err_vs_ours": max(errs), "logdet_diff_vs_ours": abs(float(ld_lib) - float(ld_ours)),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # --------------------------------------------------------------------------- our arm
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return reference_arm(args, cfg)
+    if args.impl == "library":
+        return library_arm(args, cfg)
     import torch
     import torch.distributed as dist
     import btagen
@@ -236,11 +309,14 @@ def main():
         # take r x a middle rank's blocks (flop/chain balance)
         parts = sb.plan_ends(n, world, args.r)
         s, e = parts[rank]
+        # sub-partitions per rank (intra-GPU partitioning of each rank's chain), the
+        # same on every rank: the library's default for the smallest rank
+        Q = (sd.dist_auto_q(min(e_ - s_ for s_, e_ in parts), b) if args.q == "auto" else int(args.q))
         pristine = btagen.g1_torch(0, n, b, a, device=f"cuda:{local}", start=s, end=e)
         if pristine["lower"].shape[0] == 0:
             pristine["lower"] = torch.zeros((1, b, b), dtype=torch.float64, device=f"cuda:{local}")
         work = {k: v.clone() for k, v in pristine.items()}
-        ctx = sd.DistContext(h, world, rank, n, s, e - s, b, a, device=local)
+        ctx = sd.DistContext(h, world, rank, n, s, e - s, b, a, device=local, Q=Q)
 
         def step(info=None, logdet=None):
             return sd.pselinv_step(ctx, work, check=False)
@@ -330,7 +406,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": bench_config(args.config, cfg),
-            "plan": {"n_global": n, "parallelism": f"partitions{world}" if world > 1 else
+            "plan": {"n_global": n, "parallelism": f"partitions{world}x{Q}" if world > 1 else
                      ("single" if Ps == [1] else "intra-GPU partitions " + "x".join(map(str, Ps))),
                      "step": ("POBTAF+POBTASI (serinv_selinv)" if Ps == [1] else
                               "PPOBTAF+POBTARSSI+PPOBTASI in one launch (serinv_pselinv_nested)")

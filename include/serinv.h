@@ -230,6 +230,38 @@ int serinv_ppobtasi(serinv_handle_t h, const serinv_part_t *part, const serinv_b
                     void *d_ws, size_t ws_bytes, const void *d_recvbuf, int *d_info,
                     double *d_logdet, void *stream);
 
+/*
+ * Hierarchical variant: intra-GPU partitioning of each rank's blocks (SURVEY
+ * §8(f) f1 applied per rank; nested solving of the reduced system, PAPER.md
+ * Sec. 4.2).  Rank p splits its blocks [start, start+count) into Q
+ * consecutive sub-partitions (even sizes, remainder to the earliest; each needs
+ * >= 2 blocks, count >= 2Q), so the whole matrix has P*Q partitions, rank p
+ * owning partitions [pQ, (p+1)Q).  Q must be the same on every rank.
+ *   serinv_ppobtaf_q   factors the Q sub-partitions (one launch) and packs Q
+ *                      exchange records (Q * serinv_exchange_bytes bytes in
+ *                      d_sendbuf; the rank's partial log det in the first).
+ *   (caller)           all-gather of the P send buffers (rank order) into
+ *                      d_recvbuf: P * Q records in global partition order.
+ *   serinv_ppobtasi_q  assembles the reduced system (2PQ-2 blocks with the
+ *                      twisted last partition, reading R14), solves it
+ *                      redundantly -- by the nested partitioned algorithm when
+ *                      long (serinv_auto_partitions), else as one chain --
+ *                      then the backward pass of the Q sub-partitions.
+ * Q = 1 is exactly serinv_ppobtaf / serinv_ppobtasi.  Errors as above, plus
+ * SERINV_ERR_PLAN if Q < 1 or count < 2Q (Q > 1).  d_ws from
+ * serinv_ppobtaf_q_ws(part, Q, ...), passed unchanged between the two calls.
+ * serinv_dist_auto_q: the library's default Q for a rank of `count` blocks of
+ * size b (the first level of serinv_auto_partitions(count, b)); >= 1, or a
+ * negative status.
+ */
+int serinv_ppobtaf_q_ws(const serinv_part_t *part, int Q, int64_t b, int64_t a, size_t *bytes);
+int serinv_ppobtaf_q(serinv_handle_t h, const serinv_part_t *part, int Q, const serinv_bta_t *A_local,
+                     void *d_ws, size_t ws_bytes, void *d_sendbuf, int *d_info, void *stream);
+int serinv_ppobtasi_q(serinv_handle_t h, const serinv_part_t *part, int Q, const serinv_bta_t *L_local,
+                      void *d_ws, size_t ws_bytes, const void *d_recvbuf, int *d_info,
+                      double *d_logdet, void *stream);
+int serinv_dist_auto_q(int64_t count, int64_t b);
+
 /* ------------------------------------------------------------------------- */
 /* Introspection (tests / bench).                                            */
 /* ------------------------------------------------------------------------- */

@@ -69,6 +69,12 @@ def lib():
                                  c_p, c_p, c_p]
     L.serinv_ppobtasi.argtypes = [c_p, ctypes.POINTER(Part), ctypes.POINTER(BTA), c_p, ctypes.c_size_t,
                                   c_p, c_p, c_p, c_p]
+    L.serinv_ppobtaf_q_ws.argtypes = [ctypes.POINTER(Part), ctypes.c_int, c_i64, c_i64, sz]
+    L.serinv_ppobtaf_q.argtypes = [c_p, ctypes.POINTER(Part), ctypes.c_int, ctypes.POINTER(BTA), c_p,
+                                   ctypes.c_size_t, c_p, c_p, c_p]
+    L.serinv_ppobtasi_q.argtypes = [c_p, ctypes.POINTER(Part), ctypes.c_int, ctypes.POINTER(BTA), c_p,
+                                    ctypes.c_size_t, c_p, c_p, c_p, c_p]
+    L.serinv_dist_auto_q.argtypes = [c_i64, c_i64]
     L.serinv_graph_stats.argtypes = [c_p, ctypes.c_int, c_i64, c_i64, c_i64, ctypes.c_int,
                                      ctypes.c_double, ctypes.POINTER(GraphStats)]
     L.serinv_selinv_host.argtypes = [c_p, ctypes.POINTER(BTA), ctypes.POINTER(BTA), ctypes.POINTER(BTA), c_p,
@@ -87,4 +93,5 @@ EXPORTED = [
     "serinv_pselinv_ws", "serinv_pselinv", "serinv_exchange_bytes", "serinv_ppobtaf_ws",
     "serinv_ppobtaf", "serinv_ppobtasi", "serinv_graph_stats", "serinv_last_launches", "serinv_set_trace", "serinv_selinv_host", "serinv_bench_gemm",
     "serinv_auto_partitions", "serinv_pselinv_nested_ws", "serinv_pselinv_nested", "serinv_graph_stats_nested",
+    "serinv_ppobtaf_q_ws", "serinv_ppobtaf_q", "serinv_ppobtasi_q", "serinv_dist_auto_q",
 ]

@@ -2011,32 +2011,68 @@ std::vector<int> auto_partitions(int64_t n, int64_t b) {
   return Ps;
 }
 
-// Distributed per-rank graphs.  Phase 0 (ppobtaf): factor the local partition
-// and pack the exchange record into EXT0.  Phase 1 (ppobtasi): assemble A_r
-// from the all-gathered records in EXT1 (rank order, identical on every rank),
-// POBTARSSI redundantly, scatter this rank's X_r blocks, backward pass.  Both
-// phases lay the workspace out identically (phase 1 replays the factor-phase
-// allocations), so the fill-in factor blocks B_i survive between the calls.
+// Split a rank's blocks [start, start+count) into Q consecutive sub-partitions
+// (even sizes, remainder to the earliest).  Every sub-partition needs >= 2
+// blocks except a global first one (>= 1).  Returns false if infeasible.
+bool split_rank(int64_t start, int64_t count, int Q, std::vector<int64_t> &sub) {
+  if (Q < 1 || count < 1) return false;
+  sub.assign(Q + 1, start);
+  int64_t base = count / Q, rem = count % Q;
+  for (int q = 0; q < Q; ++q) sub[q + 1] = sub[q] + base + (q < rem ? 1 : 0);
+  for (int q = 0; q < Q; ++q) {
+    int64_t c = sub[q + 1] - sub[q];
+    if (c < 1 || (c < 2 && !(start == 0 && q == 0) && Q > 1)) return false;
+  }
+  return true;
+}
+
+// Distributed per-rank graphs.  Rank `rank` of P owns the global blocks
+// [start, start+count), split into Q sub-partitions (intra-GPU partitioning of
+// the rank's chain; Q = 1 is the paper's one partition per process).  Globally
+// there are P*Q partitions, rank p owning partitions [pQ, (p+1)Q).
+// Phase 0 (ppobtaf): factor the Q local partitions and pack their Q exchange
+// records into EXT0.  Phase 1 (ppobtasi): assemble A_r (2PQ-1 blocks, 2PQ-2
+// with the twisted last partition) from the all-gathered records in EXT1
+// (global order, identical on every rank), solve it redundantly -- nested
+// (Sec. 4.2) when it is long, else as one chain (POBTARSSI) -- scatter this
+// rank's X_r blocks, backward pass.  Both phases lay the workspace out
+// identically (phase 1 replays the factor-phase allocations), so the fill-in
+// factor blocks B_i survive between the calls.
 Graph build_distributed(int phase, int P, int rank, int64_t n, int64_t start, int64_t count, int64_t b, int64_t a,
-                        const BuildOptions &opt) {
+                        const BuildOptions &opt, int Q) {
+  std::vector<int64_t> sub;
+  if (!split_rank(start, count, Q, sub)) {
+    Graph bad;
+    bad.error = "infeasible rank split";
+    return bad;
+  }
+  const int PQ = P * Q;
+  const bool tw = opt.twist_last && PQ >= 2;
+  const int nr = reduced_size(PQ, tw);
+  std::vector<int> Ps2 = Q > 1 ? auto_partitions(nr, b) : std::vector<int>{1};
   Ctx cx;
   cx.opt = opt;
-  cx.slot_cap = slot_bound(count + 2 * P + 2, b, a);
+  cx.slot_cap = slot_bound(count + 4 * PQ + 8, b, a);
   cx.slot_region = cx.alloc(cx.slot_cap);
   int64_t recsz = exchange_doubles(b, a);
   XRec x{b, a};
-  PartState ps;
-  ps.p = rank;
-  ps.s = start;
-  ps.e = start + count;
-  ps.ls = 0;
-  ps.V = top_view(n, b, a);  // local storage (block `start` at index ls = 0), global rows
-  const bool tw = opt.twist_last && P >= 2;
-  ps.bottom = tw && rank == P - 1;
-  ppobtaf_part(cx, ps, b, a);
+  std::vector<PartState> parts(Q);
+  const bool crit = 2 * Q <= cx.opt.max_crit;
+  for (int q = 0; q < Q; ++q) {
+    PartState &ps = parts[q];
+    ps.p = rank * Q + q;
+    ps.s = sub[q];
+    ps.e = sub[q + 1];
+    ps.ls = sub[q] - start;
+    ps.queue = Q == 1 ? 1 : (crit ? 2 * q + 1 : 0);
+    ps.V = top_view(n, b, a);  // local storage (block `start` at index 0), global rows
+    ps.bottom = tw && ps.p == PQ - 1;
+    ppobtaf_part(cx, ps, b, a);
+  }
   if (phase == 0) {
     int32_t packed = cx.new_ctr();
-    pack_part(cx, ps, P, b, a, BUF_EXT0, 0, packed);
+    for (int q = 0; q < Q; ++q) pack_part(cx, parts[q], PQ, b, a, BUF_EXT0, q * recsz, packed);
+    // the rank's partial log det travels in its first record
     cx.logdet(Loc{BUF_EXT0, 0, x.ld()}, 0, cx.slot_count, Loc{BUF_WS, 0, 0}, 0, 0, {});
     return cx.finalize();
   }
@@ -2045,34 +2081,43 @@ Graph build_distributed(int phase, int P, int rank, int64_t n, int64_t start, in
   cx.own.clear();
   cx.potrf_ctrs.clear();
   cx.xrc.clear();
-  Builder &PB = *ps.bld;
-  PB.factordone.clear();
-  PB.Lprod.clear();
-  PB.tstate.clear();
-  PB.input_waits.clear();
-  PB.wdiag_task.clear();
-  ps.done.clear();
+  for (auto &ps : parts) {
+    Builder &PB = *ps.bld;
+    PB.factordone.clear();
+    PB.Lprod.clear();
+    PB.tstate.clear();
+    PB.input_waits.clear();
+    PB.wdiag_task.clear();
+    ps.done.clear();
+  }
   int64_t part_slots = cx.slot_count;
-  std::vector<int64_t> st(P + 1, -1);
-  st[rank] = start;
-  st[rank + 1] = start + count;
+  // partition starts known to this rank (other ranks' inner starts only label info rows)
+  std::vector<int64_t> st(PQ + 1, -1);
+  for (int q = 0; q <= Q; ++q) st[rank * Q + q] = sub[q];
   st[0] = 0;
-  st[P] = n;
+  st[PQ] = n;
   Reduced R;
-  reduced_from_records(cx, ps.V, P, b, a, BUF_EXT1, 0, recsz, st, {}, R, tw);
-  scatter_xr(cx, ps, P, b, a, R);
-  ppobtasi_part(cx, ps, b, false);  // W tiles recomputed by TRTRI (no fused POTRF here)
+  assemble_reduced(cx, parts[0].V, PQ, b, a, BUF_EXT1, 0, recsz, st, {}, R, tw);
+  std::vector<int> lv{0};
+  lv.insert(lv.end(), Ps2.begin(), Ps2.end());
+  bool nested = Ps2[0] > 1 && psolve_level(cx, R.V, nr, b, a, lv, 1, 1.0, R.ready);
+  if (!nested) solve_reduced_chain(cx, b, a, nr, R);
+  for (auto &ps : parts) {
+    scatter_xr(cx, ps, PQ, b, a, R);
+    ppobtasi_part(cx, ps, b, false);  // W tiles recomputed by TRTRI (no fused POTRF here)
+  }
   // log det = sum of the ranks' partials (rank order) + 2 sum log diag of POBTAF(A_r)
-  cx.logdet(Loc{BUF_LOGDET, 0, 0}, part_slots, cx.slot_count - part_slots, Loc{BUF_EXT1, 0, x.ld()}, P, recsz, {});
+  cx.logdet(Loc{BUF_LOGDET, 0, 0}, part_slots, cx.slot_count - part_slots, Loc{BUF_EXT1, 0, x.ld()}, P, Q * recsz,
+            {});
   return cx.finalize();
 }
 
-int64_t distributed_ws_bytes(int P, int rank, int64_t n, int64_t start, int64_t count, int64_t b, int64_t a) {
+int64_t distributed_ws_bytes(int P, int rank, int64_t n, int64_t start, int64_t count, int64_t b, int64_t a, int Q) {
   BuildOptions opt;
   opt.apply_env();
   opt.schedule = false;
-  Graph g0 = build_distributed(0, P, rank, n, start, count, b, a, opt);
-  Graph g1 = build_distributed(1, P, rank, n, start, count, b, a, opt);
+  Graph g0 = build_distributed(0, P, rank, n, start, count, b, a, opt, Q);
+  Graph g1 = build_distributed(1, P, rank, n, start, count, b, a, opt, Q);
   if (!g0.error.empty() || !g1.error.empty()) return -1;
   return std::max(g0.ws_doubles, g1.ws_doubles) * 8;
 }

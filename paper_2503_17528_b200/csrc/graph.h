@@ -134,10 +134,11 @@ std::vector<int> auto_partitions(int64_t n, int64_t b);
 
 // Distributed per-rank graphs.  phase 0 = ppobtaf (+ pack into EXT0 send buffer),
 // phase 1 = ppobtasi (assemble from EXT1 recv buffer, POBTARSSI, backward).
+// Q = sub-partitions per rank (intra-GPU partitioning of the rank's blocks).
 Graph build_distributed(int phase, int P, int rank, int64_t n_global, int64_t start,
-                        int64_t count, int64_t b, int64_t a, const BuildOptions &opt);
+                        int64_t count, int64_t b, int64_t a, const BuildOptions &opt, int Q = 1);
 int64_t distributed_ws_bytes(int P, int rank, int64_t n_global, int64_t start, int64_t count,
-                             int64_t b, int64_t a);
+                             int64_t b, int64_t a, int Q = 1);
 int64_t exchange_doubles(int64_t b, int64_t a);
 
 // Diagnostic: independent tile GEMMs (engine throughput).

@@ -151,7 +151,8 @@ int get_graph_impl(serinv_handle_t h, const GKey &key, DevGraph **out) {
     int rank = std::get<6>(key);
     int64_t start = std::get<7>(key), count = std::get<8>(key);
     if (kind != 4 && kind != 5) return SERINV_ERR_SHAPE;
-    dg->g = build_distributed(kind - 4, P, rank, n, start, count, b, a, opt);
+    int Q = (int)std::max<int64_t>(1, std::get<5>(key));
+    dg->g = build_distributed(kind - 4, P, rank, n, start, count, b, a, opt, Q);
   }
   if (!dg->g.error.empty()) {
     fprintf(stderr, "serinv: graph build failed: %s\n", dg->g.error.c_str());
@@ -464,36 +465,51 @@ int serinv_exchange_bytes(int64_t b, int64_t a, size_t *bytes) {
   return SERINV_OK;
 }
 
-static int check_part(const serinv_part_t *pt) {
+static int check_part(const serinv_part_t *pt, int Q = 1) {
   if (!pt) return -1;
+  if (Q < 1 || Q > 65536) return SERINV_ERR_PLAN;
   if (pt->P < 1 || pt->rank < 0 || pt->rank >= pt->P || pt->count < 1 || pt->start < 0 ||
       pt->start + pt->count > pt->n_global)
     return SERINV_ERR_PLAN;
   if (pt->P > 1 && pt->rank > 0 && pt->count < 2) return SERINV_ERR_PLAN;
+  if (Q > 1 && pt->count < 2 * (int64_t)Q) return SERINV_ERR_PLAN;
   return SERINV_OK;
 }
 
-int serinv_ppobtaf_ws(const serinv_part_t *part, int64_t b, int64_t a, size_t *bytes) {
-  int rc = check_part(part);
+int serinv_ppobtaf_q_ws(const serinv_part_t *part, int Q, int64_t b, int64_t a, size_t *bytes) {
+  int rc = check_part(part, Q);
   if (rc) return rc;
-  if (!bytes) return -4;
+  if (!bytes) return -5;
   if (b < 1 || a < 0) return SERINV_ERR_SHAPE;
-  auto key = std::make_tuple(4, part->n_global, b, a, part->P, (int64_t)0, part->rank, part->start, part->count);
+  auto key = std::make_tuple(4, part->n_global, b, a, part->P, (int64_t)Q, part->rank, part->start, part->count);
   std::lock_guard<std::mutex> lk(g_ws_mu);
   auto it = g_ws_cache.find(key);
   int64_t v = it != g_ws_cache.end()
                   ? it->second
                   : (g_ws_cache[key] = distributed_ws_bytes(part->P, part->rank, part->n_global, part->start,
-                                                            part->count, b, a));
+                                                            part->count, b, a, Q));
   if (v < 0) return SERINV_ERR_SHAPE;
   *bytes = (size_t)v;
   return SERINV_OK;
 }
 
-static int run_dist(serinv_handle_t h, int phase, const serinv_part_t *part, const serinv_bta_t *A, void *d_ws,
-                    size_t ws_bytes, void *ext0, const void *ext1, int *d_info, double *d_logdet, void *stream) {
+int serinv_ppobtaf_ws(const serinv_part_t *part, int64_t b, int64_t a, size_t *bytes) {
+  return serinv_ppobtaf_q_ws(part, 1, b, a, bytes);
+}
+
+int serinv_dist_auto_q(int64_t count, int64_t b) {
+  if (count < 1 || b < 1) return SERINV_ERR_SHAPE;
+  std::vector<int> v = auto_partitions(count, b);
+  int Q = v.empty() ? 1 : v[0];
+  while (Q > 1 && count < 2 * (int64_t)Q) --Q;
+  return Q;
+}
+
+static int run_dist(serinv_handle_t h, int phase, const serinv_part_t *part, int Q, const serinv_bta_t *A,
+                    void *d_ws, size_t ws_bytes, void *ext0, const void *ext1, int *d_info, double *d_logdet,
+                    void *stream) {
   if (!h) return SERINV_ERR_HANDLE;
-  int rc = check_part(part);
+  int rc = check_part(part, Q);
   if (rc) return rc;
   if (!A || !A->diag || A->b < 1 || A->a < 0) return -3;
   if (A->n != part->count) return -3;
@@ -503,7 +519,8 @@ static int run_dist(serinv_handle_t h, int phase, const serinv_part_t *part, con
   if (!d_info) return -8;
   if (cudaSetDevice(h->device) != cudaSuccess) return SERINV_ERR_CUDA;
   DevGraph *dg = nullptr;
-  rc = get_graph(h, GKey(4 + phase, part->n_global, A->b, A->a, part->P, 0, part->rank, part->start, part->count),
+  rc = get_graph(h, GKey(4 + phase, part->n_global, A->b, A->a, part->P, (int64_t)Q, part->rank, part->start,
+                        part->count),
                  &dg);
   if (rc) return rc;
   if ((int64_t)ws_bytes < dg->g.ws_doubles * 8) return SERINV_ERR_WS;
@@ -512,16 +529,28 @@ static int run_dist(serinv_handle_t h, int phase, const serinv_part_t *part, con
   return launch(h, *dg, bufs, d_info, (cudaStream_t)stream);
 }
 
+int serinv_ppobtaf_q(serinv_handle_t h, const serinv_part_t *part, int Q, const serinv_bta_t *A_local, void *d_ws,
+                     size_t ws_bytes, void *d_sendbuf, int *d_info, void *stream) {
+  if (!d_sendbuf) return -7;
+  return run_dist(h, 0, part, Q, A_local, d_ws, ws_bytes, d_sendbuf, nullptr, d_info, nullptr, stream);
+}
+
+int serinv_ppobtasi_q(serinv_handle_t h, const serinv_part_t *part, int Q, const serinv_bta_t *L_local, void *d_ws,
+                      size_t ws_bytes, const void *d_recvbuf, int *d_info, double *d_logdet, void *stream) {
+  if (!d_recvbuf) return -7;
+  return run_dist(h, 1, part, Q, L_local, d_ws, ws_bytes, nullptr, d_recvbuf, d_info, d_logdet, stream);
+}
+
 int serinv_ppobtaf(serinv_handle_t h, const serinv_part_t *part, const serinv_bta_t *A_local, void *d_ws,
                    size_t ws_bytes, void *d_sendbuf, int *d_info, void *stream) {
   if (!d_sendbuf) return -6;
-  return run_dist(h, 0, part, A_local, d_ws, ws_bytes, d_sendbuf, nullptr, d_info, nullptr, stream);
+  return run_dist(h, 0, part, 1, A_local, d_ws, ws_bytes, d_sendbuf, nullptr, d_info, nullptr, stream);
 }
 
 int serinv_ppobtasi(serinv_handle_t h, const serinv_part_t *part, const serinv_bta_t *L_local, void *d_ws,
                     size_t ws_bytes, const void *d_recvbuf, int *d_info, double *d_logdet, void *stream) {
   if (!d_recvbuf) return -6;
-  return run_dist(h, 1, part, L_local, d_ws, ws_bytes, nullptr, d_recvbuf, d_info, d_logdet, stream);
+  return run_dist(h, 1, part, 1, L_local, d_ws, ws_bytes, nullptr, d_recvbuf, d_info, d_logdet, stream);
 }
 
 int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_t a, int P, double r,

@@ -13,6 +13,11 @@ replicated tip).  One step:
                      solves it redundantly (bit-identical on all ranks), scatters
                      its true-inverse boundary blocks and runs its backward pass
 
+With Q > 1 every rank splits its blocks into Q sub-partitions (serinv_ppobtaf_q /
+serinv_ppobtasi_q: intra-GPU partitioning of the rank's chain, the reduced
+system of 2PQ-2 blocks solved by the nested algorithm); Q = dist_auto_q(count, b)
+is the library's default, Q = 1 the paper's one partition per process.
+
 Argument marshalling + the collective only; all arithmetic is in libserinv.
 """
 from __future__ import annotations
@@ -46,29 +51,39 @@ def exchange(send, recv, group=None):
     dist.all_gather_into_tensor(recv, send, group=group)
 
 
+def dist_auto_q(count: int, b: int) -> int:
+    """The library's default sub-partitions per rank (serinv_dist_auto_q)."""
+    q = _lib.lib().serinv_dist_auto_q(count, b)
+    if q < 1:
+        raise RuntimeError(f"serinv_dist_auto_q failed: {q}")
+    return q
+
+
 class DistContext:
     """Per-rank state of the distributed routines (buffers persist between
-    ppobtaf and ppobtasi: the workspace keeps the fill-in factor blocks B_i)."""
+    ppobtaf and ppobtasi: the workspace keeps the fill-in factor blocks B_i).
+    Q = sub-partitions of this rank's blocks (the same on every rank)."""
 
     def __init__(self, handle, P: int, rank: int, n_global: int, start: int, count: int, b: int, a: int,
-                 device: int = 0, group=None):
+                 device: int = 0, group=None, Q: int = 1):
         import torch
         L = _lib.lib()
         self.h = handle
         self.part = Part(P, rank, n_global, start, count)
         self.b, self.a = b, a
+        self.Q = int(Q)
         self.group = group
         nb = ctypes.c_size_t(0)
-        rc = L.serinv_ppobtaf_ws(ctypes.byref(self.part), b, a, ctypes.byref(nb))
+        rc = L.serinv_ppobtaf_q_ws(ctypes.byref(self.part), self.Q, b, a, ctypes.byref(nb))
         if rc:
-            raise RuntimeError(f"serinv_ppobtaf_ws failed: {rc}")
+            raise RuntimeError(f"serinv_ppobtaf_q_ws failed: {rc}")
         dev = f"cuda:{device}"
         self.ws = torch.empty(max(nb.value, 256), dtype=torch.uint8, device=dev)
         xb = ctypes.c_size_t(0)
         L.serinv_exchange_bytes(b, a, ctypes.byref(xb))
         self.rec_doubles = xb.value // 8
-        self.send = torch.zeros(self.rec_doubles, dtype=torch.float64, device=dev)
-        self.recv = torch.zeros(P * self.rec_doubles, dtype=torch.float64, device=dev)
+        self.send = torch.zeros(self.Q * self.rec_doubles, dtype=torch.float64, device=dev)
+        self.recv = torch.zeros(P * self.Q * self.rec_doubles, dtype=torch.float64, device=dev)
         self.info = torch.zeros(1, dtype=torch.int32, device=dev)
         self.logdet = torch.zeros(1, dtype=torch.float64, device=dev)
 
@@ -88,8 +103,8 @@ def _stream():
 def ppobtaf(ctx: DistContext, D):
     """PARTIAL_/PERMUTED_POBTAF on the local blocks + pack of the exchange record."""
     A = _bta_local(D, ctx.b, ctx.a, ctx.part.count)
-    rc = _lib.lib().serinv_ppobtaf(ctx.h._h, ctypes.byref(ctx.part), ctypes.byref(A), ctx.ws.data_ptr(),
-                                   ctx.ws.numel(), ctx.send.data_ptr(), ctx.info.data_ptr(), _stream())
+    rc = _lib.lib().serinv_ppobtaf_q(ctx.h._h, ctypes.byref(ctx.part), ctx.Q, ctypes.byref(A), ctx.ws.data_ptr(),
+                                     ctx.ws.numel(), ctx.send.data_ptr(), ctx.info.data_ptr(), _stream())
     if rc:
         raise RuntimeError(f"serinv_ppobtaf failed: {rc}")
 
@@ -97,9 +112,9 @@ def ppobtaf(ctx: DistContext, D):
 def ppobtasi(ctx: DistContext, D):
     """POBTARSSI (redundant) + PARTIAL_/PERMUTED_POBTASI on the local blocks."""
     A = _bta_local(D, ctx.b, ctx.a, ctx.part.count)
-    rc = _lib.lib().serinv_ppobtasi(ctx.h._h, ctypes.byref(ctx.part), ctypes.byref(A), ctx.ws.data_ptr(),
-                                    ctx.ws.numel(), ctx.recv.data_ptr(), ctx.info.data_ptr(),
-                                    ctx.logdet.data_ptr(), _stream())
+    rc = _lib.lib().serinv_ppobtasi_q(ctx.h._h, ctypes.byref(ctx.part), ctx.Q, ctypes.byref(A), ctx.ws.data_ptr(),
+                                      ctx.ws.numel(), ctx.recv.data_ptr(), ctx.info.data_ptr(),
+                                      ctx.logdet.data_ptr(), _stream())
     if rc:
         raise RuntimeError(f"serinv_ppobtasi failed: {rc}")
 

@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, b, a, out_q):
+def _worker(rank, world, port, n, b, a, out_q, Q=1):
     import sys
     import torch
     import torch.distributed as dist
@@ -35,7 +35,7 @@ def _worker(rank, world, port, n, b, a, out_q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     lib = ctypes.CDLL(build_daginterp())
-    lib.dag_dist_ws_doubles.restype = ctypes.c_int64
+    lib.dag_dist_ws_doubles_q.restype = ctypes.c_int64
     lib.dag_exchange_doubles.restype = ctypes.c_int64
     A = btagen.g2(5, n, b, a)
     parts = par.plan(n, world, 1.0)
@@ -46,19 +46,19 @@ def _worker(rank, world, port, n, b, a, out_q):
         D["arrow"] = np.zeros((1, 1, b))
         D["tip"] = np.zeros((1, 1))
     i64 = ctypes.c_int64
-    wsd = lib.dag_dist_ws_doubles(world, rank, i64(n), i64(s), i64(e - s), i64(b), i64(a))
+    wsd = lib.dag_dist_ws_doubles_q(world, Q, rank, i64(n), i64(s), i64(e - s), i64(b), i64(a))
     rec = lib.dag_exchange_doubles(i64(b), i64(a))
     ws = np.zeros(wsd + 64)
-    send = torch.zeros(rec, dtype=torch.float64)
-    recv = torch.zeros(world * rec, dtype=torch.float64)
+    send = torch.zeros(Q * rec, dtype=torch.float64)         # Q records per rank (sub-partitions)
+    recv = torch.zeros(world * Q * rec, dtype=torch.float64)
     info = ctypes.c_int(0)
     ld = ctypes.c_double(0)
     ptrs = [D[k].ctypes.data_as(P_) for k in ("diag", "lower", "arrow", "tip")]
-    rc = lib.dag_run_dist_phase(0, world, rank, i64(n), i64(s), i64(e - s), i64(b), i64(a), *ptrs,
+    rc = lib.dag_run_dist_phase_q(0, world, Q, rank, i64(n), i64(s), i64(e - s), i64(b), i64(a), *ptrs,
                                 ws.ctypes.data_as(P_), P_(send.data_ptr()), None, None, ctypes.byref(info))
     assert rc == 0 and info.value == 0
     sd.exchange(send, recv)                      # the real all-gather (gloo here, NCCL on GPUs)
-    rc = lib.dag_run_dist_phase(1, world, rank, i64(n), i64(s), i64(e - s), i64(b), i64(a), *ptrs,
+    rc = lib.dag_run_dist_phase_q(1, world, Q, rank, i64(n), i64(s), i64(e - s), i64(b), i64(a), *ptrs,
                                 ws.ctypes.data_as(P_), None, P_(recv.data_ptr()), ctypes.byref(ld),
                                 ctypes.byref(info))
     assert rc == 0 and info.value == 0
@@ -66,15 +66,16 @@ def _worker(rank, world, port, n, b, a, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,b,a", [(2, 9, 5, 2), (3, 11, 4, 0), (3, 13, 66, 3)])
-def test_distributed_gloo(world, n, b, a):
+@pytest.mark.parametrize("world,n,b,a,Q", [(2, 9, 5, 2, 1), (3, 11, 4, 0, 1), (3, 13, 66, 3, 1),
+                                           (2, 20, 5, 2, 3), (3, 26, 4, 1, 4)])
+def test_distributed_gloo(world, n, b, a, Q):
     import multiprocessing as mp
     import btagen
     from oracle import invariants as inv, sequential as seq
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, b, a, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, b, a, q, Q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]

@@ -74,7 +74,7 @@ def test_pselinv_ratio_and_smallest_middles():
         assert inv.max_block_err(to_host(D), X)[0] <= TOL
 
 
-def _run_distributed_on_one_gpu(A, P, r=1.0):
+def _run_distributed_on_one_gpu(A, P, r=1.0, Q=1):
     """Simulate P ranks of serinv_ppobtaf / all-gather / serinv_ppobtasi on cuda:0."""
     import torch
     sb = _sb()
@@ -87,7 +87,7 @@ def _run_distributed_on_one_gpu(A, P, r=1.0):
     for p, (s, e) in enumerate(parts):
         loc = sd.local_blocks(A, s, e, last=(p == P - 1))
         D = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in loc.items()}
-        ctx = sd.DistContext(h, P, p, n, s, e - s, b, a)
+        ctx = sd.DistContext(h, P, p, n, s, e - s, b, a, Q=Q)
         ranks.append((s, e, D, ctx))
     for s, e, D, ctx in ranks:
         sd.ppobtaf(ctx, D)
@@ -110,6 +110,28 @@ def test_distributed_entry_points(P, n, b, a):
     L, X, ld = seq.selinv(A)
     ranks, lds = _run_distributed_on_one_gpu(A, P)
     assert len(set(lds)) == 1                    # bit-identical on every rank
+    assert abs(lds[0] - ld) <= 1e-12 * abs(ld)
+    for s, e, D, ctx in ranks:
+        G = {k: v.cpu().numpy() for k, v in D.items()}
+        for i in range(s, e):
+            assert inv.rel_err(G["diag"][i - s], X["diag"][i]) <= TOL
+            if a:
+                assert inv.rel_err(G["arrow"][i - s], X["arrow"][i]) <= TOL
+            if i < n - 1:
+                assert inv.rel_err(G["lower"][i - s], X["lower"][i]) <= TOL
+        if a:
+            assert inv.rel_err(G["tip"], X["tip"]) <= TOL
+
+
+@pytest.mark.parametrize("P,Q", [(1, 3), (2, 2), (3, 4), (2, 40)])
+@pytest.mark.parametrize("n,b,a", [(170, 64, 4), (175, 70, 0)])
+def test_distributed_subpartitions(P, Q, n, b, a):
+    # serinv_ppobtaf_q / serinv_ppobtasi_q: Q sub-partitions per rank; (2, 40) has a
+    # reduced system of 158 blocks, solved by the nested algorithm
+    A = btagen.g2(23, n, b, a)
+    L, X, ld = seq.selinv(A)
+    ranks, lds = _run_distributed_on_one_gpu(A, P, Q=Q)
+    assert len(set(lds)) == 1
     assert abs(lds[0] - ld) <= 1e-12 * abs(ld)
     for s, e, D, ctx in ranks:
         G = {k: v.cpu().numpy() for k, v in D.items()}

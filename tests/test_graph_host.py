@@ -146,6 +146,23 @@ def test_pselinv_and_distributed_graphs(P, n, b, a, twist_last, monkeypatch):
         assert abs(ldv.value - ld) <= 1e-12 * max(1, abs(ld))
 
 
+@pytest.mark.parametrize("n,b,a,P,Q", [(24, 4, 2, 2, 2), (40, 8, 3, 3, 3), (30, 5, 0, 1, 4), (33, 6, 2, 2, 5),
+                                       (80, 4, 2, 4, 10), (140, 3, 1, 2, 35)])
+def test_distributed_subpartitions(n, b, a, P, Q):
+    # each rank splits its blocks into Q sub-partitions (serinv_ppobtaf_q / _q); the
+    # last two cases have reduced systems long enough for the nested solve
+    A0 = btagen.g2(7, n, b, a)
+    L, X, ld = seq.selinv(A0)
+    A, n_, b_, a_ = prep(A0)
+    ldv, info = ctypes.c_double(0), ctypes.c_int(0)
+    rc = lib().dag_run_distributed_q(ctypes.c_int64(n), ctypes.c_int64(b), ctypes.c_int64(a), P, Q,
+                                     ctypes.c_double(1.0), *ptrs(A), ctypes.byref(ldv), ctypes.byref(info))
+    assert rc == 0 and info.value == 0
+    e, where = inv.max_block_err(cut(A, X), X)
+    assert e < 1e-11, (e, where)
+    assert abs(ldv.value - ld) <= 1e-12 * max(1, abs(ld))
+
+
 def test_partition_plan_matches_oracle_reading():
     import paper_2503_17528_b200._lib  # noqa: F401  (the product plan lives in libserinv)
     # serinv_plan is exported by libserinv.so; compare with the oracle's reading R6 when available

@@ -316,12 +316,13 @@ int dag_auto_partitions(int64_t n, int64_t b, int *Ps, int cap) {
 
 // Simulate P ranks of the distributed path on the host.  Global arrays in, X out
 // (in place); each rank works on copies of its local blocks.
-int dag_run_distributed(int64_t n, int64_t b, int64_t a, int P, double r, double *diag, double *lower, double *arrow,
-                        double *tip, double *logdet, int *info) {
+// Q = sub-partitions per rank (serinv_ppobtaf_q / serinv_ppobtasi_q).
+int dag_run_distributed_q(int64_t n, int64_t b, int64_t a, int P, int Q, double r, double *diag, double *lower,
+                          double *arrow, double *tip, double *logdet, int *info) {
   std::vector<int64_t> st;
   if (!plan_partitions(n, P, r, st)) return -3;
   int64_t rec = exchange_doubles(b, a);
-  std::vector<double> records(rec * P, 0.0);
+  std::vector<double> records(rec * P * Q, 0.0);
   struct Rank {
     std::vector<double> D, L, A, T, ws;
     int64_t cnt;
@@ -343,8 +344,8 @@ int dag_run_distributed(int64_t n, int64_t b, int64_t a, int P, double r, double
     if (a) std::copy(arrow + s * a * b, arrow + e * a * b, k.A.begin());
     k.T.assign(std::max<int64_t>(a * a, 1), 0.0);
     if (a) std::copy(tip, tip + a * a, k.T.begin());
-    Graph g0 = build_distributed(0, P, p, n, s, cnt, b, a, opt);
-    Graph g1 = build_distributed(1, P, p, n, s, cnt, b, a, opt);
+    Graph g0 = build_distributed(0, P, p, n, s, cnt, b, a, opt, Q);
+    Graph g1 = build_distributed(1, P, p, n, s, cnt, b, a, opt, Q);
     if (!g0.error.empty() || !g1.error.empty()) {
       fprintf(stderr, "graph error: %s %s\n", g0.error.c_str(), g1.error.c_str());
       return -2;
@@ -356,14 +357,14 @@ int dag_run_distributed(int64_t n, int64_t b, int64_t a, int P, double r, double
     k.c.bufs[BUF_ARROW] = k.A.data();
     k.c.bufs[BUF_TIP] = k.T.data();
     k.c.bufs[BUF_WS] = k.ws.data();
-    k.c.bufs[BUF_EXT0] = records.data() + p * rec;
+    k.c.bufs[BUF_EXT0] = records.data() + p * Q * rec;
     if (run(g0, k.c)) return -1;
     if (k.c.info) *info = k.c.info;
   }
   double ld = 0;
   for (int p = 0; p < P; ++p) {
     Rank &k = R[p];
-    Graph g1 = build_distributed(1, P, p, n, st[p], k.cnt, b, a, opt);
+    Graph g1 = build_distributed(1, P, p, n, st[p], k.cnt, b, a, opt, Q);
     double ldp = 0;
     k.c.bufs[BUF_EXT0] = nullptr;
     k.c.bufs[BUF_EXT1] = records.data();
@@ -384,17 +385,26 @@ int dag_run_distributed(int64_t n, int64_t b, int64_t a, int P, double r, double
   return 0;
 }
 
+int dag_run_distributed(int64_t n, int64_t b, int64_t a, int P, double r, double *diag, double *lower, double *arrow,
+                        double *tip, double *logdet, int *info) {
+  return dag_run_distributed_q(n, b, a, P, 1, r, diag, lower, arrow, tip, logdet, info);
+}
+
 // One distributed phase on caller buffers (used by the gloo multi-process test).
+int64_t dag_dist_ws_doubles_q(int P, int Q, int rank, int64_t n, int64_t start, int64_t count, int64_t b,
+                              int64_t a) {
+  return distributed_ws_bytes(P, rank, n, start, count, b, a, Q) / 8;
+}
 int64_t dag_dist_ws_doubles(int P, int rank, int64_t n, int64_t start, int64_t count, int64_t b, int64_t a) {
-  return distributed_ws_bytes(P, rank, n, start, count, b, a) / 8;
+  return dag_dist_ws_doubles_q(P, 1, rank, n, start, count, b, a);
 }
 int64_t dag_exchange_doubles(int64_t b, int64_t a) { return exchange_doubles(b, a); }
-int dag_run_dist_phase(int phase, int P, int rank, int64_t n, int64_t start, int64_t count, int64_t b, int64_t a,
-                       double *diag, double *lower, double *arrow, double *tip, double *ws, double *ext0,
-                       double *ext1, double *logdet, int *info) {
+int dag_run_dist_phase_q(int phase, int P, int Q, int rank, int64_t n, int64_t start, int64_t count, int64_t b,
+                         int64_t a, double *diag, double *lower, double *arrow, double *tip, double *ws, double *ext0,
+                         double *ext1, double *logdet, int *info) {
   BuildOptions opt;
   opt.grid = 8;
-  Graph g = build_distributed(phase, P, rank, n, start, count, b, a, opt);
+  Graph g = build_distributed(phase, P, rank, n, start, count, b, a, opt, Q);
   if (!g.error.empty()) return -2;
   Ctx c;
   memset(c.bufs, 0, sizeof(c.bufs));
@@ -411,6 +421,13 @@ int dag_run_dist_phase(int phase, int P, int rank, int64_t n, int64_t start, int
   *info = c.info;
   if (logdet) *logdet = ld;
   return rc;
+}
+
+int dag_run_dist_phase(int phase, int P, int rank, int64_t n, int64_t start, int64_t count, int64_t b, int64_t a,
+                       double *diag, double *lower, double *arrow, double *tip, double *ws, double *ext0,
+                       double *ext1, double *logdet, int *info) {
+  return dag_run_dist_phase_q(phase, P, 1, rank, n, start, count, b, a, diag, lower, arrow, tip, ws, ext0, ext1,
+                              logdet, info);
 }
 
 int dag_stats_sequential(int kind, int64_t n, int64_t b, int64_t a, int grid, int64_t *ntasks, double *flops,
