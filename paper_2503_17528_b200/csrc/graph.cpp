@@ -1832,6 +1832,7 @@ void BuildOptions::apply_env() {
       else if (k == "carry_chain") carry_chain = v != 0;
       else if (k == "carry_min_b") carry_min_b = (int)v;
       else if (k == "chain_step") chain_step = v != 0;
+      else if (k == "dist_len") dist_len = (int)v;
     }
     i = j + 1;
   }
@@ -2011,6 +2012,23 @@ std::vector<int> auto_partitions(int64_t n, int64_t b) {
   return Ps;
 }
 
+// Nesting plan for the distributed reduced system (solved redundantly on every
+// rank, on the critical path of all of them): partitions of about `len` blocks
+// per level (len <= 0: the single-device default, auto_partitions).
+std::vector<int> reduced_plan(int64_t nr, int64_t b, int len) {
+  if (len <= 0) return auto_partitions(nr, b);
+  std::vector<int> Ps;
+  int64_t m = nr;
+  while (m > len && (int)Ps.size() < 4) {
+    int64_t P = std::min<int64_t>((m + len - 1) / len, (m + 1) / 3);
+    if (P < 2) break;
+    Ps.push_back((int)P);
+    m = reduced_size((int)P, true);
+  }
+  if (Ps.empty()) Ps.push_back(1);
+  return Ps;
+}
+
 // Split a rank's blocks [start, start+count) into Q consecutive sub-partitions
 // (even sizes, remainder to the earliest).  Every sub-partition needs >= 2
 // blocks except a global first one (>= 1).  Returns false if infeasible.
@@ -2049,7 +2067,7 @@ Graph build_distributed(int phase, int P, int rank, int64_t n, int64_t start, in
   const int PQ = P * Q;
   const bool tw = opt.twist_last && PQ >= 2;
   const int nr = reduced_size(PQ, tw);
-  std::vector<int> Ps2 = Q > 1 ? auto_partitions(nr, b) : std::vector<int>{1};
+  std::vector<int> Ps2 = reduced_plan(nr, b, opt.dist_len);
   Ctx cx;
   cx.opt = opt;
   cx.slot_cap = slot_bound(count + 4 * PQ + 8, b, a);

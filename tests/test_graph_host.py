@@ -148,9 +148,11 @@ def test_pselinv_and_distributed_graphs(P, n, b, a, twist_last, monkeypatch):
 
 @pytest.mark.parametrize("n,b,a,P,Q", [(24, 4, 2, 2, 2), (40, 8, 3, 3, 3), (30, 5, 0, 1, 4), (33, 6, 2, 2, 5),
                                        (80, 4, 2, 4, 10), (140, 3, 1, 2, 35)])
-def test_distributed_subpartitions(n, b, a, P, Q):
+@pytest.mark.parametrize("dist_len", [0, 6])
+def test_distributed_subpartitions(n, b, a, P, Q, dist_len, monkeypatch):
     # each rank splits its blocks into Q sub-partitions (serinv_ppobtaf_q / _q); the
-    # last two cases have reduced systems long enough for the nested solve
+    # last two cases (and dist_len = 6: partitions of ~6 blocks) nest the reduced solve
+    monkeypatch.setenv("SERINV_OPT", f"dist_len={dist_len}")
     A0 = btagen.g2(7, n, b, a)
     L, X, ld = seq.selinv(A0)
     A, n_, b_, a_ = prep(A0)
