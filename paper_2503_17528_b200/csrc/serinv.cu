@@ -501,6 +501,11 @@ int serinv_dist_auto_q(int64_t count, int64_t b) {
   if (count < 1 || b < 1) return SERINV_ERR_SHAPE;
   std::vector<int> v = auto_partitions(count, b);
   int Q = v.empty() ? 1 : v[0];
+  // chain-bound blocks (b <= 1024, where the single-device selinv twists): two
+  // chains per rank (measured with tools/scaling_sim.py, C2 at P = 4 / 8:
+  // E_weak 40.6 / 38.5 % at Q = 1 -> 46.9 / 44.8 % at Q = 2); b = 2048 (C3) is
+  // FP64-bound and keeps Q = 1
+  if (Q == 1 && b <= 1024 && count >= 64) Q = 2;
   while (Q > 1 && count < 2 * (int64_t)Q) --Q;
   return Q;
 }
