@@ -125,9 +125,10 @@ def main():
     ap.add_argument("--r", type=float, default=1.0)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--strong", action="store_true", help="fixed total n (strong scaling)")
+    ap.add_argument("--shape", default=None, help="n,b,a instead of a named config (e.g. dataset (1): 256,1024,256)")
     ap.add_argument("--q", default="auto", help="sub-partitions per rank, comma list (auto = serinv_dist_auto_q)")
     args = ap.parse_args()
-    n1, b, a = CFG[args.config]
+    n1, b, a = CFG[args.config] if args.shape is None else map(int, args.shape.split(","))
     out = {"config": args.config, "b": b, "a": a, "r": args.r, "bw_allgather_model": BW_NVLINK,
            "lat_allgather_model": LAT_ALLGATHER, "rows": []}
     t_seq = single(n1, b, a, [1], args.reps)
@@ -147,7 +148,16 @@ def main():
             print(json.dumps({"P": P, "q": q, "error": str(ex)}), flush=True)
             continue
         T = max(tF) + t_ag + max(tS)
-        row = {"P": P, "Q": Q, "n": n, "parts": parts, "ppobtaf_ms": [round(x * 1e3, 3) for x in tF],
+        # flop-model ceiling: sequential work / (P x (busiest rank + redundant reduced solve));
+        # per block F+SI ~ 7 b^3 at the chain ends, ~19 b^3 in a middle partition (fill-in chains)
+        w_rank = []
+        for p, (s_, e_) in enumerate(parts):
+            c = e_ - s_
+            subs = [c // Q + (1 if q < c % Q else 0) for q in range(Q)]
+            w_rank.append(sum((7 if (p * Q + q in (0, P * Q - 1)) else 19) * m for q, m in enumerate(subs)))
+        w_red = 7 * (2 * P * Q - 2)
+        e_flop = 7 * n / (P * (max(w_rank) + w_red))
+        row = {"E_flop_model": round(e_flop, 4),"P": P, "Q": Q, "n": n, "parts": parts, "ppobtaf_ms": [round(x * 1e3, 3) for x in tF],
                "ppobtasi_ms": [round(x * 1e3, 3) for x in tS], "allgather_ms_model": round(t_ag * 1e3, 4),
                "T_ms": round(T * 1e3, 3), "TFLOPs_total": round(flops(n, b, a) / T / 1e12, 3),
                ("E_strong" if args.strong else "E_weak"): round(t1 / (P * T) if args.strong else t1 / T, 4)}
