@@ -2014,9 +2014,16 @@ std::vector<int> auto_partitions(int64_t n, int64_t b) {
 
 // Nesting plan for the distributed reduced system (solved redundantly on every
 // rank, on the critical path of all of them): partitions of about `len` blocks
-// per level (len <= 0: the single-device default, auto_partitions).
+// per level (len <= 0: the measured default below).
 std::vector<int> reduced_plan(int64_t nr, int64_t b, int len) {
-  if (len <= 0) return auto_partitions(nr, b);
+  if (len <= 0) {
+    // measured (tools/scaling_sim.py, P = 8): nesting in ~16-block partitions at
+    // b = 512 (C4: E_weak 57.7 -> 66.6 %), ~32 at b = 64 (C5: 62.8 -> 66.4 %); at
+    // b = 1024 the fill-in of a nested level costs more than the chain it cuts
+    // (C2: 45.0 -> 41.1 % at len 8), so large blocks keep the single-device plan
+    if (b > 512) return auto_partitions(nr, b);
+    len = b <= 128 ? 32 : 16;
+  }
   std::vector<int> Ps;
   int64_t m = nr;
   while (m > len && (int)Ps.size() < 4) {
