@@ -71,6 +71,15 @@ def bench_config(name, cfg):
                    if bta_bytes(n, b, a) > L2_BYTES else "inputs fit in L2 (parity-size case)")}
 
 
+def algorithmic_bytes(n, b, a):
+    """read + write of the whole BTA per phase (2 * 8 * (n(2b^2 + ab) - b^2 + a^2)),
+    F + SI = 2 phases."""
+    return 2 * 2 * 8 * (n * (2 * b * b + a * b) - b * b + a * a)
+
+
+HBM_PEAK_GBS = 6549.1     # MEASURED_PEAKS.json hbm_gbs (copy bandwidth on this pool's B200s)
+
+
 def bta_bytes(n, b, a):
     return 8 * (n * b * b + (n - 1) * b * b + n * a * b + a * a)
 
@@ -419,6 +428,12 @@ def main():
                          "traffic": ncu_traffic(args.config) if world == 1 else None,
                          "kernel": "serinv_exec_kernel (persistent, 1 launch per step)",
                          "peak_source": "measured DMMA f64 peak, profiles/fp64_peaks_r01.json"},
+            # small-b evidence: algorithmic HBM bytes per step / step time
+            "roofline_hbm": {"bound": "hbm", "achieved": round(algorithmic_bytes(n, b, a) / sec_per_step / 1e9 / N, 2),
+                             "peak": HBM_PEAK_GBS, "unit": "GB/s",
+                             "frac": round(algorithmic_bytes(n, b, a) / sec_per_step / 1e9 / N / HBM_PEAK_GBS, 4),
+                             "bytes_per_step": algorithmic_bytes(n, b, a),
+                             "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
             "clocks": clocks,
             "gpu_launches": launches * args.steps,
         }
