@@ -9,3 +9,6 @@ done
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/final2/bench_reference_C2.json 2>&1; echo ref=$?
 cat gpurun_out/final2/bench_*.json
 bash tools/gpu_d1.sh
+timeout 900 python tools/scaling_sim.py C4 2,4,8 --no-seq > gpurun_out/final2/model_C4.txt 2>&1; echo simC4=$?
+timeout 1200 python tools/scaling_sim.py C5 2,4,8 --no-seq --reps 1 > gpurun_out/final2/model_C5.txt 2>&1; echo simC5=$?
+tail -n 4 gpurun_out/final2/model_*.txt
