@@ -1294,7 +1294,10 @@ bool use_twist(int kind, int64_t n, int64_t b, const BuildOptions &opt) {
   return (kind == 2 || kind == 6) && opt.twist_min_n > 0 && n >= std::max(3, opt.twist_min_n) && b <= opt.twist_max_b;
 }
 
-void twisted_problem(Ctx &cx, Problem &P, Twist &tw, int64_t n, int64_t b, int64_t a) {
+// Twisted problem on an arbitrary BTA storage (D, Lo, Ar, tip; row() labels info
+// rows): the user matrix (build_twisted_selinv) or an assembled reduced system.
+void twisted_problem(Ctx &cx, Problem &P, Twist &tw, int64_t n, int64_t b, int64_t a, const Fam &FD, const Fam &FL,
+                     const Fam &FA, Loc tip, const std::function<int64_t(int64_t)> &row, int64_t tip_row) {
   const int64_t m = (n - 1) / 2;
   tw.m = m;
   tw.T = Fam{BUF_WS, cx.alloc((n - 1 - m) * b * b), b * b, (int32_t)b};
@@ -1318,10 +1321,10 @@ void twisted_problem(Ctx &cx, Problem &P, Twist &tw, int64_t n, int64_t b, int64
   P.nqueue2.assign(nn, 2);
   for (int64_t i = 0; i < n; ++i) {
     const int X = tw.pos[i];
-    P.rowbase[X] = i * b;
-    P.blk[{X, X}] = blkref(famD(b).at(i), (int)b, (int)b);
+    P.rowbase[X] = row(i);
+    P.blk[{X, X}] = blkref(FD.at(i), (int)b, (int)b);
     if (i < m) {  // top chain: successor i+1, L_{i+1,i} in lower[i]
-      P.blk[{tw.pos[i + 1], X}] = blkref(famL(b).at(i), (int)b, (int)b);
+      P.blk[{tw.pos[i + 1], X}] = blkref(FL.at(i), (int)b, (int)b);
       P.rows[X].push_back(tw.pos[i + 1]);
     } else if (i > m) {  // bottom chain: successor i-1, in T(i)
       P.blk[{tw.pos[i - 1], X}] = blkref(tw.T.at(i - m - 1), (int)b, (int)b);
@@ -1330,13 +1333,13 @@ void twisted_problem(Ctx &cx, Problem &P, Twist &tw, int64_t n, int64_t b, int64
       P.nqueue2[X] = 4;
     }
     if (a > 0) {
-      P.blk[{A, X}] = blkref(famA(b, a).at(i), (int)a, (int)b);
+      P.blk[{A, X}] = blkref(FA.at(i), (int)a, (int)b);
       P.rows[X].push_back(A);
     }
   }
   if (a > 0) {
-    P.rowbase[A] = n * b;
-    P.blk[{A, A}] = blkref(Loc{BUF_TIP, (int32_t)a, 0}, (int)a, (int)a);
+    P.rowbase[A] = tip_row;
+    P.blk[{A, A}] = blkref(tip, (int)a, (int)a);
   }
 }
 
@@ -1348,7 +1351,8 @@ Graph build_twisted_selinv(Ctx &cx, int64_t n, int64_t b, int64_t a, bool stream
   cx.slot_region = cx.alloc(cx.slot_cap);
   Problem P;
   Twist tw;
-  twisted_problem(cx, P, tw, n, b, a);
+  twisted_problem(cx, P, tw, n, b, a, famD(b), famL(b), famA(b, a), Loc{BUF_TIP, (int32_t)a, 0},
+                  [b](int64_t i) { return i * b; }, n * b);
   Builder bld(cx, P);
   bld.concurrency = 2;
   bld.allocate(true);
@@ -1694,11 +1698,59 @@ void solve_reduced_chain(Ctx &cx, int64_t b, int64_t a, int nr, Reduced &R) {
   for (int X = nn - 1; X >= 0; --X) R.B->invert_node(X);
 }
 
+// POBTARSSI in the twisted order (reading R13): the reduced system is alone on
+// the critical path after the exchange, so its chain is split in two (top-down
+// and bottom-up towards the middle block).  Bottom couplings live transposed in
+// workspace T(j) and are copied back (with their X-ready signals) at the end.
+void solve_reduced_twisted(Ctx &cx, int64_t b, int64_t a, int nr, Reduced &R) {
+  Twist tw;
+  twisted_problem(cx, R.P, tw, nr, b, a, R.D, R.Lo, R.Ar, R.tip, R.V.row, R.V.tip_row);
+  R.B.reset(new Builder(cx, R.P));
+  Builder &bld = *R.B;
+  bld.concurrency = 2;
+  bld.allocate(true);
+  const int nn = (int)R.P.size.size();
+  const int64_t m = tw.m;
+  std::vector<int32_t> tin(nr, -1);
+  for (int64_t j = m + 1; j < nr; ++j) {  // T(j) = A_{j,j-1}^T
+    tin[j] = cx.new_ctr();
+    cx.copy_block(tw.T.at(j - m - 1), R.Lo.at(j - 1), (int)b, (int)b, true, R.ready, {tin[j]});
+  }
+  std::vector<int64_t> blk_of(nn, -1);
+  for (int64_t i = 0; i < nr; ++i) blk_of[tw.pos[i]] = i;
+  for (int X = 0; X < nn; ++X) {
+    bld.input_waits = R.ready;
+    if (blk_of[X] > m) bld.input_waits.push_back(tin[blk_of[X]]);
+    bld.factor_node(X);
+  }
+  bld.input_waits = R.ready;
+  for (int X = 0; X < nn; ++X) bld.precompute_node(X, true);
+  for (int X = nn - 1; X >= 0; --X) {
+    bld.invert_node(X);
+    const int64_t i = blk_of[X];
+    if (i > m) {  // X_{i,i-1} = T(i)^T
+      const Loc src = tw.T.at(i - m - 1);
+      const Loc dst = R.Lo.at(i - 1);
+      std::vector<int32_t> w;
+      for (int q = 0; q < ntiles(b); ++q) w.push_back(cx.XRC(src, q, 0));
+      cx.copy_block(dst, src, (int)b, (int)b, true, w, {},
+                    [&](RawTask &rt, int q, int c) { cx.sig_xblock(rt, dst, q, c); });
+    }
+  }
+}
+
+void solve_reduced(Ctx &cx, int64_t b, int64_t a, int nr, Reduced &R) {
+  if (cx.opt.twist_reduced && nr >= 4)
+    solve_reduced_twisted(cx, b, a, nr, R);
+  else
+    solve_reduced_chain(cx, b, a, nr, R);
+}
+
 void reduced_from_records(Ctx &cx, const View &V0, int P, int64_t b, int64_t a, int32_t rbuf, int64_t rec0,
                           int64_t recsz, const std::vector<int64_t> &starts, const std::vector<int32_t> &inwaits,
                           Reduced &R, bool tw) {
   assemble_reduced(cx, V0, P, b, a, rbuf, rec0, recsz, starts, inwaits, R, tw);
-  solve_reduced_chain(cx, b, a, reduced_size(P, tw), R);
+  solve_reduced(cx, b, a, reduced_size(P, tw), R);
 }
 
 // Copy the true-inverse boundary blocks of partition ps from X_r into its
@@ -1777,7 +1829,8 @@ int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a, const Bui
   Problem P;
   if (use_twist(kind, n, b, opt)) {
     Twist tw;
-    twisted_problem(cx, P, tw, n, b, a);
+    twisted_problem(cx, P, tw, n, b, a, famD(b), famL(b), famA(b, a), Loc{BUF_TIP, (int32_t)a, 0},
+                    [b](int64_t i) { return i * b; }, n * b);
     Builder bld(cx, P);
     bld.allocate(true);
     return cx.ws_top * 8;
@@ -1833,6 +1886,7 @@ void BuildOptions::apply_env() {
       else if (k == "carry_min_b") carry_min_b = (int)v;
       else if (k == "chain_step") chain_step = v != 0;
       else if (k == "dist_len") dist_len = (int)v;
+      else if (k == "twist_reduced") twist_reduced = v != 0;
     }
     i = j + 1;
   }
@@ -1952,7 +2006,7 @@ bool psolve_level(Ctx &cx, const View &V, int64_t n, int64_t b, int64_t a, const
   assemble_reduced(cx, V, P, b, a, BUF_WS, recs, recsz, starts, {packed}, R, tw);
   const int nr = reduced_size(P, tw);
   bool nested = lvl + 1 < Ps.size() && psolve_level(cx, R.V, nr, b, a, Ps, lvl + 1, r, R.ready);
-  if (!nested) solve_reduced_chain(cx, b, a, nr, R);
+  if (!nested) solve_reduced(cx, b, a, nr, R);
   for (int p = 0; p < P; ++p) {
     parts[p].done.push_back(packed);  // scatter overwrites what the pack copies read
     scatter_xr(cx, parts[p], P, b, a, R);
@@ -2126,7 +2180,7 @@ Graph build_distributed(int phase, int P, int rank, int64_t n, int64_t start, in
   std::vector<int> lv{0};
   lv.insert(lv.end(), Ps2.begin(), Ps2.end());
   bool nested = Ps2[0] > 1 && psolve_level(cx, R.V, nr, b, a, lv, 1, 1.0, R.ready);
-  if (!nested) solve_reduced_chain(cx, b, a, nr, R);
+  if (!nested) solve_reduced(cx, b, a, nr, R);
   for (auto &ps : parts) {
     scatter_xr(cx, ps, PQ, b, a, R);
     ppobtasi_part(cx, ps, b, false);  // W tiles recomputed by TRTRI (no fused POTRF here)

@@ -111,6 +111,7 @@ struct BuildOptions {
                                 // measured slower: E's last update becomes a bulk round trip on the chain)        // POTRF publishes W before its log-det partial and L (TF_EARLY_SIG)            // POTRF tasks: 8 x 8-block warp-pipelined Cholesky (else 16 x 16 leaves)
   int wide_min_wave = 512;      // 128 x 64 tasks for inversion waves of >= this many tiles (0: never)
   int twist_max_b = 1024;       // ... and b <= twist_max_b (larger blocks: the one-sided chain hides under the work)
+  bool twist_reduced = true;    // reduced systems (>= 4 blocks) solved in the twisted order (two chains)
   int dist_len = 0;             // distributed reduced system: nested partitions of ~dist_len blocks (0: measured default)
   // overrides from the environment (SERINV_OPT="key=value,..."), for tuning runs
   void apply_env();
