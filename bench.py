@@ -93,8 +93,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference", "library"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--r", type=float, default=1.0,
-                    help="N > 1: blocks of the first / last rank relative to a middle rank (serinv_plan_ends)")
+    ap.add_argument("--r", default="auto",
+                    help="N > 1: blocks of the first / last rank relative to a middle rank (serinv_plan_ends); "
+                         "'auto' = distributed.auto_r(b)")
     ap.add_argument("--q", default="auto",
                     help="N > 1: sub-partitions per rank (serinv_ppobtaf_q); 'auto' = serinv_dist_auto_q")
     ap.add_argument("--partitions", default="auto",
@@ -316,7 +317,8 @@ def main():
         from paper_2503_17528_b200 import distributed as sd
         # twisted scheme (reading R14): first and last rank are fill-in free, so they
         # take r x a middle rank's blocks (flop/chain balance)
-        parts = sb.plan_ends(n, world, args.r)
+        r_end = sd.auto_r(b) if args.r == "auto" else float(args.r)
+        parts = sb.plan_ends(n, world, r_end)
         s, e = parts[rank]
         # sub-partitions per rank (intra-GPU partitioning of each rank's chain), the
         # same on every rank: the library's default for the smallest rank
@@ -415,7 +417,8 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": bench_config(args.config, cfg),
-            "plan": {"n_global": n, "parallelism": f"partitions{world}x{Q}" if world > 1 else
+            "plan": {"n_global": n, "end_ratio_r": r_end if world > 1 else None,
+                     "parallelism": f"partitions{world}x{Q}" if world > 1 else
                      ("single" if Ps == [1] else "intra-GPU partitions " + "x".join(map(str, Ps))),
                      "step": ("POBTAF+POBTASI (serinv_selinv)" if Ps == [1] else
                               "PPOBTAF+POBTARSSI+PPOBTASI in one launch (serinv_pselinv_nested)")

@@ -51,6 +51,14 @@ def exchange(send, recv, group=None):
     dist.all_gather_into_tensor(recv, send, group=group)
 
 
+def auto_r(b: int) -> float:
+    """Default end-rank ratio for serinv_plan_ends (first / last rank blocks relative to
+    a middle rank), measured with tools/scaling_sim.py at P = 8
+    (profiles/r01/scaling/end_ratio/): b >= 2048 (C3 strong) 2.0 (E 35 -> 42 %),
+    b = 1024 (C2 weak) 1.2 (45.0 -> 46.7 %), b <= 512 (C4 weak) 1.0 (1.2 is slower)."""
+    return 2.0 if b >= 2048 else (1.2 if b >= 1024 else 1.0)
+
+
 def dist_auto_q(count: int, b: int) -> int:
     """The library's default sub-partitions per rank (serinv_dist_auto_q)."""
     q = _lib.lib().serinv_dist_auto_q(count, b)

@@ -129,7 +129,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config")
     ap.add_argument("Ps")
-    ap.add_argument("--r", type=float, default=1.0)
+    ap.add_argument("--r", type=float, default=1.0, help="end-rank ratio (bench default: distributed.auto_r(b))")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--strong", action="store_true", help="fixed total n (strong scaling)")
     ap.add_argument("--no-seq", action="store_true", help="skip the one-chain T1 when the auto plan partitions")
