@@ -92,6 +92,9 @@ def parse():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference", "library"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the distributed path (NCCL process group, serinv_ppobtaf_q / _q) even at N = 1 "
+                         "(exercises the N > 1 code path on a one-GPU box)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--r", default="auto",
                     help="N > 1: blocks of the first / last rank relative to a middle rank (serinv_plan_ends); "
@@ -287,7 +290,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     N = max(args.gpus, world)
     torch.cuda.set_device(local)
-    if world > 1:
+    dpath = world > 1 or args.dist   # distributed path (one process per GPU)
+    if dpath:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_loc, b, a = cfg["n"], cfg["b"], cfg["a"]
     n = n_loc * world
@@ -295,13 +299,13 @@ def main():
     h = sb.default_handle(local)
 
     def barrier():
-        if world > 1:
+        if dpath:
             dist.barrier()
 
     # ---- inputs resident in HBM (pristine copy restored between steps, untimed); the
     # generator's torch twin builds G1 directly in HBM, bit-identical to btagen.g1
     Ps = [1]
-    if world == 1:
+    if not dpath:
         Ps = (sb.auto_partitions(n, b) if args.partitions == "auto"
               else [int(x) for x in args.partitions.split("x")])
         pristine = btagen.g1_torch(0, n, b, a, device=f"cuda:{local}")
@@ -341,7 +345,7 @@ def main():
         restore()
         step()
     torch.cuda.synchronize()
-    info = h.scalars()[0] if world == 1 else ctx.info
+    info = h.scalars()[0] if not dpath else ctx.info
     if int(info.item()) != 0:
         raise SystemExit(f"factorisation failed: info={int(info.item())}")
 
@@ -361,9 +365,9 @@ def main():
             torch.cuda.synchronize()
             barrier()
             times.append(e0.elapsed_time(e1) / 1e3)
-    launches = h.last_launches() * (1 if world == 1 else 2)  # N > 1: ppobtaf + ppobtasi
+    launches = h.last_launches() * (1 if not dpath else 2)  # distributed: ppobtaf + ppobtasi
     t = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if dpath:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total = float(t.item())
     sec_per_step = total / args.steps
@@ -371,7 +375,7 @@ def main():
 
     # ---- end to end through the public API with host buffers (pinned H2D, D2H of X + logdet)
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not dpath:
         pinned = {k: v.cpu().pin_memory() for k, v in pristine.items()}
         out = {k: torch.empty_like(v).pin_memory() for k, v in pinned.items()}
         ld_host = torch.empty(1, dtype=torch.float64).pin_memory()
@@ -417,18 +421,18 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": bench_config(args.config, cfg),
-            "plan": {"n_global": n, "end_ratio_r": r_end if world > 1 else None,
-                     "parallelism": f"partitions{world}x{Q}" if world > 1 else
+            "plan": {"n_global": n, "end_ratio_r": r_end if dpath else None,
+                     "parallelism": f"partitions{world}x{Q}" if dpath else
                      ("single" if Ps == [1] else "intra-GPU partitions " + "x".join(map(str, Ps))),
                      "step": ("POBTAF+POBTASI (serinv_selinv)" if Ps == [1] else
                               "PPOBTAF+POBTARSSI+PPOBTASI in one launch (serinv_pselinv_nested)")
-                             if world == 1 else "PPOBTAF + NCCL all-gather + PPOBTASI"},
+                             if not dpath else "PPOBTAF + NCCL all-gather + PPOBTASI"},
             "seconds_per_step": round(sec_per_step, 6),
             "tflops_pobtaf_plus_pobtasi": round(value, 4),
             "fraction_of_fp64_peak": round(value / (FP64_PEAK_TFLOPS * N), 4),
             "roofline": {"bound": "tensor", "achieved": round(value / N, 4), "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": round(value / N / FP64_PEAK_TFLOPS, 4),
-                         "traffic": ncu_traffic(args.config) if world == 1 else None,
+                         "traffic": ncu_traffic(args.config) if not dpath else None,
                          "kernel": "serinv_exec_kernel (persistent, 1 launch per step)",
                          "peak_source": "measured DMMA f64 peak, profiles/fp64_peaks_r01.json"},
             # small-b evidence: algorithmic HBM bytes per step / step time
@@ -445,7 +449,7 @@ def main():
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dpath:
         dist.destroy_process_group()
     return 0
 
