@@ -375,6 +375,38 @@ def main():
 
     # ---- end to end through the public API with host buffers (pinned H2D, D2H of X + logdet)
     e2e = None
+    if not args.no_e2e and dpath:
+        # per rank: pinned H2D of the local blocks, ppobtaf -> NCCL all-gather -> ppobtasi,
+        # D2H of the local X blocks + log det; whole-job bytes, time = max over ranks
+        pinned = {k: v.cpu().pin_memory() for k, v in pristine.items()}
+        out = {k: torch.empty_like(v).pin_memory() for k, v in pinned.items()}
+        ld_host = torch.empty(1, dtype=torch.float64).pin_memory()
+        h2d_loc = sum(v.numel() * 8 for v in pinned.values())
+        et = []
+        for it in range(args.warmup + args.steps):
+            barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for k in work:
+                work[k].copy_(pinned[k], non_blocking=True)
+            step()
+            for k in work:
+                out[k].copy_(work[k], non_blocking=True)
+            ld_host.copy_(ctx.logdet, non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if it >= args.warmup:
+                et.append(e0.elapsed_time(e1) / 1e3)
+        te = torch.tensor([statistics.mean(et), float(h2d_loc)], dtype=torch.float64, device="cuda")
+        tb = te.clone()
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tb, op=dist.ReduceOp.SUM)
+        h2d = int(tb[1].item())
+        e2e = {"value": round(fl / float(te[0].item()) / 1e12, 4), "unit": "TFLOP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d + 8 * world,
+               "ms_per_step": round(float(te[0].item()) * 1e3, 3)}
     if not args.no_e2e and not dpath:
         pinned = {k: v.cpu().pin_memory() for k, v in pristine.items()}
         out = {k: torch.empty_like(v).pin_memory() for k, v in pinned.items()}
