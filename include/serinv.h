@@ -78,8 +78,11 @@ const char *serinv_version(void);
 /* Human-readable text for a status code. */
 const char *serinv_status_string(int status);
 
-/* Create / destroy a handle bound to CUDA device `cuda_device`.  One handle per
- * host thread; the handle caches task graphs keyed by problem shape. */
+/* Create / destroy a handle bound to CUDA device `cuda_device`.  The handle caches
+ * task graphs keyed by problem shape (and SERINV_OPT).  Calls through one handle
+ * execute on the device in call order, whatever streams they use (each call waits
+ * for the previous one's work; the enqueue is serialised across host threads), so
+ * a handle may be shared, at the price of that serialisation. */
 int serinv_create(serinv_handle_t *h, int cuda_device);
 int serinv_destroy(serinv_handle_t h);
 
@@ -194,66 +197,99 @@ int serinv_pselinv_nested(serinv_handle_t h, const serinv_bta_t *A, int nlev, co
                           void *d_ws, size_t ws_bytes, int *d_info, double *d_logdet, void *stream);
 
 /*
- * Distributed partitioned method, one process per GPU (rank p of P owns the
- * blocks [starts[p], starts[p+1]) of serinv_plan).  The caller passes its LOCAL
- * blocks:
+ * Partition plan the partitioned solvers (serinv_pselinv, serinv_pselinv_nested)
+ * actually use: serinv_plan_ends with the twisted last partition (the default,
+ * reading R14), serinv_plan when SERINV_OPT=twist_last=0 selects the paper's
+ * scheme.  Same arguments and errors as serinv_plan.
+ */
+int serinv_pselinv_plan(int64_t n, int P, double r, int64_t *starts);
+
+/* ------------------------------------------------------------------------- */
+/* Distributed method, one process per GPU (Sec. 3, Alg. 3-6; the    */
+/* paper's exchange is NCCL).                                      */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * Communicator.  An NCCL communicator owned by the library; it carries the one
+ * exchange step of the method (an all-gather of the per-partition records, which
+ * replaces the paper's Reduce + Gather + Scatter).  NCCL is loaded at run
+ * time (libnccl.so.2; the copy already mapped into the process is reused), so the
+ * library itself does not depend on it.
+ *   serinv_nccl_unique_id  on ONE rank: writes SERINV_NCCL_ID_BYTES bytes that the
+ *                          caller broadcasts to every rank (e.g. torch.distributed).
+ *   serinv_comm_init       collective over the P ranks (ncclCommInitRank) on CUDA
+ *                          device `cuda_device`; id may be NULL only for P == 1 (no
+ *                          NCCL: the all-gather of one rank is a device copy).
+ *   serinv_comm_destroy    collective; frees the communicator.
+ * Errors: SERINV_ERR_NCCL (NCCL missing or an NCCL call failed), -k argument k.
+ */
+#define SERINV_NCCL_ID_BYTES 128
+typedef struct serinv_comm *serinv_comm_t;
+int serinv_nccl_unique_id(unsigned char *id);
+int serinv_comm_init(serinv_comm_t *comm, const unsigned char *id, int P, int rank, int cuda_device);
+int serinv_comm_destroy(serinv_comm_t comm);
+
+/*
+ * Rank p of P owns the global blocks [start, start+count) (e.g. of serinv_plan /
+ * serinv_plan_ends) and passes its LOCAL blocks:
  *     diag  [count][b][b], arrow [count][a][b],
  *     lower [count][b][b]  where lower[count-1] is the coupling A_{e,e-1} to the
  *                          next rank (P:378 assigns A_{i+1,i} to column i's
  *                          partition); the last rank passes count-1 lower blocks.
  *     tip   replicated: every rank passes the same A_{n,n} and receives X_{n,n}.
- * part = {P, rank, n_global, start, count}.
+ * part = {P, rank, n_global, start, count}.  Each rank splits its blocks into Q
+ * consecutive sub-partitions (intra-GPU partitioning; even sizes,
+ * remainder to the earliest, each >= 2 blocks when Q > 1): the matrix has P*Q
+ * partitions.  Q = 1 is the paper's one partition per process; Q must be the
+ * same on every rank (serinv_dist_auto_q is the library's default).
  *
- *   serinv_ppobtaf   PARTIAL_POBTAF (rank 0) or PERMUTED_POBTAF (rank > 0) on
- *                    the local blocks (no communication), then packs this rank's
- *                    boundary blocks + U_p + partial log det into d_sendbuf
- *                    (serinv_exchange_bytes bytes).
- *   (caller)         all-gather of the P send buffers into d_recvbuf (rank
- *                    order) -- NCCL via torch.distributed in the Python binding.
- *   serinv_ppobtasi  assembles the reduced system A_r from d_recvbuf in a fixed
- *                    rank order (bit-identical on every rank), runs POBTARSSI
- *                    redundantly, then PARTIAL_/PERMUTED_POBTASI on the local
- *                    blocks.  Writes X in place and the global log det.
- * d_ws must be passed unchanged from serinv_ppobtaf to serinv_ppobtasi (it keeps
- * the fill-in factor blocks B_i, Alg. 6 l.3/l.11).
+ *   serinv_ppobtaf   PARTIAL_POBTAF (partition 0) / PERMUTED_POBTAF (middle
+ *                    partitions, Alg. 4 fill-in chain) / the twisted last partition
+ *                    (reading R14) on the local blocks -- no communication -- then
+ *                    packs the Q exchange records (boundary blocks, couplings, U_p,
+ *                    the partial log det, this rank's info and the partition
+ *                    bounds) and all-gathers the P*Q records over `comm` (one
+ *                    ncclAllGather on `stream`).
+ *   serinv_ppobtasi  assembles the reduced system A_r (2PQ-2 blocks; 2PQ-1 with
+ *                    twist_last=0) from the gathered records in partition order --
+ *                    bit-identical on every rank --, solves it redundantly
+ *                    (POBTARSSI; nested partitioned solve when long, Sec. 4.2), then
+ *                    PARTIAL_/PERMUTED_POBTASI on the local blocks: X in place,
+ *                    X_{n,n} in tip, the global log det in *d_logdet.
+ * d_ws: serinv_ppobtaf_ws(part, Q, ...) bytes, passed UNCHANGED from serinv_ppobtaf
+ * to serinv_ppobtasi (it holds the fill-in factor blocks B_i, Alg. 6 l.3/l.11, and
+ * the gathered records).  comm must have P == part->P and rank == part->rank.
+ * Status: *d_info after serinv_ppobtasi is the SAME on every rank: the smallest
+ * 1-based global row of a non-positive pivot any rank's PPOBTAF met; else the
+ * reduced system's; else 0 (-1: watchdog).  The global log det is NaN when it is
+ * non-zero.  The log det is only known after the reduced solve, so it is an
+ * output of serinv_ppobtasi (SURVEY 8(b)'s sketch had it on ppobtaf).
  */
 typedef struct {
   int P, rank;
   int64_t n_global, start, count;
 } serinv_part_t;
 
-int serinv_exchange_bytes(int64_t b, int64_t a, size_t *bytes);
-int serinv_ppobtaf_ws(const serinv_part_t *part, int64_t b, int64_t a, size_t *bytes);
-int serinv_ppobtaf(serinv_handle_t h, const serinv_part_t *part, const serinv_bta_t *A_local,
-                   void *d_ws, size_t ws_bytes, void *d_sendbuf, int *d_info, void *stream);
-int serinv_ppobtasi(serinv_handle_t h, const serinv_part_t *part, const serinv_bta_t *L_local,
-                    void *d_ws, size_t ws_bytes, const void *d_recvbuf, int *d_info,
-                    double *d_logdet, void *stream);
+int serinv_ppobtaf_ws(const serinv_part_t *part, int Q, int64_t b, int64_t a, size_t *bytes);
+int serinv_ppobtaf(serinv_handle_t h, serinv_comm_t comm, const serinv_part_t *part, int Q,
+                   const serinv_bta_t *A_local, void *d_ws, size_t ws_bytes, int *d_info, void *stream);
+int serinv_ppobtasi(serinv_handle_t h, serinv_comm_t comm, const serinv_part_t *part, int Q,
+                    const serinv_bta_t *L_local, void *d_ws, size_t ws_bytes, int *d_info, double *d_logdet,
+                    void *stream);
 
 /*
- * Hierarchical variant: intra-GPU partitioning of each rank's blocks (SURVEY
- * §8(f) f1 applied per rank; nested solving of the reduced system, PAPER.md
- * Sec. 4.2).  Rank p splits its blocks [start, start+count) into Q
- * consecutive sub-partitions (even sizes, remainder to the earliest; each needs
- * >= 2 blocks, count >= 2Q), so the whole matrix has P*Q partitions, rank p
- * owning partitions [pQ, (p+1)Q).  Q must be the same on every rank.
- *   serinv_ppobtaf_q   factors the Q sub-partitions (one launch) and packs Q
- *                      exchange records (Q * serinv_exchange_bytes bytes in
- *                      d_sendbuf; the rank's partial log det in the first).
- *   (caller)           all-gather of the P send buffers (rank order) into
- *                      d_recvbuf: P * Q records in global partition order.
- *   serinv_ppobtasi_q  assembles the reduced system (2PQ-2 blocks with the
- *                      twisted last partition, reading R14), solves it
- *                      redundantly -- by the nested partitioned algorithm when
- *                      long (serinv_auto_partitions), else as one chain --
- *                      then the backward pass of the Q sub-partitions.
- * Q = 1 is exactly serinv_ppobtaf / serinv_ppobtasi.  Errors as above, plus
- * SERINV_ERR_PLAN if Q < 1 or count < 2Q (Q > 1).  d_ws from
- * serinv_ppobtaf_q_ws(part, Q, ...), passed unchanged between the two calls.
- * serinv_dist_auto_q: the library's default Q for a rank of `count` blocks of
- * size b (the first level of serinv_auto_partitions(count, b)); >= 1, or a
- * negative status.
+ * The same two phases with the exchange left to the caller (any transport):
+ *   serinv_ppobtaf_q   factors and packs the Q records into d_sendbuf
+ *                      (Q * serinv_exchange_bytes bytes);
+ *   (caller)           all-gather of the P send buffers, rank order, into
+ *                      d_recvbuf (P * Q records);
+ *   serinv_ppobtasi_q  as serinv_ppobtasi, reading d_recvbuf.
+ * d_ws: serinv_ppobtaf_q_ws bytes, passed unchanged between the two calls.
+ * serinv_dist_auto_q: the library's default Q for a rank of `count` blocks of size
+ * b (>= 1), or a negative status.  Errors as above, plus SERINV_ERR_PLAN if
+ * Q < 1 or count < 2Q (Q > 1).
  */
+int serinv_exchange_bytes(int64_t b, int64_t a, size_t *bytes);
 int serinv_ppobtaf_q_ws(const serinv_part_t *part, int Q, int64_t b, int64_t a, size_t *bytes);
 int serinv_ppobtaf_q(serinv_handle_t h, const serinv_part_t *part, int Q, const serinv_bta_t *A_local,
                      void *d_ws, size_t ws_bytes, void *d_sendbuf, int *d_info, void *stream);

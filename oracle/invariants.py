@@ -76,14 +76,24 @@ def llt_residual(L, A, blocks=None) -> float:
     return worst
 
 
-def xa_residual(X, A, blocks=None) -> float:
+def xa_residual(X, A, blocks=None, scale=None, tip=None) -> float:
     """max abs residual of (XA) - I on diagonal blocks, arrow row and tip,
-    normalised by ||X_blk|| ||A_blk|| scale (max over checked blocks)."""
+    normalised by max|A_diag| * max|X_diag| (the scaled residual |XA - I| / (|A| |X|),
+    so it is invariant under A -> cA; max over checked blocks).
+
+    blocks: the block rows to check (default all); tip: also check the tip row
+    (default: only when all blocks are checked); scale: the normalisation, for
+    callers that pass lazily loaded blocks (X[k][i] / A[k][i] are only indexed)."""
     n, b = A["diag"].shape[0], A["diag"].shape[1]
     a = A["tip"].shape[0]
     worst = 0.0
     idx = range(n) if blocks is None else blocks
-    scale = max(np.abs(A["diag"]).max(), 1.0) * max(np.abs(X["diag"]).max(), 1.0)
+    if scale is None:
+        scale = float(np.abs(A["diag"]).max()) * float(np.abs(X["diag"]).max())
+        if not scale > 0.0:
+            scale = 1.0
+    if tip is None:
+        tip = blocks is None
     for i in idx:
         R = X["diag"][i] @ A["diag"][i]
         if i > 0:
@@ -100,7 +110,7 @@ def xa_residual(X, A, blocks=None) -> float:
             if i + 1 < n:
                 R = R + X["arrow"][i + 1] @ A["lower"][i]
             worst = max(worst, float(np.abs(R).max()) / scale)
-    if a and blocks is None:
+    if a and tip:
         R = X["tip"] @ A["tip"]
         for i in range(n):
             R = R + X["arrow"][i] @ A["arrow"][i].T

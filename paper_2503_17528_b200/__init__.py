@@ -15,14 +15,14 @@ compute call requires the CUDA library and a device.
 from __future__ import annotations
 
 import ctypes
-import math
+import threading
 
 from . import _lib
 from ._lib import BTA, GraphStats, Part
 
 __all__ = ["Handle", "pobtaf", "pobtasi", "selinv", "selinv_host", "pselinv", "plan", "version",
            "NotPositiveDefinite", "SerinvError", "ppobtaf", "ppobtasi", "exchange_bytes",
-           "graph_stats", "default_handle", "auto_partitions"]
+           "graph_stats", "default_handle", "auto_partitions", "pselinv_plan", "plan_ends", "Comm"]
 
 
 class SerinvError(RuntimeError):
@@ -98,15 +98,20 @@ class Handle:
         return v.value
 
 
-_default = {}
+_default = threading.local()
 
 
 def default_handle(device: int | None = None) -> Handle:
+    """The calling thread's handle for `device` (one per thread and device: its
+    workspace, info and log det buffers are not shared between threads)."""
     import torch
     d = torch.cuda.current_device() if device is None else int(device)
-    h = _default.get(d)
+    hs = getattr(_default, "handles", None)
+    if hs is None:
+        hs = _default.handles = {}
+    h = hs.get(d)
     if h is None:
-        h = _default[d] = Handle(d)
+        h = hs[d] = Handle(d)
     return h
 
 
@@ -226,9 +231,19 @@ def selinv_host(A_host, D, X_host=None, *, handle: Handle | None = None, check: 
 
 
 def plan(n: int, P: int, r: float = 1.0):
-    """Partition plan (reading R6): [(start, end)] for ranks 0..P-1."""
+    """The paper's partition plan (reading R6, Fig. 2): [(start, end)] for ranks 0..P-1.
+    The partitioned solvers use pselinv_plan (the twisted scheme by default)."""
     starts = (ctypes.c_int64 * (P + 1))()
     _check(_lib.lib().serinv_plan(n, P, float(r), starts), "serinv_plan")
+    return [(starts[p], starts[p + 1]) for p in range(P)]
+
+
+def pselinv_plan(n: int, P: int, r: float = 1.0):
+    """The partition plan pselinv / pselinv_nested actually use (serinv_pselinv_plan):
+    plan_ends with the twisted last partition (default), plan with
+    SERINV_OPT=twist_last=0.  [(start, end)]."""
+    starts = (ctypes.c_int64 * (P + 1))()
+    _check(_lib.lib().serinv_pselinv_plan(n, P, float(r), starts), "serinv_pselinv_plan")
     return [(starts[p], starts[p + 1]) for p in range(P)]
 
 
@@ -291,5 +306,5 @@ def graph_stats(kind: int, n: int, b: int, a: int, P=1, r: float = 1.0, handle: 
     return dict(tasks=st.tasks, counters=st.counters, flops=st.flops, grid=st.grid, tile=st.tile)
 
 
-from .distributed import ppobtaf, ppobtasi  # noqa: E402,F401
+from .distributed import Comm, ppobtaf, ppobtasi  # noqa: E402,F401
 from . import distributed  # noqa: E402,F401

@@ -64,11 +64,15 @@ def lib():
     L.serinv_graph_stats_nested.argtypes = [c_p, c_i64, c_i64, c_i64, ctypes.c_int, ip, ctypes.c_double,
                                             ctypes.POINTER(GraphStats)]
     L.serinv_exchange_bytes.argtypes = [c_i64, c_i64, sz]
-    L.serinv_ppobtaf_ws.argtypes = [ctypes.POINTER(Part), c_i64, c_i64, sz]
-    L.serinv_ppobtaf.argtypes = [c_p, ctypes.POINTER(Part), ctypes.POINTER(BTA), c_p, ctypes.c_size_t,
-                                 c_p, c_p, c_p]
-    L.serinv_ppobtasi.argtypes = [c_p, ctypes.POINTER(Part), ctypes.POINTER(BTA), c_p, ctypes.c_size_t,
-                                  c_p, c_p, c_p, c_p]
+    L.serinv_ppobtaf_ws.argtypes = [ctypes.POINTER(Part), ctypes.c_int, c_i64, c_i64, sz]
+    L.serinv_ppobtaf.argtypes = [c_p, c_p, ctypes.POINTER(Part), ctypes.c_int, ctypes.POINTER(BTA), c_p,
+                                 ctypes.c_size_t, c_p, c_p]
+    L.serinv_ppobtasi.argtypes = [c_p, c_p, ctypes.POINTER(Part), ctypes.c_int, ctypes.POINTER(BTA), c_p,
+                                  ctypes.c_size_t, c_p, c_p, c_p]
+    L.serinv_nccl_unique_id.argtypes = [c_p]
+    L.serinv_comm_init.argtypes = [ctypes.POINTER(c_p), c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    L.serinv_comm_destroy.argtypes = [c_p]
+    L.serinv_pselinv_plan.argtypes = [c_i64, ctypes.c_int, ctypes.c_double, ctypes.POINTER(c_i64)]
     L.serinv_ppobtaf_q_ws.argtypes = [ctypes.POINTER(Part), ctypes.c_int, c_i64, c_i64, sz]
     L.serinv_ppobtaf_q.argtypes = [c_p, ctypes.POINTER(Part), ctypes.c_int, ctypes.POINTER(BTA), c_p,
                                    ctypes.c_size_t, c_p, c_p, c_p]
@@ -94,4 +98,5 @@ EXPORTED = [
     "serinv_ppobtaf", "serinv_ppobtasi", "serinv_graph_stats", "serinv_last_launches", "serinv_set_trace", "serinv_selinv_host", "serinv_bench_gemm",
     "serinv_auto_partitions", "serinv_pselinv_nested_ws", "serinv_pselinv_nested", "serinv_graph_stats_nested",
     "serinv_ppobtaf_q_ws", "serinv_ppobtaf_q", "serinv_ppobtasi_q", "serinv_dist_auto_q",
+    "serinv_nccl_unique_id", "serinv_comm_init", "serinv_comm_destroy", "serinv_pselinv_plan",
 ]

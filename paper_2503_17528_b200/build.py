@@ -15,13 +15,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libserinv.so")
-SOURCES = ["exec.cu", "serinv.cu", "graph.cpp"]
-HEADERS = ["exec.h", "graph.h", "task.h"]
+SOURCES = ["exec.cu", "serinv.cu", "graph.cpp", "comm.cpp"]
+HEADERS = ["exec.h", "graph.h", "task.h", "dist_meta.h", "comm.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O2", "-shared",
+    "-Xcompiler", "-fPIC,-O2", "-shared", "-ldl",
 ]
 
 

@@ -1042,7 +1042,6 @@ __device__ __forceinline__ void leaf_chol16(double *St, double *Wt, double *dv, 
   }
   if (h == (j >> 3) && c0 + j < m) {
     dv[c0 + j] = dj;
-    if (!(dj > 0.0)) atomicMin(s_bad, c0 + j);
   }
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
@@ -1273,7 +1272,7 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   double *lb = S2 + SERINV_TILE * LDT;    // [4][64] published pivot columns
   double *rsv = lb + 4 * SERINV_TILE;     // [64] 1 / L_jj
   double *dv = rsv + SERINV_TILE;         // [64] pivots
-  __shared__ int s_bad;
+  __shared__ int s_bad, s_nan;  // first genuine / NaN-pivot failure in the tile
   const bool trsm2 = factor && (T.flags & TF_TRSM2);
   double acc2[2][4][2];
   if (factor && (T.flags & TF_CARRY)) {
@@ -1295,14 +1294,12 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   }
   for (int idx = tid; idx < SERINV_TILE * LDT; idx += NT) Wt[idx] = 0.0;
   if (tid < SERINV_TILE) rsv[tid] = 0.0;
-  if (tid == 0) s_bad = 1 << 30;
+  if (tid == 0) s_bad = s_nan = 1 << 30;
   __syncthreads();
   phase_mark(p, tsk, 0);
   const bool chol8 = factor && (T.flags & TF_CHOL8);
   if (chol8) {
     chol8_pipelined(St, Wt, S2, dv, m);
-    if (tid < m && !(dv[tid] > 0.0)) atomicMin(&s_bad, tid);
-    __syncthreads();
   } else if (factor) {
     // Left-looking over 16-column blocks.  Per block: (1) DMMA update of the
     // block columns from the finished columns to the left, (2) one warp factors
@@ -1372,8 +1369,13 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
     if (tid < m) {
       const double d = St[tid * LDT + tid];
       rsv[tid] = 1.0 / d;
-      if (!(d != 0.0) || !isfinite(d)) atomicMin(&s_bad, tid);
+      if (!(d != 0.0) || !isfinite(d)) atomicMin(isnan(d) ? &s_nan : &s_bad, tid);
     }
+  }
+  __syncthreads();
+  if (factor && tid < m) {  // pivots (before the square root) of either factorisation path
+    const double d = dv[tid];
+    if (!(d > 0.0)) atomicMin(isnan(d) ? &s_nan : &s_bad, tid);
   }
   __syncthreads();
   phase_mark(p, tsk, 1);
@@ -1425,6 +1427,7 @@ __device__ void run_potrf_trtri(const Params &p, const Task &T, double *smem, bo
   }
   phase_mark(p, tsk, 2);
   if (tid == 0 && s_bad < (1 << 30)) record_info(p.info, T.aux1 + s_bad + 1);
+  if (tid == 0 && s_nan < (1 << 30)) record_info(p.info2, T.aux1 + s_nan + 1);
   const bool early = factor && (T.flags & TF_EARLY_SIG) && (T.flags & TF_W_OUT);
   if (early) {
     // W = L^{-1} is what the chain's next TRSM waits for: store it and publish the
@@ -1613,7 +1616,7 @@ __device__ void run_logdet(const Params &p, const Task &T, double *smem) {
       const double *ex = lptr(p, T.c0);
       for (int j = 0; j < T.aux1; ++j) v += __ldcg(ex + T.aux2 * j);
     }
-    int inf = *(volatile int *)p.info;
+    const int inf = *(volatile int *)p.info | *(volatile int *)p.info2;
     *lptr(p, T.out) = inf ? __longlong_as_double(0x7ff8000000000000ULL) : v;
   }
 }

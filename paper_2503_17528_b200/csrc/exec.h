@@ -20,7 +20,8 @@ struct Params {
   int nurgent;           // CTAs serving the urgent queue
   int ntasks;
   double *bufs[BUF_COUNT];
-  int *info;
+  int *info;             // first genuine failure (finite pivot <= 0 / zero diagonal), dpotrf row
+  int *info2;            // failures with a NaN pivot (propagated, or NaN input): merged after the launch
   unsigned long long *trace;  // optional: 4 x u64 per task {claim, start, end, meta}
 };
 }  // namespace dev

@@ -15,6 +15,7 @@
 //            the in-process partitioned pipeline (Alg. 3-6 + Sec. 3.3) and the
 //            per-rank distributed graphs.
 #include "graph.h"
+#include "dist_meta.h"
 
 #include <algorithm>
 #include <cassert>
@@ -1668,7 +1669,7 @@ void assemble_reduced(Ctx &cx, const View &V0, int P, int64_t b, int64_t a, int3
   const int64_t tip_row = V0.tip_row;
   std::vector<int64_t> st = starts;
   R.V = View{R.D, R.Lo, R.Ar,
-             [st, vrow, tip_row](int64_t i) -> int64_t {
+             [st, vrow, b](int64_t i) -> int64_t {
                int64_t blk;
                if (i == 0)
                  blk = st[1] - 1;
@@ -1676,7 +1677,9 @@ void assemble_reduced(Ctx &cx, const View &V0, int P, int64_t b, int64_t a, int3
                  int p = (int)((i + 1) / 2);
                  blk = (i & 1) ? st[p] : st[p + 1] - 1;
                }
-               return blk >= 0 ? vrow(blk) : tip_row;
+               // a partition start this rank does not know (distributed): encoded, decoded
+               // after the solve from the records' meta (dist_meta.h)
+               return blk >= 0 ? vrow(blk) : (int64_t)kEncRow + i * b;
              },
              tip_row};
   R.ready = ready;
@@ -1970,7 +1973,16 @@ bool plan_partitions_ends(int64_t n, int P, double r, std::vector<int64_t> &star
   return s + end == n;
 }
 
-int64_t exchange_doubles(int64_t b, int64_t a) { return (4 * b * b + 2 * a * b + a * a + 1 + 31) / 32 * 32; }
+bool plan_partitions_for(int64_t n, int P, double r, bool twist_last, std::vector<int64_t> &starts) {
+  return twist_last ? plan_partitions_ends(n, P, r, starts) : plan_partitions(n, P, r, starts);
+}
+
+int64_t exchange_meta_offset(int64_t b, int64_t a) { return 4 * b * b + 2 * a * b + a * a; }
+
+// record = boundary blocks + U_p + the dist_meta.h tail (log det partial, info, s, e), padded to 32 doubles
+int64_t exchange_doubles(int64_t b, int64_t a) {
+  return (4 * b * b + 2 * a * b + a * a + kMetaDoubles + 31) / 32 * 32;
+}
 
 // One level of the (nested) partitioned solve of the BTA matrix V (n blocks, tip
 // in BUF_TIP): PPOBTAF on Ps[lvl] partitions, A_r (2P-1 blocks) assembled, then
@@ -1981,7 +1993,7 @@ bool psolve_level(Ctx &cx, const View &V, int64_t n, int64_t b, int64_t a, const
                   double r, const std::vector<int32_t> &inw) {
   const int P = Ps[lvl];
   std::vector<int64_t> starts;
-  const bool ok = cx.opt.twist_last ? plan_partitions_ends(n, P, r, starts) : plan_partitions(n, P, r, starts);
+  const bool ok = plan_partitions_for(n, P, r, cx.opt.twist_last, starts);
   if (P < 1 || (lvl > 0 && P < 2) || !ok) return false;
   const int64_t recsz = exchange_doubles(b, a);
   const int64_t recs = cx.alloc(recsz * P);
@@ -2017,7 +2029,7 @@ bool psolve_level(Ctx &cx, const View &V, int64_t n, int64_t b, int64_t a, const
 
 Graph build_pselinv(int64_t n, int64_t b, int64_t a, const std::vector<int> &Ps, double r, const BuildOptions &opt) {
   std::vector<int64_t> starts;
-  if (Ps.empty() || !plan_partitions(n, Ps[0], r, starts)) {
+  if (Ps.empty() || !plan_partitions_for(n, Ps[0], r, opt.twist_last, starts)) {
     Graph bad;
     bad.error = "infeasible plan";
     return bad;

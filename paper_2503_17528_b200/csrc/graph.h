@@ -142,6 +142,8 @@ Graph build_distributed(int phase, int P, int rank, int64_t n_global, int64_t st
 int64_t distributed_ws_bytes(int P, int rank, int64_t n_global, int64_t start, int64_t count,
                              int64_t b, int64_t a, int Q = 1);
 int64_t exchange_doubles(int64_t b, int64_t a);
+// offset of the record's meta tail (dist_meta.h: log det partial, info, s, e)
+int64_t exchange_meta_offset(int64_t b, int64_t a);
 
 // Diagnostic: independent tile GEMMs (engine throughput).
 Graph build_gemm_bench(int ntasks, int k, int nseg, const BuildOptions &opt);
@@ -154,6 +156,9 @@ int reduced_size(int P, bool twisted_last);
 bool plan_partitions(int64_t n, int P, double r, std::vector<int64_t> &starts);
 // Twisted-scheme plan (reading R14): first and last partition r x a middle one.
 bool plan_partitions_ends(int64_t n, int P, double r, std::vector<int64_t> &starts);
+// The plan the partitioned solvers actually use: plan_partitions_ends with the
+// twisted last partition (default), else the paper's plan_partitions.
+bool plan_partitions_for(int64_t n, int P, double r, bool twist_last, std::vector<int64_t> &starts);
 
 // Bytes reserved at the end of the workspace for counters (+1 claim counter).
 int64_t counter_bytes(int32_t nctr);

@@ -18,6 +18,8 @@
 #include <vector>
 
 #include "../../include/serinv.h"
+#include "comm.h"
+#include "dist_meta.h"
 #include "graph.h"
 #include "task.h"
 
@@ -48,6 +50,12 @@ struct DevGraph {
 };
 
 typedef std::tuple<int, int64_t, int64_t, int64_t, int, int64_t, int, int64_t, int64_t> GKey;
+// graphs and workspace layouts depend on the build options (SERINV_OPT): part of every cache key
+typedef std::pair<GKey, std::string> CKey;
+inline std::string opt_string() {
+  const char *e = getenv("SERINV_OPT");
+  return e ? std::string(e) : std::string();
+}
 
 }  // namespace
 
@@ -63,13 +71,36 @@ struct serinv_ctx {
   size_t trace_cap = 0;                 // records
   cudaStream_t s_in = nullptr, s_out = nullptr;  // streaming host IO copy streams
   cudaEvent_t ev_start = nullptr, ev_in = nullptr, ev_out = nullptr;
-  std::map<GKey, std::unique_ptr<DevGraph>> cache;
+  std::map<CKey, std::unique_ptr<DevGraph>> cache;
   std::mutex mu;
+  // A handle's calls execute in call order, whatever streams they are enqueued on:
+  // every call waits for the previous call's device work (ev_last) and the whole
+  // enqueue sequence is one critical section.  The cached graphs' dependency
+  // counters are reset by each call, so two calls must never overlap on the device.
+  std::recursive_mutex call_mu;
+  cudaEvent_t ev_last = nullptr;
+  int depth = 0;
 };
 
 namespace {
 
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+// One API call's critical section (see serinv_ctx::call_mu); nests.
+struct CallGuard {
+  serinv_handle_t h;
+  cudaStream_t st;
+  std::unique_lock<std::recursive_mutex> lk;
+  CallGuard(serinv_handle_t h_, cudaStream_t st_) : h(h_), st(st_), lk(h_->call_mu) {
+    if (h->depth++ == 0) {
+      h->last_launches = 0;
+      cudaStreamWaitEvent(st, h->ev_last, 0);
+    }
+  }
+  ~CallGuard() {
+    if (--h->depth == 0) cudaEventRecord(h->ev_last, st);
+  }
+};
 
 int upload(DevGraph &dg, int grid) {
   Graph &g = dg.g;
@@ -96,7 +127,7 @@ int upload(DevGraph &dg, int grid) {
   dg.nq = (int)g.qoff.size() - 1;
   dg.ncrit = g.ncrit;
   dg.nurgent = g.nurgent;
-  dg.nctr_alloc = (int64_t)g.nctr + dg.nq + 2 + grid;
+  dg.nctr_alloc = (int64_t)g.nctr + dg.nq + 2 + grid + 1;  // + info2 (exec.h)
   if (cudaMalloc(&dg.ctr, (size_t)dg.nctr_alloc * sizeof(int32_t)) != cudaSuccess) return SERINV_ERR_CUDA;
   dg.ntasks = (int64_t)g.tasks.size();
   dg.nwaits = (int64_t)g.waits.size();
@@ -122,7 +153,8 @@ int get_graph(serinv_handle_t h, const GKey &key, DevGraph **out) {
 }
 int get_graph_impl(serinv_handle_t h, const GKey &key, DevGraph **out) {
   std::lock_guard<std::mutex> lk(h->mu);
-  auto it = h->cache.find(key);
+  const CKey ckey(key, opt_string());
+  auto it = h->cache.find(ckey);
   if (it != h->cache.end()) {
     *out = it->second.get();
     return SERINV_OK;
@@ -161,16 +193,22 @@ int get_graph_impl(serinv_handle_t h, const GKey &key, DevGraph **out) {
   int rc = upload(*dg, h->grid);
   if (rc) return rc;
   *out = dg.get();
-  h->cache[key] = std::move(dg);
+  h->cache[ckey] = std::move(dg);
   return SERINV_OK;
 }
 
+__global__ void info_merge_kernel(int *info, const int *info2) {
+  if (threadIdx.x == 0 && *info == 0) *info = *info2;
+}
+
+// reset: clear the graph's counters (and *d_info unless keep_info) before the kernel
 int launch(serinv_handle_t h, DevGraph &dg, double *bufs[BUF_COUNT], int *d_info, cudaStream_t st,
-           bool reset = true) {
+           bool reset = true, bool keep_info = false) {
+  CallGuard guard(h, st);
   if (reset) {
     if (cudaMemsetAsync(dg.ctr, 0, (size_t)dg.nctr_alloc * sizeof(int32_t), st) != cudaSuccess)
       return SERINV_ERR_CUDA;
-    if (cudaMemsetAsync(d_info, 0, sizeof(int), st) != cudaSuccess) return SERINV_ERR_CUDA;
+    if (!keep_info && cudaMemsetAsync(d_info, 0, sizeof(int), st) != cudaSuccess) return SERINV_ERR_CUDA;
   }
   dev::Params p;
   p.tasks = dg.d_tasks;
@@ -187,9 +225,12 @@ int launch(serinv_handle_t h, DevGraph &dg, double *bufs[BUF_COUNT], int *d_info
   p.ntasks = (int)dg.ntasks;
   for (int i = 0; i < BUF_COUNT; ++i) p.bufs[i] = bufs[i];
   p.info = d_info;
+  p.info2 = dg.ctr + dg.nctr_alloc - 1;
   p.trace = (h->trace && (size_t)dg.ntasks <= h->trace_cap) ? h->trace : nullptr;
   serinv_exec_kernel<<<h->grid, 256, h->smem, st>>>(p);
-  h->last_launches = 1;
+  // failures with a NaN pivot count only if there was no genuine one (exec.h)
+  info_merge_kernel<<<1, 32, 0, st>>>(d_info, p.info2);
+  h->last_launches += 2;
   return cudaGetLastError() == cudaSuccess ? SERINV_OK : SERINV_ERR_CUDA;
 }
 
@@ -262,6 +303,7 @@ int serinv_create(serinv_handle_t *h, int cuda_device) {
   c->grid = c->sms * per_sm;
   if (cudaMalloc(&c->dummy, 256) != cudaSuccess) return SERINV_ERR_CUDA;
   c->dummy_info = (int *)(c->dummy + 16);
+  if (cudaEventCreateWithFlags(&c->ev_last, cudaEventDisableTiming) != cudaSuccess) return SERINV_ERR_CUDA;
   *h = c.release();
   return SERINV_OK;
 }
@@ -277,6 +319,7 @@ int serinv_destroy(serinv_handle_t h) {
   if (h->ev_start) cudaEventDestroy(h->ev_start);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
+  if (h->ev_last) cudaEventDestroy(h->ev_last);
   delete h;
   return SERINV_OK;
 }
@@ -339,6 +382,15 @@ int serinv_plan(int64_t n, int P, double r, int64_t *starts) {
   return SERINV_OK;
 }
 
+int serinv_pselinv_plan(int64_t n, int P, double r, int64_t *starts) {
+  if (!starts) return -4;
+  if (!(r > 0.0) || !std::isfinite(r)) return -3;
+  std::vector<int64_t> s;
+  if (!plan_partitions_for(n, P, r, env_opt().twist_last, s)) return SERINV_ERR_PLAN;
+  for (size_t i = 0; i < s.size(); ++i) starts[i] = s[i];
+  return SERINV_OK;
+}
+
 int serinv_plan_ends(int64_t n, int P, double r, int64_t *starts) {
   if (!starts) return -4;
   if (!(r > 0.0) || !std::isfinite(r)) return -3;
@@ -350,19 +402,21 @@ int serinv_plan_ends(int64_t n, int P, double r, int64_t *starts) {
 
 // workspace queries of the partitioned graphs build the graph: memoise them
 static std::mutex g_ws_mu;
-static std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int64_t, int, int64_t, int64_t>, int64_t> g_ws_cache;
+static std::map<CKey, int64_t> g_ws_cache;
 
 int serinv_pselinv_ws(int64_t n, int64_t b, int64_t a, int P, double r, size_t *bytes) {
   if (!bytes) return -6;
   if (n < 1 || b < 1 || a < 0) return SERINV_ERR_SHAPE;
   std::vector<int64_t> s;
-  if (!plan_partitions(n, P, r, s)) return SERINV_ERR_PLAN;
+  if (!(r > 0.0) || !std::isfinite(r) || !plan_partitions_for(n, P, r, env_opt().twist_last, s))
+    return SERINV_ERR_PLAN;
   int64_t rb;
   memcpy(&rb, &r, 8);
   auto key = std::make_tuple(3, n, b, a, P, rb, 0, (int64_t)0, (int64_t)0);
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  auto it = g_ws_cache.find(key);
-  int64_t v = it != g_ws_cache.end() ? it->second : (g_ws_cache[key] = pselinv_ws_bytes(n, b, a, P, r));
+  const CKey ckey(key, opt_string());
+  auto it = g_ws_cache.find(ckey);
+  int64_t v = it != g_ws_cache.end() ? it->second : (g_ws_cache[ckey] = pselinv_ws_bytes(n, b, a, P, r));
   if (v < 0) return SERINV_ERR_SHAPE;
   *bytes = (size_t)v;
   return SERINV_OK;
@@ -376,7 +430,8 @@ int serinv_pselinv(serinv_handle_t h, const serinv_bta_t *A, int P, double r, vo
   if (!d_info) return -7;
   if (!d_ws || !aligned16(d_ws)) return SERINV_ERR_WS;
   std::vector<int64_t> s;
-  if (!plan_partitions(A->n, P, r, s)) return SERINV_ERR_PLAN;
+  if (!(r > 0.0) || !std::isfinite(r) || !plan_partitions_for(A->n, P, r, env_opt().twist_last, s))
+    return SERINV_ERR_PLAN;
   if (P == 1) return run_seq(h, 2, A, d_ws, ws_bytes, d_info, d_logdet, stream);
   if (cudaSetDevice(h->device) != cudaSuccess) return SERINV_ERR_CUDA;
   int64_t rb;
@@ -399,7 +454,7 @@ static int nested_key(int64_t n, int nlev, const int *Ps, double r, int64_t *mor
   opt.apply_env();
   for (int l = 0; l < nlev; ++l) {
     std::vector<int64_t> s;
-    if (Ps[l] < 1 || Ps[l] > 0xffff || (l > 0 && Ps[l] < 2) || !plan_partitions(m, Ps[l], r, s))
+    if (Ps[l] < 1 || Ps[l] > 0xffff || (l > 0 && Ps[l] < 2) || !plan_partitions_for(m, Ps[l], r, opt.twist_last, s))
       return SERINV_ERR_PLAN;
     if (l > 0) *more |= (int64_t)Ps[l] << (16 * (l - 1));
     m = reduced_size(Ps[l], opt.twist_last);
@@ -427,9 +482,11 @@ int serinv_pselinv_nested_ws(int64_t n, int64_t b, int64_t a, int nlev, const in
   memcpy(&rb, &r, 8);
   auto key = std::make_tuple(3, n, b, a, Ps[0], rb, 0, more, (int64_t)nlev);
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  auto it = g_ws_cache.find(key);
-  int64_t v = it != g_ws_cache.end() ? it->second
-                                     : (g_ws_cache[key] = pselinv_ws_bytes(n, b, a, std::vector<int>(Ps, Ps + nlev), r));
+  const CKey ckey(key, opt_string());
+  auto it = g_ws_cache.find(ckey);
+  int64_t v = it != g_ws_cache.end()
+                  ? it->second
+                  : (g_ws_cache[ckey] = pselinv_ws_bytes(n, b, a, std::vector<int>(Ps, Ps + nlev), r));
   if (v < 0) return SERINV_ERR_SHAPE;
   *bytes = (size_t)v;
   return SERINV_OK;
@@ -483,18 +540,15 @@ int serinv_ppobtaf_q_ws(const serinv_part_t *part, int Q, int64_t b, int64_t a, 
   if (b < 1 || a < 0) return SERINV_ERR_SHAPE;
   auto key = std::make_tuple(4, part->n_global, b, a, part->P, (int64_t)Q, part->rank, part->start, part->count);
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  auto it = g_ws_cache.find(key);
+  const CKey ckey(key, opt_string());
+  auto it = g_ws_cache.find(ckey);
   int64_t v = it != g_ws_cache.end()
                   ? it->second
-                  : (g_ws_cache[key] = distributed_ws_bytes(part->P, part->rank, part->n_global, part->start,
+                  : (g_ws_cache[ckey] = distributed_ws_bytes(part->P, part->rank, part->n_global, part->start,
                                                             part->count, b, a, Q));
   if (v < 0) return SERINV_ERR_SHAPE;
   *bytes = (size_t)v;
   return SERINV_OK;
-}
-
-int serinv_ppobtaf_ws(const serinv_part_t *part, int64_t b, int64_t a, size_t *bytes) {
-  return serinv_ppobtaf_q_ws(part, 1, b, a, bytes);
 }
 
 int serinv_dist_auto_q(int64_t count, int64_t b) {
@@ -509,6 +563,27 @@ int serinv_dist_auto_q(int64_t count, int64_t b) {
   while (Q > 1 && count < 2 * (int64_t)Q) --Q;
   return Q;
 }
+
+}  // extern "C"
+
+namespace {
+// Status handling of the distributed path (dist_meta.h): PPOBTAF's info and the
+// partition's [s, e) go into the rank's records before the exchange; PPOBTASI
+// starts from the smallest row any rank reported and decodes reduced-system rows
+// of other ranks' partitions afterwards -- every rank ends with the same status.
+__global__ void dist_meta_kernel(double *send, int Q, int64_t recsz, int64_t mo, const int *info, int64_t start,
+                                 int64_t count) {
+  const int v = *(volatile const int *)info;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Q; q += gridDim.x * blockDim.x)
+    meta_write(send, Q, recsz, mo, v, start, count, q);
+}
+__global__ void dist_combine_kernel(const double *recv, int nrec, int64_t recsz, int64_t mo, int *info) {
+  if (threadIdx.x == 0) *info = meta_combine_info(recv, nrec, recsz, mo);
+}
+__global__ void dist_final_kernel(const double *recv, int nrec, int64_t recsz, int64_t mo, int64_t b, int *info) {
+  if (threadIdx.x == 0) *info = meta_final_info(*info, recv, nrec, recsz, mo, b);
+}
+}  // namespace
 
 static int run_dist(serinv_handle_t h, int phase, const serinv_part_t *part, int Q, const serinv_bta_t *A,
                     void *d_ws, size_t ws_bytes, void *ext0, const void *ext1, int *d_info, double *d_logdet,
@@ -531,8 +606,29 @@ static int run_dist(serinv_handle_t h, int phase, const serinv_part_t *part, int
   if ((int64_t)ws_bytes < dg->g.ws_doubles * 8) return SERINV_ERR_WS;
   double *bufs[BUF_COUNT] = {A->diag, A->lower, A->arrow, A->tip, (double *)d_ws, (double *)ext0,
                              (double *)ext1, d_logdet ? d_logdet : h->dummy};
-  return launch(h, *dg, bufs, d_info, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  CallGuard guard(h, st);
+  const int64_t recsz = exchange_doubles(A->b, A->a), mo = exchange_meta_offset(A->b, A->a);
+  if (phase == 0) {
+    rc = launch(h, *dg, bufs, d_info, st);
+    if (rc) return rc;
+    dist_meta_kernel<<<(Q + 127) / 128, 128, 0, st>>>((double *)ext0, Q, recsz, mo, d_info, part->start,
+                                                      part->count);
+    h->last_launches += 1;
+    return cudaGetLastError() == cudaSuccess ? SERINV_OK : SERINV_ERR_CUDA;
+  }
+  dist_combine_kernel<<<1, 32, 0, st>>>((const double *)ext1, part->P * Q, recsz, mo, d_info);
+  rc = launch(h, *dg, bufs, d_info, st, true, /*keep_info=*/true);
+  if (rc) return rc;
+  dist_final_kernel<<<1, 32, 0, st>>>((const double *)ext1, part->P * Q, recsz, mo, A->b, d_info);
+  h->last_launches += 2;
+  return cudaGetLastError() == cudaSuccess ? SERINV_OK : SERINV_ERR_CUDA;
 }
+
+// comm entry points: workspace = graph workspace | send records | recv records
+static int64_t up256(int64_t x) { return (x + 255) / 256 * 256; }
+
+extern "C" {
 
 int serinv_ppobtaf_q(serinv_handle_t h, const serinv_part_t *part, int Q, const serinv_bta_t *A_local, void *d_ws,
                      size_t ws_bytes, void *d_sendbuf, int *d_info, void *stream) {
@@ -546,16 +642,57 @@ int serinv_ppobtasi_q(serinv_handle_t h, const serinv_part_t *part, int Q, const
   return run_dist(h, 1, part, Q, L_local, d_ws, ws_bytes, nullptr, d_recvbuf, d_info, d_logdet, stream);
 }
 
-int serinv_ppobtaf(serinv_handle_t h, const serinv_part_t *part, const serinv_bta_t *A_local, void *d_ws,
-                   size_t ws_bytes, void *d_sendbuf, int *d_info, void *stream) {
-  if (!d_sendbuf) return -6;
-  return run_dist(h, 0, part, 1, A_local, d_ws, ws_bytes, d_sendbuf, nullptr, d_info, nullptr, stream);
+int serinv_ppobtaf_ws(const serinv_part_t *part, int Q, int64_t b, int64_t a, size_t *bytes) {
+  if (!bytes) return -5;
+  size_t g = 0;
+  int rc = serinv_ppobtaf_q_ws(part, Q, b, a, &g);
+  if (rc) return rc;
+  const int64_t rec = exchange_doubles(b, a) * 8;
+  *bytes = (size_t)(up256((int64_t)g) + up256((int64_t)Q * rec) + up256((int64_t)part->P * Q * rec));
+  return SERINV_OK;
 }
 
-int serinv_ppobtasi(serinv_handle_t h, const serinv_part_t *part, const serinv_bta_t *L_local, void *d_ws,
-                    size_t ws_bytes, const void *d_recvbuf, int *d_info, double *d_logdet, void *stream) {
-  if (!d_recvbuf) return -6;
-  return run_dist(h, 1, part, 1, L_local, d_ws, ws_bytes, nullptr, d_recvbuf, d_info, d_logdet, stream);
+static int comm_split_ws(serinv_comm_t comm, const serinv_part_t *part, int Q, const serinv_bta_t *A, void *d_ws,
+                         size_t ws_bytes, size_t *gbytes, double **send, double **recv) {
+  if (!comm) return -2;
+  if (!part || !A) return -3;
+  if (comm_size(comm) != part->P || comm_rank(comm) != part->rank) return -3;
+  size_t total = 0;
+  int rc = serinv_ppobtaf_ws(part, Q, A->b, A->a, &total);
+  if (rc) return rc;
+  if (!d_ws || ws_bytes < total) return SERINV_ERR_WS;
+  size_t g = 0;
+  serinv_ppobtaf_q_ws(part, Q, A->b, A->a, &g);
+  const int64_t rec = exchange_doubles(A->b, A->a) * 8;
+  *gbytes = (size_t)up256((int64_t)g);
+  *send = (double *)((char *)d_ws + *gbytes);
+  *recv = (double *)((char *)*send + up256((int64_t)Q * rec));
+  return SERINV_OK;
+}
+
+int serinv_ppobtaf(serinv_handle_t h, serinv_comm_t comm, const serinv_part_t *part, int Q,
+                   const serinv_bta_t *A_local, void *d_ws, size_t ws_bytes, int *d_info, void *stream) {
+  if (!h) return SERINV_ERR_HANDLE;
+  size_t g = 0;
+  double *send = nullptr, *recv = nullptr;
+  int rc = comm_split_ws(comm, part, Q, A_local, d_ws, ws_bytes, &g, &send, &recv);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  CallGuard guard(h, st);
+  rc = run_dist(h, 0, part, Q, A_local, d_ws, g, send, nullptr, d_info, nullptr, stream);
+  if (rc) return rc;
+  return comm_allgather_f64(comm, send, recv, (size_t)Q * exchange_doubles(A_local->b, A_local->a), st);
+}
+
+int serinv_ppobtasi(serinv_handle_t h, serinv_comm_t comm, const serinv_part_t *part, int Q,
+                    const serinv_bta_t *L_local, void *d_ws, size_t ws_bytes, int *d_info, double *d_logdet,
+                    void *stream) {
+  if (!h) return SERINV_ERR_HANDLE;
+  size_t g = 0;
+  double *send = nullptr, *recv = nullptr;
+  int rc = comm_split_ws(comm, part, Q, L_local, d_ws, ws_bytes, &g, &send, &recv);
+  if (rc) return rc;
+  return run_dist(h, 1, part, Q, L_local, d_ws, g, nullptr, recv, d_info, d_logdet, stream);
 }
 
 int serinv_graph_stats(serinv_handle_t h, int kind, int64_t n, int64_t b, int64_t a, int P, double r,
@@ -776,6 +913,7 @@ int serinv_selinv_host(serinv_handle_t h, const serinv_bta_t *A_host, const seri
       return SERINV_ERR_CUDA;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  CallGuard guard(h, st);
   if (cudaMemsetAsync(dg->ctr, 0, (size_t)dg->nctr_alloc * sizeof(int32_t), st) != cudaSuccess ||
       cudaMemsetAsync(d_info, 0, sizeof(int), st) != cudaSuccess || cudaEventRecord(h->ev_start, st) != cudaSuccess)
     return SERINV_ERR_CUDA;

@@ -1,22 +1,28 @@
 """Distributed PPOBTAF / PPOBTASI: one process per GPU (Alg. 3-6, Sec. 3.3).
 
-Rank p owns the global blocks [s, e) of `serinv_plan` and passes its LOCAL
+Rank p owns the global blocks [s, e) of a partition plan and passes its LOCAL
 blocks (diag/arrow [count], lower [count] -- the last rank [count-1] -- and the
 replicated tip).  One step:
 
     serinv_ppobtaf   local elimination (no communication) + pack of this rank's
-                     exchange record (boundary blocks, couplings, U_p, log det
-                     partial) into the send buffer
-    all-gather       of the P records (NCCL through torch.distributed; the only
-                     inter-GPU transfer: <= 4b^2 + 2ab + a^2 doubles per rank)
-    serinv_ppobtasi  every rank assembles A_r (2P-1 blocks) in rank order,
-                     solves it redundantly (bit-identical on all ranks), scatters
-                     its true-inverse boundary blocks and runs its backward pass
+                     exchange records (boundary blocks, couplings, U_p, log det
+                     partial, info, partition bounds), then the library's own
+                     all-gather of the P*Q records over its NCCL communicator
+                     (serinv_comm_t; the only inter-GPU transfer)
+    serinv_ppobtasi  every rank assembles A_r in partition order, solves it
+                     redundantly (bit-identical on all ranks), scatters its
+                     true-inverse boundary blocks and runs its backward pass
 
-With Q > 1 every rank splits its blocks into Q sub-partitions (serinv_ppobtaf_q /
-serinv_ppobtasi_q: intra-GPU partitioning of the rank's chain, the reduced
-system of 2PQ-2 blocks solved by the nested algorithm); Q = dist_auto_q(count, b)
-is the library's default, Q = 1 the paper's one partition per process.
+`Comm` wraps serinv_comm_t (NCCL unique id broadcast through torch.distributed);
+`DistContext(..., comm=Comm(...))` uses it.  Without a communicator the context
+uses the transport-agnostic pair serinv_ppobtaf_q / serinv_ppobtasi_q with the
+all-gather done here by torch.distributed (any backend, e.g. gloo with
+host-staged buffers) -- the same records, the same kernels.
+
+Every rank splits its blocks into Q sub-partitions (intra-GPU partitioning of the
+rank's chain, the reduced system of 2PQ-2 blocks solved by the nested
+algorithm); Q = dist_auto_q(count, b) is the library's default, Q = 1 the
+paper's one partition per process.
 
 Argument marshalling + the collective only; all arithmetic is in libserinv.
 """
@@ -51,6 +57,42 @@ def exchange(send, recv, group=None):
     dist.all_gather_into_tensor(recv, send, group=group)
 
 
+class Comm:
+    """The library's NCCL communicator (serinv_nccl_unique_id / serinv_comm_init /
+    serinv_comm_destroy).  Collective: every rank of `group` constructs it; rank 0's
+    unique id is broadcast with torch.distributed.  P == 1 needs no NCCL."""
+
+    def __init__(self, P: int, rank: int, device: int, group=None):
+        L = _lib.lib()
+        self.P, self.rank, self.device = int(P), int(rank), int(device)
+        self._c = ctypes.c_void_p()
+        uid = None
+        if self.P > 1:
+            import torch.distributed as dist
+            buf = (ctypes.c_ubyte * 128)()
+            if self.rank == 0:
+                rc = L.serinv_nccl_unique_id(buf)
+                if rc:
+                    raise RuntimeError(f"serinv_nccl_unique_id failed: {rc}")
+            obj = [bytes(buf)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = (ctypes.c_ubyte * 128).from_buffer_copy(obj[0])
+        rc = L.serinv_comm_init(ctypes.byref(self._c), uid, self.P, self.rank, self.device)
+        if rc:
+            raise RuntimeError(f"serinv_comm_init failed: {rc}")
+
+    def close(self):
+        if self._c:
+            _lib.lib().serinv_comm_destroy(self._c)
+            self._c = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def auto_r(b: int) -> float:
     """Default end-rank ratio for serinv_plan_ends (first / last rank blocks relative to
     a middle rank), measured with tools/scaling_sim.py at P = 8
@@ -73,7 +115,7 @@ class DistContext:
     Q = sub-partitions of this rank's blocks (the same on every rank)."""
 
     def __init__(self, handle, P: int, rank: int, n_global: int, start: int, count: int, b: int, a: int,
-                 device: int = 0, group=None, Q: int = 1):
+                 device: int = 0, group=None, Q: int = 1, comm: Comm | None = None):
         import torch
         L = _lib.lib()
         self.h = handle
@@ -81,17 +123,24 @@ class DistContext:
         self.b, self.a = b, a
         self.Q = int(Q)
         self.group = group
+        self.comm = comm
         nb = ctypes.c_size_t(0)
-        rc = L.serinv_ppobtaf_q_ws(ctypes.byref(self.part), self.Q, b, a, ctypes.byref(nb))
+        if comm is not None:   # graph workspace + send + recv records, one buffer
+            rc = L.serinv_ppobtaf_ws(ctypes.byref(self.part), self.Q, b, a, ctypes.byref(nb))
+        else:
+            rc = L.serinv_ppobtaf_q_ws(ctypes.byref(self.part), self.Q, b, a, ctypes.byref(nb))
         if rc:
-            raise RuntimeError(f"serinv_ppobtaf_q_ws failed: {rc}")
+            raise RuntimeError(f"serinv_ppobtaf_ws failed: {rc}")
         dev = f"cuda:{device}"
         self.ws = torch.empty(max(nb.value, 256), dtype=torch.uint8, device=dev)
         xb = ctypes.c_size_t(0)
         L.serinv_exchange_bytes(b, a, ctypes.byref(xb))
         self.rec_doubles = xb.value // 8
-        self.send = torch.zeros(self.Q * self.rec_doubles, dtype=torch.float64, device=dev)
-        self.recv = torch.zeros(P * self.Q * self.rec_doubles, dtype=torch.float64, device=dev)
+        # caller-side exchange buffers (the communicator path keeps them inside ws)
+        self.send = self.recv = None
+        if comm is None:
+            self.send = torch.zeros(self.Q * self.rec_doubles, dtype=torch.float64, device=dev)
+            self.recv = torch.zeros(P * self.Q * self.rec_doubles, dtype=torch.float64, device=dev)
         self.info = torch.zeros(1, dtype=torch.int32, device=dev)
         self.logdet = torch.zeros(1, dtype=torch.float64, device=dev)
 
@@ -109,8 +158,15 @@ def _stream():
 
 
 def ppobtaf(ctx: DistContext, D):
-    """PARTIAL_/PERMUTED_POBTAF on the local blocks + pack of the exchange record."""
+    """PARTIAL_/PERMUTED_POBTAF on the local blocks + pack of the exchange records
+    (+ the library's all-gather when the context has a communicator)."""
     A = _bta_local(D, ctx.b, ctx.a, ctx.part.count)
+    if ctx.comm is not None:
+        rc = _lib.lib().serinv_ppobtaf(ctx.h._h, ctx.comm._c, ctypes.byref(ctx.part), ctx.Q, ctypes.byref(A),
+                                       ctx.ws.data_ptr(), ctx.ws.numel(), ctx.info.data_ptr(), _stream())
+        if rc:
+            raise RuntimeError(f"serinv_ppobtaf failed: {rc}")
+        return
     rc = _lib.lib().serinv_ppobtaf_q(ctx.h._h, ctypes.byref(ctx.part), ctx.Q, ctypes.byref(A), ctx.ws.data_ptr(),
                                      ctx.ws.numel(), ctx.send.data_ptr(), ctx.info.data_ptr(), _stream())
     if rc:
@@ -120,6 +176,13 @@ def ppobtaf(ctx: DistContext, D):
 def ppobtasi(ctx: DistContext, D):
     """POBTARSSI (redundant) + PARTIAL_/PERMUTED_POBTASI on the local blocks."""
     A = _bta_local(D, ctx.b, ctx.a, ctx.part.count)
+    if ctx.comm is not None:
+        rc = _lib.lib().serinv_ppobtasi(ctx.h._h, ctx.comm._c, ctypes.byref(ctx.part), ctx.Q, ctypes.byref(A),
+                                        ctx.ws.data_ptr(), ctx.ws.numel(), ctx.info.data_ptr(),
+                                        ctx.logdet.data_ptr(), _stream())
+        if rc:
+            raise RuntimeError(f"serinv_ppobtasi failed: {rc}")
+        return
     rc = _lib.lib().serinv_ppobtasi_q(ctx.h._h, ctypes.byref(ctx.part), ctx.Q, ctypes.byref(A), ctx.ws.data_ptr(),
                                       ctx.ws.numel(), ctx.recv.data_ptr(), ctx.info.data_ptr(),
                                       ctx.logdet.data_ptr(), _stream())
@@ -130,11 +193,15 @@ def ppobtasi(ctx: DistContext, D):
 def pselinv_step(ctx: DistContext, D, check: bool = True):
     """One distributed selected inversion: returns the global log det (check=True)."""
     ppobtaf(ctx, D)
-    exchange(ctx.send, ctx.recv, ctx.group)
+    if ctx.comm is None:
+        exchange(ctx.send, ctx.recv, ctx.group)
     ppobtasi(ctx, D)
     if check:
         info = int(ctx.info.item())
+        if info < 0:
+            raise RuntimeError("serinv: internal watchdog fired (a task dependency never completed)")
         if info:
-            raise ArithmeticError(f"not positive definite (global row {info})")
+            from . import NotPositiveDefinite
+            raise NotPositiveDefinite(info, ctx.b, ctx.part.n_global)
         return float(ctx.logdet.item())
     return None

@@ -23,7 +23,7 @@ def _sb():
     return sb
 
 
-@pytest.mark.parametrize("cfg", [(128, 1024, 64, "g1"), (256, 512, 16, "g2")])
+@pytest.mark.parametrize("cfg", [(256, 512, 16, "g2")])   # C2 / C4 on G1 seed 0: test_gpu_timed_inputs.py
 def test_full_size_against_oracle(cfg):
     n, b, a, gen = cfg
     sb = _sb()

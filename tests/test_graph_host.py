@@ -303,3 +303,38 @@ def test_pselinv_graph_ends_plan(P, r):
     assert rc == 0 and info.value == 0
     assert inv.max_block_err(cut(A, X), X)[0] < 1e-11
     assert abs(ldv.value - ld) <= 1e-12 * max(1, abs(ld))
+
+
+@pytest.mark.parametrize("P,Q", [(3, 1), (3, 2), (2, 4)])
+@pytest.mark.parametrize("where", ["interior", "boundary", "tip"])
+def test_distributed_info_is_global_and_agreed(P, Q, where):
+    # every rank reports the SAME status after serinv_ppobtasi (dist_meta.h):
+    # a bad pivot inside a partition (met by one rank's PPOBTAF), at a partition
+    # boundary (met in the redundant reduced solve, whose row labels for other
+    # ranks' partitions are decoded from the exchange records), or in the tip.
+    # The reported row is the genuine failure (finite pivot <= 0); the NaN pivots it
+    # propagates to other blocks are not reported.  dag_run_distributed_q returns -4
+    # if two ranks disagree.
+    n, b, a = 36, 5, 2
+    A0 = btagen.g1(5, n, b, a)
+    s1, e1 = par.plan(n, P, 1.0)[1]
+    c1 = (e1 - s1) // Q + ((e1 - s1) % Q > 0)    # rank 1's first sub-partition: [s1, s1 + c1)
+    assert c1 >= 3
+    if where == "interior":
+        blk = s1 + 1 if P > 2 else s1 + c1 - 2   # eliminated inside rank 1's PPOBTAF
+        A0["diag"][blk][1, 1] = -1e6
+        expect = blk * b + 2
+    elif where == "boundary":
+        blk = s1                                 # a boundary block: met in the reduced system
+        A0["diag"][blk][3, 3] = -1e6
+        expect = blk * b + 4
+    else:
+        A0["tip"][1, 1] = -1e6
+        expect = n * b + 2
+    A, n_, b_, a_ = prep(A0)
+    ldv, info = ctypes.c_double(0), ctypes.c_int(0)
+    rc = lib().dag_run_distributed_q(ctypes.c_int64(n), ctypes.c_int64(b), ctypes.c_int64(a), P, Q,
+                                     ctypes.c_double(1.0), *ptrs(A), ctypes.byref(ldv), ctypes.byref(info))
+    assert rc == 0, rc
+    assert info.value == expect, (info.value, expect)
+    assert np.isnan(ldv.value)

@@ -108,3 +108,93 @@ def test_logdet_fixed_order_deterministic():
     l1 = seq.selinv(A)[2]
     l2 = seq.selinv(A)[2]
     assert l1 == l2
+
+
+# ---------------------------------------------------------------------------
+# Sensitivity pins of the size-independent checkers.  The -m gpu
+# full-size tests at C3 use xa_residual on sampled blocks as their parity
+# property, so it must fail on small errors:
+#   xa_residual (scaled |XA - I| / (max|A| max|X|)): exact results give < 1e-13; an
+#     error of 1e-8 * max|X_diag| in ONE entry of any selected block gives >= 1e-9
+#     (it bounds absolute errors relative to the largest entry of X);
+#   llt_residual (relative Frobenius per pattern block): an error of 1e-8 ||L_blk||_F
+#     in one entry gives >= 1e-9.
+
+@pytest.mark.parametrize("key,blk", [("diag", 0), ("diag", 3), ("arrow", 0), ("arrow", 7), ("tip", None)])
+@pytest.mark.parametrize("gen", ["g1", "g2"])
+def test_xa_residual_detects_a_1e8_perturbation(key, blk, gen):
+    A = btagen.generate(gen, 3, 8, 16, 3)
+    L, X, ld = seq.selinv(A)
+    assert inv.xa_residual(X, A) < 1e-13
+    for r, c in ((1, 2), (2, 2), (0, 15 if key != "tip" else 2)):
+        Xp = {k: v.copy() for k, v in X.items()}
+        T = Xp[key] if blk is None else Xp[key][blk]
+        T[r, c] += 1e-8 * np.abs(X["diag"]).max()
+        if key in ("diag", "tip"):   # X_ii / X_nn are stored full symmetric
+            T[c, r] = T[r, c]
+        res = inv.xa_residual(Xp, A)
+        assert res >= 1e-9, (r, c, res)
+        # the sampled form the GPU tests use sees it too when the block's row is sampled
+        assert (inv.xa_residual(Xp, A, blocks=[0, 7], tip=True) if key == "tip"
+                else inv.xa_residual(Xp, A, blocks=[blk])) >= 1e-9
+
+
+@pytest.mark.parametrize("gen", ["g1", "g2"])
+@pytest.mark.parametrize("mutation", ["lower_sign", "lower_transposed", "lower_zero", "lower_shifted",
+                                      "arrow_sign", "diag_swapped", "tip_dropped_term"])
+def test_xa_residual_detects_plausible_mistakes(gen, mutation):
+    # X_{i+1,i} enters (XA)|pattern only through products with the off-diagonal
+    # blocks of A, so a 1e-8 error in it is scaled by |A_{i+1,i}| / |A_ii| there;
+    # the mistakes a wrong implementation makes (sign, transposed operand, dropped
+    # or misplaced block) change it by O(|X_{i+1,i}|) and are caught by far.
+    A = btagen.generate(gen, 6, 8, 16, 3)
+    L, X, ld = seq.selinv(A)
+    Xp = {k: v.copy() for k, v in X.items()}
+    i = 3
+    if mutation == "lower_sign":
+        Xp["lower"][i] = -Xp["lower"][i]
+    elif mutation == "lower_transposed":
+        Xp["lower"][i] = Xp["lower"][i].T.copy()
+    elif mutation == "lower_zero":
+        Xp["lower"][i] = 0.0
+    elif mutation == "lower_shifted":
+        Xp["lower"][i] = X["lower"][i + 1]
+    elif mutation == "arrow_sign":
+        Xp["arrow"][i] = -Xp["arrow"][i]
+    elif mutation == "diag_swapped":
+        Xp["diag"][i] = X["diag"][i + 1]
+    else:   # tip without the arrow contributions' final term
+        Xp["tip"] = np.linalg.inv(A["tip"])
+    assert inv.xa_residual(Xp, A, blocks=[i, i + 1], tip=True) >= 1e-9
+
+
+@pytest.mark.parametrize("key,blk", [("diag", 0), ("diag", 5), ("lower", 3), ("arrow", 7), ("tip", None)])
+def test_llt_residual_detects_a_1e8_perturbation(key, blk):
+    A = btagen.g1(4, 8, 16, 3)
+    L, X, ld = seq.selinv(A)
+    assert inv.llt_residual(L, A) < 1e-13
+    Lp = {k: v.copy() for k, v in L.items()}
+    T = Lp[key] if blk is None else Lp[key][blk]
+    T[2, 1] += 1e-8 * np.linalg.norm(T)
+    assert inv.llt_residual(Lp, A) >= 1e-9
+
+
+def test_xa_residual_lazy_blocks_and_scale():
+    # the GPU tests pass lazily fetched blocks and an explicit scale: same value
+    A = btagen.g2(2, 9, 12, 2)
+    L, X, ld = seq.selinv(A)
+
+    class Lazy:
+        def __init__(self, arr):
+            self.arr = arr
+            self.shape = arr.shape
+
+        def __getitem__(self, i):
+            return self.arr[i]
+    scale = float(np.abs(A["diag"]).max()) * float(np.abs(X["diag"]).max())
+    keys = ("diag", "lower", "arrow")
+    XL = {k: Lazy(X[k]) for k in keys} | {"tip": X["tip"]}
+    AL = {k: Lazy(A[k]) for k in keys} | {"tip": A["tip"]}
+    blocks = [0, 4, 8]
+    assert inv.xa_residual(XL, AL, blocks=blocks, scale=scale, tip=True) == \
+        inv.xa_residual(X, A, blocks=blocks, tip=True)

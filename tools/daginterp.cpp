@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../paper_2503_17528_b200/csrc/graph.h"
+#include "../paper_2503_17528_b200/csrc/dist_meta.h"
 
 using namespace serinv;
 
@@ -18,8 +19,12 @@ namespace {
 struct Ctx {
   double *bufs[BUF_COUNT];
   std::vector<int32_t> ctr;
-  int info = 0;
+  int info = 0;   // first genuine failure (finite pivot <= 0, zero / infinite diagonal)
+  int info2 = 0;  // failures with a NaN pivot (propagated from an earlier failure or NaN input)
 };
+inline void rec_info(int &slot, int v) {
+  if (!slot || v < slot) slot = v;
+}
 
 inline double *ptr(Ctx &c, const Loc &l) { return c.bufs[l.buf] + l.off; }
 inline double get(Ctx &c, const Loc &l, int r, int k) { return ptr(c, l)[(int64_t)r * l.ld + k]; }
@@ -28,7 +33,16 @@ inline double opget(Ctx &c, const Loc &l, int trans, int i, int j) {
   return trans ? get(c, l, j, i) : get(c, l, i, j);
 }
 
+int run_tasks(const Graph &g, Ctx &c);
+// as the device launch: NaN-pivot failures count only when there is no genuine one
 int run(const Graph &g, Ctx &c) {
+  c.info2 = 0;
+  const int rc = run_tasks(g, c);
+  if (!c.info) c.info = c.info2;
+  return rc;
+}
+
+int run_tasks(const Graph &g, Ctx &c) {
   c.ctr.assign(g.nctr, 0);
   if (g.arr_ctr >= 0) c.ctr[g.arr_ctr] = 1 << 30;  // streaming IO: every block has arrived
   if (g.arr_ctr2 >= 0) c.ctr[g.arr_ctr2] = 1 << 30;
@@ -112,7 +126,7 @@ int run(const Graph &g, Ctx &c) {
           double d = A_(j, j);
           for (int k = 0; k < j; ++k) d -= A_(j, k) * A_(j, k);
           if (!(d > 0.0)) {
-            if (!c.info || T.aux1 + j + 1 < c.info) c.info = T.aux1 + j + 1;
+            rec_info(std::isnan(d) ? c.info2 : c.info, T.aux1 + j + 1);
             d = NAN;
           }
           d = std::sqrt(d);
@@ -150,7 +164,7 @@ int run(const Graph &g, Ctx &c) {
       if (T.type == TK_TRTRI) {
         for (int j = 0; j < m; ++j)
           if (!(A_(j, j) != 0.0) || !std::isfinite(A_(j, j)))
-            if (!c.info || T.aux1 + j + 1 < c.info) c.info = T.aux1 + j + 1;
+            rec_info(std::isnan(A_(j, j)) ? c.info2 : c.info, T.aux1 + j + 1);
       }
       auto trsm_tile = [&](int s0, int s1, const Loc &out, int mm, double beta) {
         // (beta * C + alpha * sum_{s0 <= s < s1} ...) * W^T  at out (mm x m)
@@ -229,7 +243,7 @@ int run(const Graph &g, Ctx &c) {
       for (int i = 0; i < T.aux0; ++i) s += ptr(c, T.r)[i];
       double v = 2.0 * s;
       for (int j = 0; j < T.aux1; ++j) v += ptr(c, T.c0)[T.aux2 * j];
-      *ptr(c, T.out) = c.info ? NAN : v;
+      *ptr(c, T.out) = (c.info || c.info2) ? NAN : v;
     }
     for (int s = 0; s < T.nsig; ++s) c.ctr[g.sigs[T.sig0 + s]]++;
   }
@@ -321,7 +335,7 @@ int dag_run_distributed_q(int64_t n, int64_t b, int64_t a, int P, int Q, double 
                           double *arrow, double *tip, double *logdet, int *info) {
   std::vector<int64_t> st;
   if (!plan_partitions(n, P, r, st)) return -3;
-  int64_t rec = exchange_doubles(b, a);
+  int64_t rec = exchange_doubles(b, a), mo = exchange_meta_offset(b, a);
   std::vector<double> records(rec * P * Q, 0.0);
   struct Rank {
     std::vector<double> D, L, A, T, ws;
@@ -359,9 +373,10 @@ int dag_run_distributed_q(int64_t n, int64_t b, int64_t a, int P, int Q, double 
     k.c.bufs[BUF_WS] = k.ws.data();
     k.c.bufs[BUF_EXT0] = records.data() + p * Q * rec;
     if (run(g0, k.c)) return -1;
-    if (k.c.info) *info = k.c.info;
+    for (int q = 0; q < Q; ++q) meta_write(records.data() + p * Q * rec, Q, rec, mo, k.c.info, s, cnt, q);
   }
   double ld = 0;
+  *info = 0;
   for (int p = 0; p < P; ++p) {
     Rank &k = R[p];
     Graph g1 = build_distributed(1, P, p, n, st[p], k.cnt, b, a, opt, Q);
@@ -369,9 +384,15 @@ int dag_run_distributed_q(int64_t n, int64_t b, int64_t a, int P, int Q, double 
     k.c.bufs[BUF_EXT0] = nullptr;
     k.c.bufs[BUF_EXT1] = records.data();
     k.c.bufs[BUF_LOGDET] = &ldp;
-    k.c.info = 0;
+    const int comb = meta_combine_info(records.data(), P * Q, rec, mo);  // as serinv_ppobtasi
+    k.c.info = comb;
     if (run(g1, k.c)) return -1;
-    if (k.c.info && !*info) *info = k.c.info;
+    k.c.info = comb ? comb : meta_decode_info(k.c.info, records.data(), rec, mo, b);
+    if (p == 0) *info = k.c.info;
+    else if (k.c.info != *info) {
+      fprintf(stderr, "rank info mismatch: %d vs %d\n", k.c.info, *info);
+      return -4;
+    }
     if (p == 0) ld = ldp;
     else if (!(ldp == ld) && !(std::isnan(ld) && std::isnan(ldp))) fprintf(stderr, "rank logdet mismatch\n");
     int64_t s = st[p], e = st[p + 1], cnt = k.cnt;
@@ -417,7 +438,15 @@ int dag_run_dist_phase_q(int phase, int P, int Q, int rank, int64_t n, int64_t s
   c.bufs[BUF_EXT0] = ext0;
   c.bufs[BUF_EXT1] = ext1;
   c.bufs[BUF_LOGDET] = &ld;
+  // the status handling of serinv_ppobtaf / serinv_ppobtasi (dist_meta.h)
+  const int64_t rec = exchange_doubles(b, a), mo = exchange_meta_offset(b, a);
+  const int comb = phase == 1 ? meta_combine_info(ext1, P * Q, rec, mo) : 0;
+  c.info = comb;
   int rc = run(g, c);
+  if (phase == 0)
+    for (int q = 0; q < Q; ++q) meta_write(ext0, Q, rec, mo, c.info, start, count, q);
+  else
+    c.info = comb ? comb : meta_decode_info(c.info, ext1, rec, mo, b);
   *info = c.info;
   if (logdet) *logdet = ld;
   return rc;
