@@ -1195,6 +1195,7 @@ __device__ void chol8_pipelined(double *St, double *Wt, double *S2, double *dv, 
       if (k > 0) {
         double l[2] = {0.0, 0.0};
         blk_mma_nt(l, blk(St, k, k - 1), blk(Wt, k - 1, k - 1));
+        __syncwarp();  // in-place: every lane's operand reads before any lane's store
         blk_store(blk(St, k, k - 1), l);
         __syncwarp();
         asm volatile("bar.arrive 1, 256;" ::: "memory");
@@ -1211,6 +1212,7 @@ __device__ void chol8_pipelined(double *St, double *Wt, double *S2, double *dv, 
       if (ip < 8) {  // panel block (ip, k-1)
         double l[2] = {0.0, 0.0};
         blk_mma_nt(l, blk(St, ip, k - 1), blk(Wt, k - 1, k - 1));
+        __syncwarp();  // in-place: every lane's operand reads before any lane's store
         blk_store(blk(St, ip, k - 1), l);
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");

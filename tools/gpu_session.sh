@@ -11,7 +11,7 @@ mkdir -p $OUT
 { nproc; free -g; nvidia-smi --query-gpu=name,clocks.max.sm,power.limit,temperature.gpu --format=csv; } > $OUT/host.txt 2>&1
 if [ "$K" != "none" ]; then
   if [ "$K" = "all" ]; then
-    timeout 1800 python -m pytest tests -m gpu -q -x -rs > $OUT/gpu_tests.txt 2>&1; echo tests=$?
+    timeout 1800 python -m pytest tests -m gpu -q -rs > $OUT/gpu_tests.txt 2>&1; echo tests=$?
   else
     timeout 1800 python -m pytest tests -m gpu -q -rs -k "$K" > $OUT/gpu_tests.txt 2>&1; echo tests=$?
   fi
@@ -21,4 +21,9 @@ fi
 for c in $CFGS; do
   timeout 1200 python bench.py --config $c $EXTRA > $OUT/bench_$c.json 2> $OUT/bench_$c.err; echo bench_$c=$?
   tail -c 3000 $OUT/bench_$c.json
+done
+# optional traces: TRACE="selinv:365:2048:4 pobtaf:365:2048:4"
+for t in $TRACE; do
+  IFS=: read kind n b a P <<< "$t"
+  timeout 600 python tools/trace.py $kind $n $b $a --P ${P:-1} > $OUT/trace_${kind}_${n}_${b}.txt 2>&1; echo trace_$t=$?
 done
