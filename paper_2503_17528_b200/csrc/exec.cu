@@ -1623,13 +1623,13 @@ __device__ void run_logdet(const Params &p, const Task &T, double *smem) {
   }
 }
 
+__device__ void run_tasks(const Params &p, double *smem, int &s_task, int &s_q);
 }  // namespace dev
 
 extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev::Params p) {
   using namespace dev;
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_task, s_q;
-  unsigned long long t_claim = 0, t_start = 0;
   // ---- roles: the first nq-1 CTAs to arrive serve the critical queues and get
   // their SM to themselves (co-resident siblings on those SMs exit); the rest
   // serve the bulk queue.  All CTAs are co-resident, so the barrier is safe.
@@ -1685,7 +1685,23 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
     s_q = q;
   }
   __syncthreads();
-  if (s_q < 0) return;
+  if (s_q >= 0) run_tasks(p, smem, s_task, s_q);
+  // the last CTA out merges the NaN-pivot failures into *info (only if there was
+  // no genuine failure): every other CTA's records are ordered before its
+  // fence + increment of the exit counter
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.done, 1) == (int)gridDim.x - 1) {
+      __threadfence();
+      const int i2 = *(volatile int *)p.info2;
+      if (i2 != 0) atomicCAS(p.info, 0, i2);
+    }
+  }
+}
+
+namespace dev {
+__device__ void run_tasks(const Params &p, double *smem, int &s_task, int &s_q) {
+  unsigned long long t_claim = 0, t_start = 0;
   for (;;) {
     if (threadIdx.x == 0) {
       int q = s_q, t = -1;
@@ -1761,6 +1777,7 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
     }
   }
 }
+}  // namespace dev
 
 int exec_smem_bytes() { return dev::SMEM_DOUBLES * 8; }
 

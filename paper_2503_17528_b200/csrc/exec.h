@@ -21,7 +21,8 @@ struct Params {
   int ntasks;
   double *bufs[BUF_COUNT];
   int *info;             // first genuine failure (finite pivot <= 0 / zero diagonal), dpotrf row
-  int *info2;            // failures with a NaN pivot (propagated, or NaN input): merged after the launch
+  int *info2;            // failures with a NaN pivot (propagated, or NaN input): merged by the last CTA out
+  int *done;             // CTAs that finished (zeroed before each launch)
   unsigned long long *trace;  // optional: 4 x u64 per task {claim, start, end, meta}
 };
 }  // namespace dev

@@ -127,7 +127,7 @@ int upload(DevGraph &dg, int grid) {
   dg.nq = (int)g.qoff.size() - 1;
   dg.ncrit = g.ncrit;
   dg.nurgent = g.nurgent;
-  dg.nctr_alloc = (int64_t)g.nctr + dg.nq + 2 + grid + 1;  // + info2 (exec.h)
+  dg.nctr_alloc = (int64_t)g.nctr + dg.nq + 2 + grid + 2;  // + done, info2 (exec.h)
   if (cudaMalloc(&dg.ctr, (size_t)dg.nctr_alloc * sizeof(int32_t)) != cudaSuccess) return SERINV_ERR_CUDA;
   dg.ntasks = (int64_t)g.tasks.size();
   dg.nwaits = (int64_t)g.waits.size();
@@ -197,10 +197,6 @@ int get_graph_impl(serinv_handle_t h, const GKey &key, DevGraph **out) {
   return SERINV_OK;
 }
 
-__global__ void info_merge_kernel(int *info, const int *info2) {
-  if (threadIdx.x == 0 && *info == 0) *info = *info2;
-}
-
 // reset: clear the graph's counters (and *d_info unless keep_info) before the kernel
 int launch(serinv_handle_t h, DevGraph &dg, double *bufs[BUF_COUNT], int *d_info, cudaStream_t st,
            bool reset = true, bool keep_info = false) {
@@ -226,11 +222,10 @@ int launch(serinv_handle_t h, DevGraph &dg, double *bufs[BUF_COUNT], int *d_info
   for (int i = 0; i < BUF_COUNT; ++i) p.bufs[i] = bufs[i];
   p.info = d_info;
   p.info2 = dg.ctr + dg.nctr_alloc - 1;
+  p.done = dg.ctr + dg.nctr_alloc - 2;
   p.trace = (h->trace && (size_t)dg.ntasks <= h->trace_cap) ? h->trace : nullptr;
   serinv_exec_kernel<<<h->grid, 256, h->smem, st>>>(p);
-  // failures with a NaN pivot count only if there was no genuine one (exec.h)
-  info_merge_kernel<<<1, 32, 0, st>>>(d_info, p.info2);
-  h->last_launches += 2;
+  h->last_launches += 1;
   return cudaGetLastError() == cudaSuccess ? SERINV_OK : SERINV_ERR_CUDA;
 }
 

@@ -33,7 +33,10 @@ def main(path, config, command):
     head = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     names, units = rows[head], rows[head + 1]
     data = next(r for r in rows[head + 2:] if any("serinv_exec" in c for c in r))
-    out = {"config": config, "kernel": "serinv_exec_kernel", "command": command, "units_raw": {}}
+    sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+    from bench import src_sha
+    out = {"config": config, "kernel": "serinv_exec_kernel", "command": command, "src_sha": src_sha(),
+           "units_raw": {}}
     for m, key in METRICS.items():
         if m not in names:
             continue
