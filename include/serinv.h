@@ -204,6 +204,27 @@ int serinv_pselinv_nested(serinv_handle_t h, const serinv_bta_t *A, int nlev, co
  */
 int serinv_pselinv_plan(int64_t n, int P, double r, int64_t *starts);
 
+/*
+ * Small-block engine (b <= 64, a <= 16): the same partitioned method with nested
+ * solving (Sec. 3, Alg. 3-6; Sec. 4.2) executed by two kernels
+ * per nesting level in which one CTA carries a whole partition's chain with its
+ * blocks resident in shared memory.  Ps[0..nlev-1]: partitions
+ * per level (each >= 2; level k+1 works on the 2 Ps[k] - 2 block reduced system of
+ * level k, twisted last partition, reading R14); the last reduced system is
+ * solved as one chain (Alg. 1 + Alg. 2).  nlev = 0: the whole matrix as one chain;
+ * nlev < 0: the library's plan (serinv_sb_auto_plan; Ps ignored).  A -> X in
+ * place, log det in *d_logdet, *d_info as serinv_selinv (dpotrf row semantics).
+ * Errors: SERINV_ERR_SHAPE (b > 64, a > 16, n < 1), SERINV_ERR_PLAN (a level has a
+ * middle partition of < 2 blocks or an end partition of < 1), SERINV_ERR_WS.
+ * The library caches the plan's index tables per shape in the handle.
+ *   serinv_sb_auto_plan  writes min(levels, cap) entries, returns the level count
+ *                        (>= 0) or a negative status.
+ */
+int serinv_sb_auto_plan(int64_t n, int64_t b, int64_t a, int *Ps, int cap);
+int serinv_sb_ws(int64_t n, int64_t b, int64_t a, int nlev, const int *Ps, size_t *bytes);
+int serinv_sb_selinv(serinv_handle_t h, const serinv_bta_t *A, int nlev, const int *Ps, void *d_ws,
+                     size_t ws_bytes, int *d_info, double *d_logdet, void *stream);
+
 /* ------------------------------------------------------------------------- */
 /* Distributed method, one process per GPU (Sec. 3, Alg. 3-6; the    */
 /* paper's exchange is NCCL).                                      */

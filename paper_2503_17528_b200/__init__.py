@@ -22,7 +22,8 @@ from ._lib import BTA, GraphStats, Part
 
 __all__ = ["Handle", "pobtaf", "pobtasi", "selinv", "selinv_host", "pselinv", "plan", "version",
            "NotPositiveDefinite", "SerinvError", "ppobtaf", "ppobtasi", "exchange_bytes",
-           "graph_stats", "default_handle", "auto_partitions", "pselinv_plan", "plan_ends", "Comm"]
+           "graph_stats", "default_handle", "auto_partitions", "pselinv_plan", "plan_ends", "Comm",
+           "selinv_sb", "sb_auto_plan"]
 
 
 class SerinvError(RuntimeError):
@@ -284,6 +285,37 @@ def pselinv(diag, lower, arrow, tip, P, r: float = 1.0, *, handle: Handle | None
     rc = L.serinv_pselinv_nested(h._h, ctypes.byref(A), len(Ps), arr, float(r), ws.data_ptr(), ws.numel(),
                                  info.data_ptr(), logdet.data_ptr(), _stream())
     _check(rc, "pselinv")
+    return _finish(h, info, logdet, check, A.b, A.n)
+
+
+def sb_auto_plan(n: int, b: int, a: int) -> list[int]:
+    """The small-block engine's default nesting plan (serinv_sb_auto_plan)."""
+    out = (ctypes.c_int * 32)()
+    k = _lib.lib().serinv_sb_auto_plan(n, b, a, out, 32)
+    if k < 0:
+        raise SerinvError(-k, "sb_auto_plan")
+    return list(out[:k])
+
+
+def selinv_sb(diag, lower, arrow, tip, Ps=None, *, handle: Handle | None = None, check: bool = True, info=None,
+              logdet=None):
+    """POBTAF + POBTASI by the small-block engine (b <= 64, a <= 16; serinv_sb_selinv):
+    the partitioned method with nested solving, Ps = partitions per level (None: the
+    library's plan; [] = one chain).  A -> X in place.  Returns log det."""
+    L = _lib.lib()
+    h = handle or default_handle(diag.device.index)
+    A = _bta(diag, lower, arrow, tip)
+    nlev = -1 if Ps is None else len(Ps)
+    arr = (ctypes.c_int * max(1, nlev))(*([] if Ps is None else [int(x) for x in Ps]))
+    nb = ctypes.c_size_t(0)
+    _check(L.serinv_sb_ws(A.n, A.b, A.a, nlev, arr, ctypes.byref(nb)), "sb_ws")
+    ws = h.workspace(nb.value)
+    si, sl = h.scalars()
+    info = si if info is None else info
+    logdet = sl if logdet is None else logdet
+    rc = L.serinv_sb_selinv(h._h, ctypes.byref(A), nlev, arr, ws.data_ptr(), ws.numel(), info.data_ptr(),
+                            logdet.data_ptr(), _stream())
+    _check(rc, "sb_selinv")
     return _finish(h, info, logdet, check, A.b, A.n)
 
 

@@ -86,6 +86,10 @@ def lib():
     L.serinv_bench_gemm.argtypes = [c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, ctypes.c_size_t, c_p]
     L.serinv_set_trace.argtypes = [c_p, c_p, ctypes.c_size_t]
     L.serinv_last_launches.argtypes = [c_p, ctypes.POINTER(ctypes.c_int)]
+    L.serinv_sb_auto_plan.argtypes = [c_i64, c_i64, c_i64, ip, ctypes.c_int]
+    L.serinv_sb_ws.argtypes = [c_i64, c_i64, c_i64, ctypes.c_int, ip, sz]
+    L.serinv_sb_selinv.argtypes = [c_p, ctypes.POINTER(BTA), ctypes.c_int, ip, c_p, ctypes.c_size_t, c_p, c_p,
+                                   c_p]
     _lib = L
     return L
 
@@ -99,4 +103,5 @@ EXPORTED = [
     "serinv_auto_partitions", "serinv_pselinv_nested_ws", "serinv_pselinv_nested", "serinv_graph_stats_nested",
     "serinv_ppobtaf_q_ws", "serinv_ppobtaf_q", "serinv_ppobtasi_q", "serinv_dist_auto_q",
     "serinv_nccl_unique_id", "serinv_comm_init", "serinv_comm_destroy", "serinv_pselinv_plan",
+    "serinv_sb_auto_plan", "serinv_sb_ws", "serinv_sb_selinv",
 ]

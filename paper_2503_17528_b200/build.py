@@ -15,8 +15,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libserinv.so")
-SOURCES = ["exec.cu", "serinv.cu", "graph.cpp", "comm.cpp"]
-HEADERS = ["exec.h", "graph.h", "task.h", "dist_meta.h", "comm.h"]
+SOURCES = ["exec.cu", "serinv.cu", "graph.cpp", "comm.cpp", "sb.cu"]
+HEADERS = ["exec.h", "graph.h", "task.h", "dist_meta.h", "comm.h", "sb.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

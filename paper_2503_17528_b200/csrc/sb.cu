@@ -1,0 +1,959 @@
+// sb.cu -- small-block engine: the partitioned selected inversion of PAPER.md
+// Sec. 3 (PPOBTAF Alg. 3-4, POBTARSSI Sec. 3.3, PPOBTASI Alg. 5-6) with nested
+// solving of the reduced systems (Sec. 4.2), for b <= 64, a <= 16.
+//
+// Why a second engine.  With b = 64 a block step of Alg. 1 is ~0.5 MFLOP: the
+// tile-task executor (exec.cu) pays a dependency hop (global counter publish /
+// poll, operand re-staging through L2) between every POTRF, TRSM and SYRK of the
+// chain, and the chain is the bound (BASELINE C5).  Here ONE CTA carries a whole
+// partition's chain: the running diagonal block, the coupling, the fill-in block
+// B_i (Alg. 4) and the arrow rows stay in shared memory from step to step, the
+// persistent accumulators (A_ff, A_{n,f}, U_p of Alg. 4 l.9-12) in registers, and
+// the partitions of a level run concurrently on all SMs.  Two kernels per level:
+//   sb_factor_kernel   PPOBTAF of every partition of the level (2 CTAs / SM, so
+//                      one CTA's latency-bound 64 x 64 Cholesky overlaps the
+//                      other's DMMA products) writing the boundary blocks straight
+//                      into the next level's reduced arrays (order of reading R14,
+//                      DESIGN.md); the last level (one partition) is the plain
+//                      sequential POBTAF incl. the tip (Alg. 1).
+//   sb_inverse_kernel  PPOBTASI of every partition (1 CTA / SM, 224 KB of
+//                      operands resident), seeded by the next level's X.
+// Block products are warp-level DMMA (mma.sync m8n8k4 f64; tcgen05 has no f64
+// kind) on shared-memory tiles whose 64-double rows are XOR-swizzled so that the
+// fragment loads of both operand orientations are bank-conflict free.  TRSM is a
+// product with W = L_ii^{-1}; W is what the factor pass stores in the
+// diagonal slot (the inverse pass needs W, not L_ii).  Padding: blocks of b < 64
+// are embedded in 64 x 64 tiles with an identity diagonal, arrow rows a < 16 with
+// zeros, so the padded problem has the same factors / inverse on the real part.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "graph.h"
+#include "sb.h"
+
+namespace serinv {
+namespace sb {
+namespace dev {
+
+constexpr int T = 64;
+constexpr int NT = 256;
+constexpr int AR = kMaxA;  // arrow tile rows
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int TD = T * T;        // doubles per 64 x 64 tile
+constexpr int AD = AR * T;       // doubles per arrow tile (16 x 64)
+
+enum PartType { P_TOP = 0, P_MID = 1, P_BOT = 2, P_SEQ = 3 };
+
+// element (r, c) of a tile with 64-double rows: bank-conflict-free DMMA fragment
+// loads for [row][k] (lanes: r = l/4, c = l%4) and [k][row] (r = l%4, c = l/4)
+__device__ __forceinline__ int swz(int r, int c) { return (r << 6) + (c ^ (((r & 3) << 3) | (r & 4))); }
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+__device__ void record_info(int *info, int v) {
+  int old = *(volatile int *)info;
+  while (old == 0 || v < old) {
+    int prev = atomicCAS(info, old, v);
+    if (prev == old) break;
+    old = prev;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tile movement.  A tile is rows_t x 64 (rows_t = 64 or AR) in swizzled smem.
+// ---------------------------------------------------------------------------
+// s <- op(g) padded: (r, c) = trans ? g[c*ld + r] : g[r*ld + c] for r < rows, c < cols,
+// else (pad && r == c).  Full 64 x 64 untransposed blocks go by cp.async (caller waits).
+__device__ void ld_tile(double *s, const double *g, int rows_t, int rows, int cols, int ld, bool trans,
+                        bool pad) {
+  const int tid = threadIdx.x;
+  if (!trans && rows == T && cols == T && ld == T && rows_t == T) {
+#pragma unroll 4
+    for (int i = tid; i < TD / 2; i += NT) {
+      const int r = i >> 5, c = (i & 31) * 2;
+      cp_async16(s + swz(r, c), g + r * T + c);
+    }
+    return;
+  }
+  for (int i = tid; i < rows_t * T; i += NT) {
+    int r, c;
+    if (trans) {  // consecutive threads read consecutive global addresses
+      r = i & 63;
+      c = i >> 6;
+      if (rows_t < T) {  // r ranges over rows_t
+        r = i % rows_t;
+        c = i / rows_t;
+      }
+    } else {
+      r = i >> 6;
+      c = i & 63;
+    }
+    double v;
+    if (r < rows && c < cols)
+      v = trans ? __ldg(g + (int64_t)c * ld + r) : __ldg(g + (int64_t)r * ld + c);
+    else
+      v = (pad && r == c) ? 1.0 : 0.0;
+    s[swz(r, c)] = v;
+  }
+}
+
+// g <- op(s) (rows x cols of the tile; trans: g[c*ld + r] = s(r, c))
+__device__ void st_tile(double *g, const double *s, int rows, int cols, int ld, bool trans) {
+  const int tid = threadIdx.x;
+  if (!trans && rows == T && cols == T && ld == T) {
+    for (int i = tid; i < TD / 2; i += NT) {
+      const int r = i >> 5, c = (i & 31) * 2;
+      *(double2 *)(g + r * T + c) = *(const double2 *)(s + swz(r, c));
+    }
+    return;
+  }
+  for (int i = tid; i < rows * cols; i += NT) {
+    if (trans) {
+      const int c = i / rows, r = i % rows;  // consecutive threads: consecutive g addresses
+      g[(int64_t)c * ld + r] = s[swz(r, c)];
+    } else {
+      const int r = i / cols, c = i % cols;
+      g[(int64_t)r * ld + c] = s[swz(r, c)];
+    }
+  }
+}
+
+// global -> global copy of a rows x cols block (same ld)
+__device__ void cp_block(double *dst, const double *src, int64_t count) {
+  for (int64_t i = threadIdx.x; i < count; i += NT) dst[i] = __ldg(src + i);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-level DMMA products on smem tiles: acc[MI][NI] (8 x 8 fragments, lane l
+// holds (l/4, 2(l%4) + {0,1})) of the (8MI x 8NI) block at (m0, n0)
+//   acc += sgn * sum_{k in [k0, k1)} op(A)[m][k] op(B)[k][n]
+// ---------------------------------------------------------------------------
+template <int MI, int NI, bool TA, bool TB, bool NEG>
+__device__ __forceinline__ void mma(double (&acc)[MI][NI][2], const double *A, const double *B, int m0, int n0,
+                                    int k0, int k1) {
+  const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
+#pragma unroll 2
+  for (int k = k0; k < k1; k += 4) {
+    double af[MI], bf[NI];
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int m = m0 + 8 * i + lr, kk = k + lc;
+      const double v = TA ? A[swz(kk, m)] : A[swz(m, kk)];
+      af[i] = NEG ? -v : v;
+    }
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const int n = n0 + 8 * j + lr, kk = k + lc;
+      bf[j] = TB ? B[swz(n, kk)] : B[swz(kk, n)];
+    }
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) dmma(acc[i][j], af[i], bf[j]);
+  }
+}
+
+template <int MI, int NI>
+__device__ __forceinline__ void acc_zero(double (&acc)[MI][NI][2]) {
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+// acc <- g (rows x cols block, ld), padded with the identity (pad) or zeros
+template <int MI, int NI>
+__device__ __forceinline__ void acc_ld(double (&acc)[MI][NI][2], const double *g, int ld, int rows, int cols,
+                                       int m0, int n0, bool pad) {
+  const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const int m = m0 + 8 * i + lr, n = n0 + 8 * j + 2 * lc;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = n + e;
+        acc[i][j][e] = (m < rows && c < cols) ? __ldg(g + (int64_t)m * ld + c) : ((pad && m == c) ? 1.0 : 0.0);
+      }
+    }
+}
+
+template <int MI, int NI>
+__device__ __forceinline__ void acc_st_smem(double *s, const double (&acc)[MI][NI][2], int m0, int n0,
+                                            double sgn) {
+  const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const int m = m0 + 8 * i + lr, n = n0 + 8 * j + 2 * lc;
+      *(double2 *)(s + swz(m, n)) = make_double2(sgn * acc[i][j][0], sgn * acc[i][j][1]);
+    }
+}
+
+// g <- sgn * acc (rows x cols of the block; trans: g[c*ld + r] = value (r, c))
+template <int MI, int NI>
+__device__ __forceinline__ void acc_st_global(double *g, const double (&acc)[MI][NI][2], int ld, int rows,
+                                              int cols, int m0, int n0, bool trans, double sgn) {
+  const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const int m = m0 + 8 * i + lr, n = n0 + 8 * j + 2 * lc;
+      if (m >= rows) continue;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = n + e;
+        if (c < cols) {
+          if (trans)
+            g[(int64_t)c * ld + m] = sgn * acc[i][j][e];
+          else
+            g[(int64_t)m * ld + c] = sgn * acc[i][j][e];
+        }
+      }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// In-place Cholesky + triangular inverse of a 64 x 64 SPD tile (lower triangle
+// read): D <- W = L^{-1} (lower, strict upper zero).  ldg[t] = L_tt.  Blocked
+// right-looking on 8-column panels: warp 0 factors the 8 x 8 diagonal block in
+// registers (pivots, the product-form inverse W_jj alongside), all warps the
+// panel TRSM (with W_jj) and the trailing update by DMMA; then W from the
+// blocks: W_21 = -W_22 L_21 W_11 on 8 / 16 / 32 levels.  *s_bad = first
+// non-positive (or NaN) pivot index, 64 if none.  Called by all NT threads.
+// ---------------------------------------------------------------------------
+__device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad) {
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, lr = l >> 2, lc = l & 3;
+  if (tid == 0) *s_bad = 64;
+  for (int j = 0; j < 8; ++j) {
+    const int R = 8 * j;
+    if (w == 0) {
+      const int c0 = 2 * lc;
+      double a0 = D[swz(R + lr, R + c0)], a1 = D[swz(R + lr, R + c0 + 1)];
+      double w0 = (lr == c0) ? 1.0 : 0.0, w1 = (lr == c0 + 1) ? 1.0 : 0.0;
+      int bad = 64;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int q = k >> 1;
+        const double t = (k & 1) ? a1 : a0;  // own row's column-k value on lanes with l%4 == k/2
+        const double dkk = __shfl_sync(FULL, t, 4 * k + q);
+        const double ark = __shfl_sync(FULL, t, 4 * lr + q);
+        const double ac0 = __shfl_sync(FULL, t, 4 * c0 + q);
+        const double ac1 = __shfl_sync(FULL, t, 4 * (c0 + 1) + q);
+        const double wk0 = __shfl_sync(FULL, w0, 4 * k + lc);
+        const double wk1 = __shfl_sync(FULL, w1, 4 * k + lc);
+        if (!(dkk > 0.0) && bad == 64) bad = R + k;
+        const double rs = rsqrt(dkk);
+        const double inv = rs * rs;
+        const double lrk = ark * rs;
+        if (c0 == k) {
+          if (lr > k) a0 = lrk;
+          else if (lr == k) a0 = dkk * rs;
+        } else if (c0 > k && lr >= c0) {
+          a0 -= ark * ac0 * inv;
+        }
+        if (c0 + 1 == k) {
+          if (lr > k) a1 = lrk;
+          else if (lr == k) a1 = dkk * rs;
+        } else if (c0 + 1 > k && lr >= c0 + 1) {
+          a1 -= ark * ac1 * inv;
+        }
+        if (lr == k) {
+          w0 *= rs;
+          w1 *= rs;
+        } else if (lr > k) {
+          const double f = lrk * rs;
+          w0 -= f * wk0;
+          w1 -= f * wk1;
+        }
+      }
+      D[swz(R + lr, R + c0)] = (c0 <= lr) ? a0 : 0.0;
+      D[swz(R + lr, R + c0 + 1)] = (c0 + 1 <= lr) ? a1 : 0.0;
+      Wd[swz(lr, R + c0)] = w0;
+      Wd[swz(lr, R + c0 + 1)] = w1;
+      if (lr == c0) ldg[R + lr] = a0;
+      if (lr == c0 + 1) ldg[R + lr] = a1;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+      if (l == 0 && bad < *s_bad) *s_bad = bad;
+    }
+    __syncthreads();
+    if (j == 7) break;
+    {  // panel TRSM: L_ij = A_ij W_jj^T, i = j+1+w
+      const int i = j + 1 + w;
+      if (i < 8) {
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 4)
+          dmma(acc, D[swz(8 * i + lr, R + kk + lc)], Wd[swz(lr, R + kk + lc)]);
+        *(double2 *)(D + swz(8 * i + lr, R + 2 * lc)) = make_double2(acc[0], acc[1]);
+      }
+    }
+    __syncthreads();
+    {  // trailing update A_ik -= L_ij L_kj^T, j < k <= i
+      const int nb = 7 - j, np = nb * (nb + 1) / 2;
+      for (int t = w; t < np; t += 8) {
+        int ii = 0, tt = t;
+        while (tt > ii) {
+          tt -= ii + 1;
+          ++ii;
+        }
+        const int i = j + 1 + ii, k = j + 1 + tt;
+        double2 c = *(const double2 *)(D + swz(8 * i + lr, 8 * k + 2 * lc));
+        double acc[2] = {c.x, c.y};
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 4)
+          dmma(acc, -D[swz(8 * i + lr, R + kk + lc)], D[swz(8 * k + lr, R + kk + lc)]);
+        *(double2 *)(D + swz(8 * i + lr, 8 * k + 2 * lc)) = make_double2(acc[0], acc[1]);
+      }
+    }
+    __syncthreads();
+  }
+  // ---- W = L^{-1}: diagonal blocks from Wd
+  for (int i = tid; i < 8 * T; i += NT) {
+    const int r = i >> 6, c = i & 63, jb = c >> 3;
+    D[swz(8 * jb + r, c)] = Wd[swz(r, c)];
+  }
+  __syncthreads();
+  // level 8: W_{2p+1,2p} = -W_{2p+1,2p+1} (L_{2p+1,2p} W_{2p,2p}); T in block (2p, 2p+1)
+  if (w < 4) {
+    const int b0 = 16 * w;
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 4) dmma(acc, D[swz(b0 + 8 + lr, b0 + kk + lc)], D[swz(b0 + kk + lc, b0 + lr)]);
+    *(double2 *)(D + swz(b0 + lr, b0 + 8 + 2 * lc)) = make_double2(acc[0], acc[1]);
+  }
+  __syncthreads();
+  if (w < 4) {
+    const int b0 = 16 * w;
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 4)
+      dmma(acc, -D[swz(b0 + 8 + lr, b0 + 8 + kk + lc)], D[swz(b0 + kk + lc, b0 + 8 + lr)]);
+    *(double2 *)(D + swz(b0 + 8 + lr, b0 + 2 * lc)) = make_double2(acc[0], acc[1]);
+  }
+  __syncthreads();
+  // level 16: quads q (base 32q): T = L21 W11 -> rows 32q.., cols 32q+16.. ; W21 = -W22 T
+  {
+    const int q = w >> 2, fi = (w >> 1) & 1, fj = w & 1, b0 = 32 * q;
+    // block-lower k ranges: the strict-upper blocks hold the previous level's T
+    double acc[2] = {0.0, 0.0};
+    for (int kk = 8 * fj; kk < 16; kk += 4)
+      dmma(acc, D[swz(b0 + 16 + 8 * fi + lr, b0 + kk + lc)], D[swz(b0 + kk + lc, b0 + 8 * fj + lr)]);
+    *(double2 *)(D + swz(b0 + 8 * fi + lr, b0 + 16 + 8 * fj + 2 * lc)) = make_double2(acc[0], acc[1]);
+    __syncthreads();
+    acc[0] = acc[1] = 0.0;
+    for (int kk = 0; kk < 8 * (fi + 1); kk += 4)
+      dmma(acc, -D[swz(b0 + 16 + 8 * fi + lr, b0 + 16 + kk + lc)], D[swz(b0 + kk + lc, b0 + 16 + 8 * fj + lr)]);
+    *(double2 *)(D + swz(b0 + 16 + 8 * fi + lr, b0 + 8 * fj + 2 * lc)) = make_double2(acc[0], acc[1]);
+    __syncthreads();
+  }
+  // level 32: T = L21 W11 (32 x 32) -> rows 0..31, cols 32..63 ; W21 = -W22 T
+  {
+    const int fi = w >> 1, fj0 = (w & 1) * 2;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int kk = 8 * fj0; kk < 32; kk += 4) {
+      const double a = D[swz(32 + 8 * fi + lr, kk + lc)];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double bv = D[swz(kk + lc, 8 * (fj0 + e) + lr)];
+        dmma(acc[e], a, (kk >> 3) >= fj0 + e ? bv : 0.0);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      *(double2 *)(D + swz(8 * fi + lr, 32 + 8 * (fj0 + e) + 2 * lc)) = make_double2(acc[e][0], acc[e][1]);
+    __syncthreads();
+    acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.0;
+    for (int kk = 0; kk < 8 * (fi + 1); kk += 4) {
+      const double a = -D[swz(32 + 8 * fi + lr, 32 + kk + lc)];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) dmma(acc[e], a, D[swz(kk + lc, 32 + 8 * (fj0 + e) + lr)]);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      *(double2 *)(D + swz(32 + 8 * fi + lr, 8 * (fj0 + e) + 2 * lc)) = make_double2(acc[e][0], acc[e][1]);
+    __syncthreads();
+  }
+  // strict-upper blocks -> 0 (W is lower triangular)
+  for (int i = tid; i < TD; i += NT) {
+    const int r = i >> 6, c = i & 63;
+    if ((c >> 3) > (r >> 3)) D[swz(r, c)] = 0.0;
+  }
+  __syncthreads();
+}
+
+// sum_t log(ldg[t]) in a fixed order (warp w of the caller; all lanes get it)
+__device__ __forceinline__ double logsum64(const double *ldg) {
+  const int l = threadIdx.x & 31;
+  double v = log(ldg[l]) + log(ldg[l + 32]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+struct Chain {
+  int type;
+  int64_t s, e;  // block range of the partition
+  int nn;        // nodes in the chain
+  int nel;       // eliminated nodes (0..nel-1)
+  int dir;       // +1: node k = block s0 + k;  -1: node k = block e - 1 - k
+  int64_t s0;
+  __device__ int64_t blk(int k) const { return dir > 0 ? s0 + k : e - 1 - k; }
+};
+
+__device__ Chain chain_of(const Level &L, int p) {
+  Chain c;
+  c.s = L.starts[p];
+  c.e = L.starts[p + 1];
+  const int cnt = (int)(c.e - c.s);
+  c.type = L.P == 1 ? P_SEQ : (p == 0 ? P_TOP : (p == L.P - 1 ? P_BOT : P_MID));
+  c.dir = c.type == P_BOT ? -1 : 1;
+  c.s0 = c.type == P_MID ? c.s + 1 : c.s;
+  c.nn = c.type == P_MID ? cnt - 1 : cnt;
+  c.nel = c.type == P_SEQ ? cnt : (c.type == P_MID ? cnt - 2 : cnt - 1);
+  return c;
+}
+
+// coupling block between node k+1 and node k (rows of node k+1): storage and orientation
+__device__ __forceinline__ double *coupling(const Level &L, const Chain &c, int k, int64_t bb, bool *trans) {
+  if (c.dir > 0) {
+    *trans = false;
+    return L.Lo + c.blk(k) * bb;
+  }
+  *trans = true;  // A_{j-1,j} = A_{j,j-1}^T, stored at Lo[j-1]
+  return L.Lo + (c.blk(k) - 1) * bb;
+}
+
+// ---------------------------------------------------------------------------
+// PPOBTAF (Alg. 3-4; Alg. 1 for the last level) of the partitions of one level.
+// ---------------------------------------------------------------------------
+constexpr int F_SMEM_DOUBLES = 3 * TD + AD + 8 * T + T;
+
+extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm) {
+  extern __shared__ __align__(16) double sm[];
+  double *D = sm, *X = D + TD, *B = X + TD, *Ar = B + TD, *Wd = Ar + AD, *ldg = Wd + 8 * T;
+  __shared__ int s_bad;
+  const Level &L = prm.L;
+  const int b = prm.b, a = prm.a, tid = threadIdx.x, w = tid >> 5;
+  const int64_t bb = (int64_t)b * b, ab = (int64_t)a * b;
+  const int m0 = 16 * (w >> 1), n0 = 32 * (w & 1);  // 64 x 64 warp tile
+  const int an0 = 8 * w;                              // 16 x 64 warp tile (arrow rows)
+
+  for (int p = blockIdx.x; p < L.P; p += gridDim.x) {
+    const Chain c = chain_of(L, p);
+    const bool mid = c.type == P_MID;
+    double lsum = 0.0;
+    int firstbad = 0;
+    // running diagonal / arrow blocks of node 0 (and B_{s+1} = A_{s+1,s}^T, Alg. 4 l.1)
+    ld_tile(D, L.D + c.blk(0) * bb, T, b, b, b, false, true);
+    ld_tile(Ar, L.Ar + c.blk(0) * ab, AR, a, b, b, false, false);
+    if (mid) ld_tile(B, L.Lo + c.s * bb, T, b, b, b, true, false);
+    cp_wait_all();
+    __syncthreads();
+    double Aff[2][4][2], Anf[2][1][2], Uac[1][1][2];
+    acc_zero(Aff);
+    acc_zero(Anf);
+    acc_zero(Uac);
+    for (int k = 0; k < c.nel; ++k) {
+      const int64_t bk = c.blk(k);
+      const bool nxt = k + 1 < c.nn;
+      chol_inv64(D, Wd, ldg, &s_bad);  // D <- W_k
+      if (w == 7) {
+        const double ls = logsum64(ldg);
+        if (tid == NT - 32) lsum += ls;  // one thread keeps the partition's partial (fixed order)
+      }
+      if (tid == 0 && s_bad < 64 && s_bad < b && firstbad == 0)
+        firstbad = (int)(L.grow[bk] + s_bad + 1);
+      bool tr = false;
+      double *cpl = nxt ? coupling(L, c, k, bb, &tr) : nullptr;
+      if (nxt) ld_tile(X, cpl, T, b, b, b, tr, false);
+      st_tile(L.D + bk * bb, D, b, b, b, false);  // W_k -> diag slot
+      cp_wait_all();
+      __syncthreads();
+      if (nxt) {  // L_{k+1,k} = A_{k+1,k} W^T  (W lower: (W^T)[kk][n] = 0 for kk > n)
+        double acc[2][4][2];
+        acc_zero(acc);
+        mma<2, 4, false, true, false>(acc, X, D, m0, n0, 0, n0 + 32);
+        __syncthreads();
+        acc_st_smem(X, acc, m0, n0, 1.0);
+        acc_st_global(cpl, acc, b, b, b, m0, n0, tr, 1.0);
+      }
+      if (mid) {  // L_{f,k} = B_k W^T (Alg. 4, fill-in TRSM)
+        double acc[2][4][2];
+        acc_zero(acc);
+        mma<2, 4, false, true, false>(acc, B, D, m0, n0, 0, n0 + 32);
+        __syncthreads();
+        acc_st_smem(B, acc, m0, n0, 1.0);
+        acc_st_global(L.Bf + bk * bb, acc, b, b, b, m0, n0, false, 1.0);
+      }
+      if (a > 0) {  // L_{n,k} = A_{n,k} W^T
+        double acc[2][1][2];
+        acc_zero(acc);
+        mma<2, 1, false, true, false>(acc, Ar, D, 0, an0, 0, an0 + 8);
+        __syncthreads();
+        acc_st_smem(Ar, acc, 0, an0, 1.0);
+        acc_st_global(L.Ar + bk * ab, acc, b, a, b, 0, an0, false, 1.0);
+      }
+      __syncthreads();
+      // ---- Schur updates (Alg. 1 l.5-7, Alg. 4 l.9-12); W is dead
+      if (nxt) {  // A_{k+1,k+1} - L_{k+1,k} L_{k+1,k}^T -> D
+        double acc[2][4][2];
+        acc_ld(acc, L.D + c.blk(k + 1) * bb, b, b, b, m0, n0, true);
+        mma<2, 4, false, true, true>(acc, X, X, m0, n0, 0, T);
+        acc_st_smem(D, acc, m0, n0, 1.0);
+      }
+      if (a > 0) {
+        if (w < 4) mma<1, 1, false, true, true>(Uac, Ar, Ar, 8 * (w >> 1), 8 * (w & 1), 0, T);  // U -= Ln Ln^T
+        if (mid) mma<2, 1, false, true, true>(Anf, Ar, B, 0, an0, 0, T);                      // A_nf -= Ln B^T
+      }
+      if (mid) mma<2, 4, false, true, true>(Aff, B, B, m0, n0, 0, T);  // A_ff -= B B^T
+      double accA[2][1][2];
+      if (a > 0 && nxt) {  // A_{n,k+1} - L_{n,k} L_{k+1,k}^T
+        acc_ld(accA, L.Ar + c.blk(k + 1) * ab, b, a, b, 0, an0, false);
+        mma<2, 1, false, true, true>(accA, Ar, X, 0, an0, 0, T);
+      }
+      double accB[2][4][2];
+      if (mid && nxt) {  // B_{k+1} = -B_k L_{k+1,k}^T
+        acc_zero(accB);
+        mma<2, 4, false, true, true>(accB, B, X, m0, n0, 0, T);
+      }
+      __syncthreads();
+      if (a > 0 && nxt) acc_st_smem(Ar, accA, 0, an0, 1.0);
+      if (mid && nxt) acc_st_smem(B, accB, m0, n0, 1.0);
+      __syncthreads();
+    }
+    if (tid == 0 && firstbad) record_info(prm.info, firstbad);
+    if (tid == NT - 32) L.ldp[p] = lsum;
+    const int64_t aa = (int64_t)a * a;
+    if (c.type != P_SEQ) {
+      // ---- boundary blocks -> the reduced system (reading R9 / R14 order)
+      const int ib = c.type == P_TOP ? 0 : (c.type == P_MID ? 2 * p : 2 * p - 1);
+      st_tile(L.Dn + ib * bb, D, b, b, b, false);
+      if (a > 0) st_tile(L.Arn + ib * ab, Ar, a, b, b, false);
+      if (c.type != P_BOT) cp_block(L.Lon + (int64_t)(c.type == P_TOP ? 0 : 2 * p) * bb, L.Lo + (c.e - 1) * bb, bb);
+      if (mid) {
+        // A_ff + sum(-B B^T), A_{n,f} + sum(-Ln B^T), (L_p, F_p) coupling = B_{e-1}^T
+        double acc[2][4][2];
+        acc_ld(acc, L.D + c.s * bb, b, b, b, m0, n0, false);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[i][j][0] += Aff[i][j][0];
+            acc[i][j][1] += Aff[i][j][1];
+          }
+        acc_st_global(L.Dn + (2 * p - 1) * bb, acc, b, b, b, m0, n0, false, 1.0);
+        if (a > 0) {
+          double acn[2][1][2];
+          acc_ld(acn, L.Ar + c.s * ab, b, a, b, 0, an0, false);
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            acn[i][0][0] += Anf[i][0][0];
+            acn[i][0][1] += Anf[i][0][1];
+          }
+          acc_st_global(L.Arn + (2 * p - 1) * ab, acn, b, a, b, 0, an0, false, 1.0);
+        }
+        st_tile(L.Lon + (int64_t)(2 * p - 1) * bb, B, b, b, b, true);
+      }
+      if (a > 0 && w < 4) acc_st_global(L.U + p * aa, Uac, a, a, a, 8 * (w >> 1), 8 * (w & 1), false, 1.0);
+    } else if (a > 0) {
+      // ---- tip (Alg. 1 l.12): L_nn = chol(A_nn + sum of every level's U), X_nn = W^T W (Alg. 2 l.1)
+      __syncthreads();
+      ld_tile(D, prm.tip, T, a, a, a, false, true);
+      __syncthreads();
+      if (w < 4) {
+        const int l = tid & 31, mm = 8 * (w >> 1) + (l >> 2), nn2 = 8 * (w & 1) + 2 * (l & 3);
+        D[swz(mm, nn2)] += Uac[0][0][0];
+        D[swz(mm, nn2 + 1)] += Uac[0][0][1];
+      }
+      __syncthreads();
+      chol_inv64(D, Wd, ldg, &s_bad);
+      if (w == 7) {
+        const double ls = logsum64(ldg);
+        if (tid == NT - 32) lsum += ls;
+      }
+      if (tid == 0 && s_bad < a) record_info(prm.info, (int)(prm.tip_row + s_bad + 1));
+      if (w < 4) {
+        double acc[1][1][2];
+        acc_zero(acc);
+        mma<1, 1, true, false, false>(acc, D, D, 8 * (w >> 1), 8 * (w & 1), 0, T);
+        acc_st_global(prm.tip, acc, a, a, a, 8 * (w >> 1), 8 * (w & 1), false, 1.0);
+      }
+      if (tid == NT - 32) L.ldp[p] = lsum;
+    }
+    __syncthreads();
+  }
+  // ---- last CTA out: tip += sum_p U_p (partition order, reading R8); last level: log det
+  __shared__ int s_last;
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(L.done, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (L.P > 1 && a > 0) {
+    for (int i = tid; i < a * a; i += NT) {
+      double v = prm.tip[i];
+      for (int q = 0; q < L.P; ++q) v += *(volatile double *)(L.U + (int64_t)q * a * a + i);
+      prm.tip[i] = v;
+    }
+  }
+  if (L.P == 1 && tid == 0) {
+    double s = 0.0;
+    for (int i = 0; i < prm.n_ldp; ++i) s += *(volatile const double *)(prm.ldp_all + i);
+    const int inf = *(volatile int *)prm.info;
+    *prm.logdet = inf ? __longlong_as_double(0x7ff8000000000000ULL) : 2.0 * s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// PPOBTASI (Alg. 5-6; Alg. 2 for the last level), W-form:
+//   Lc~ = L_{k+1,k} W, Ln~ = L_{n,k} W, Lf~ = L_{f,k} W, Lam = W^T W
+//   X_{k+1,k} = -(X_{k+1,k+1} Lc~ + X_{n,k+1}^T Ln~ + Q_{k+1}^T Lf~)
+//   Q_k       = -(Q_{k+1} Lc~ + X_ff Lf~ + X_nf^T Ln~)                 (middle)
+//   X_{n,k}   = -(X_{n,k+1} Lc~ + X_nn Ln~ + X_nf Lf~)
+//   X_kk      = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~
+// (reading R11: l.7's L_{0,i} is the factor fill-in block; Q_k = X_{f,k}).
+// ---------------------------------------------------------------------------
+constexpr int I_SMEM_DOUBLES = 6 * TD + 4 * AD;
+
+extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm) {
+  extern __shared__ __align__(16) double sm[];
+  double *W = sm, *Lc = W + TD, *Lf = Lc + TD, *Xd = Lf + TD, *Q = Xd + TD, *Xff = Q + TD;
+  double *Ln = Xff + TD, *Xn = Ln + AD, *Xnf = Xn + AD, *Xnn = Xnf + AD;
+  const Level &L = prm.L;
+  const int b = prm.b, a = prm.a, tid = threadIdx.x, w = tid >> 5;
+  const int64_t bb = (int64_t)b * b, ab = (int64_t)a * b;
+  const int m0 = 16 * (w >> 1), n0 = 32 * (w & 1);
+  const int an0 = 8 * w;
+
+  for (int p = blockIdx.x; p < L.P; p += gridDim.x) {
+    const Chain c = chain_of(L, p);
+    const bool mid = c.type == P_MID;
+    // ---- seeds: the boundary blocks of X from the solved reduced system (reading R10)
+    if (a > 0) ld_tile(Xnn, prm.tip, AR, a, a, a, false, true);
+    if (c.type != P_SEQ) {
+      const int ib = c.type == P_TOP ? 0 : (c.type == P_MID ? 2 * p : 2 * p - 1);
+      const int64_t bblk = c.type == P_BOT ? c.s : c.e - 1;  // the boundary block of the chain
+      ld_tile(Xd, L.Dn + ib * bb, T, b, b, b, false, true);
+      if (a > 0) ld_tile(Xn, L.Arn + ib * ab, AR, a, b, b, false, false);
+      cp_block(L.D + bblk * bb, L.Dn + ib * bb, bb);
+      if (a > 0) cp_block(L.Ar + bblk * ab, L.Arn + ib * ab, ab);
+      if (c.type != P_BOT) cp_block(L.Lo + (c.e - 1) * bb, L.Lon + (int64_t)(c.type == P_TOP ? 0 : 2 * p) * bb, bb);
+      if (mid) {
+        ld_tile(Xff, L.Dn + (2 * p - 1) * bb, T, b, b, b, false, true);
+        if (a > 0) ld_tile(Xnf, L.Arn + (2 * p - 1) * ab, AR, a, b, b, false, false);
+        ld_tile(Q, L.Lon + (int64_t)(2 * p - 1) * bb, T, b, b, b, true, false);  // Q_{e-1} = X_{f,l} = X_r(L,F)^T
+        cp_block(L.D + c.s * bb, L.Dn + (2 * p - 1) * bb, bb);
+        if (a > 0) cp_block(L.Ar + c.s * ab, L.Arn + (2 * p - 1) * ab, ab);
+      }
+    }
+    cp_wait_all();
+    __syncthreads();
+    for (int k = c.nel - 1; k >= 0; --k) {
+      const int64_t bk = c.blk(k);
+      const bool nxt = k + 1 < c.nn;
+      bool tr = false;
+      double *cpl = nxt ? coupling(L, c, k, bb, &tr) : nullptr;
+      ld_tile(W, L.D + bk * bb, T, b, b, b, false, true);
+      if (nxt) ld_tile(Lc, cpl, T, b, b, b, tr, false);
+      if (mid) ld_tile(Lf, L.Bf + bk * bb, T, b, b, b, false, false);
+      if (a > 0) ld_tile(Ln, L.Ar + bk * ab, AR, a, b, b, false, false);
+      cp_wait_all();
+      __syncthreads();
+      // ---- Lc~, Lf~, Ln~ (W lower: W[kk][n] = 0 for kk < n) and Lam = W^T W
+      double aX[2][4][2];
+      acc_zero(aX);
+      mma<2, 4, true, false, false>(aX, W, W, m0, n0, max(m0, n0), T);
+      {
+        double aL[2][4][2], aF[2][4][2], aN[2][1][2];
+        if (nxt) {
+          acc_zero(aL);
+          mma<2, 4, false, false, false>(aL, Lc, W, m0, n0, n0, T);
+        }
+        if (mid) {
+          acc_zero(aF);
+          mma<2, 4, false, false, false>(aF, Lf, W, m0, n0, n0, T);
+        }
+        if (a > 0) {
+          acc_zero(aN);
+          mma<2, 1, false, false, false>(aN, Ln, W, 0, an0, an0, T);
+        }
+        __syncthreads();
+        if (nxt) acc_st_smem(Lc, aL, m0, n0, 1.0);
+        if (mid) acc_st_smem(Lf, aF, m0, n0, 1.0);
+        if (a > 0) acc_st_smem(Ln, aN, 0, an0, 1.0);
+      }
+      __syncthreads();
+      // ---- X_{k+1,k}, Q_k, X_{n,k}  (W is dead: its buffer receives X_{k+1,k})
+      {
+        double aA[2][4][2], aB[2][4][2], aN[2][1][2];
+        if (nxt) {
+          acc_zero(aA);
+          mma<2, 4, false, false, false>(aA, Xd, Lc, m0, n0, 0, T);
+          if (a > 0) mma<2, 4, true, false, false>(aA, Xn, Ln, m0, n0, 0, AR);
+          if (mid) mma<2, 4, true, false, false>(aA, Q, Lf, m0, n0, 0, T);
+        }
+        if (mid) {
+          acc_zero(aB);
+          mma<2, 4, false, false, false>(aB, Q, Lc, m0, n0, 0, T);
+          mma<2, 4, false, false, false>(aB, Xff, Lf, m0, n0, 0, T);
+          if (a > 0) mma<2, 4, true, false, false>(aB, Xnf, Ln, m0, n0, 0, AR);
+        }
+        if (a > 0) {
+          acc_zero(aN);
+          if (nxt) mma<2, 1, false, false, false>(aN, Xn, Lc, 0, an0, 0, T);
+          mma<2, 1, false, false, false>(aN, Xnn, Ln, 0, an0, 0, AR);
+          if (mid) mma<2, 1, false, false, false>(aN, Xnf, Lf, 0, an0, 0, T);
+        }
+        __syncthreads();
+        if (nxt) {
+          acc_st_smem(W, aA, m0, n0, -1.0);
+          acc_st_global(cpl, aA, b, b, b, m0, n0, tr, -1.0);
+        }
+        if (mid) acc_st_smem(Q, aB, m0, n0, -1.0);
+        if (a > 0) {
+          acc_st_smem(Xn, aN, 0, an0, -1.0);
+          acc_st_global(L.Ar + bk * ab, aN, b, a, b, 0, an0, false, -1.0);
+        }
+      }
+      __syncthreads();
+      // ---- X_kk = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~
+      if (nxt) mma<2, 4, true, false, true>(aX, W, Lc, m0, n0, 0, T);
+      if (a > 0) mma<2, 4, true, false, true>(aX, Xn, Ln, m0, n0, 0, AR);
+      if (mid) mma<2, 4, true, false, true>(aX, Q, Lf, m0, n0, 0, T);
+      acc_st_smem(Xd, aX, m0, n0, 1.0);
+      acc_st_global(L.D + bk * bb, aX, b, b, b, m0, n0, false, 1.0);
+      __syncthreads();
+    }
+    if (mid) {  // X_{s+1,s} = Q_{s+1}^T (reading R10)
+      st_tile(L.Lo + c.s * bb, Q, b, b, b, true);
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace dev
+
+// ---------------------------------------------------------------------------
+// Host: plan and launches
+// ---------------------------------------------------------------------------
+bool make_plan(int64_t n, int64_t b, int64_t a, const std::vector<int> &Ps, Plan &pl) {
+  if (n < 1 || b < 1 || b > kMaxB || a < 0 || a > kMaxA) return false;
+  pl = Plan();
+  pl.n = n;
+  pl.b = b;
+  pl.a = a;
+  pl.Ps = Ps;
+  const int nl = (int)Ps.size();
+  std::vector<int64_t> grow0(n);
+  for (int64_t i = 0; i < n; ++i) grow0[i] = i * b;
+  pl.grow.push_back(grow0);
+  pl.nlev.push_back(n);
+  int64_t m = n;
+  for (int l = 0; l < nl; ++l) {
+    const int P = Ps[l];
+    std::vector<int64_t> st;
+    if (P < 2 || !plan_partitions_ends(m, P, 1.0, st)) return false;
+    for (int p = 0; p < P; ++p) {  // sizes: ends >= 1, middles >= 2
+      const int64_t cnt = st[p + 1] - st[p];
+      if (cnt < ((p == 0 || p == P - 1) ? 1 : 2)) return false;
+    }
+    pl.starts.push_back(st);
+    const int64_t nr = 2 * (int64_t)P - 2;
+    const std::vector<int64_t> &g = pl.grow.back();
+    std::vector<int64_t> gr(nr);
+    gr[0] = g[st[1] - 1];
+    for (int p = 1; p < P; ++p) {
+      gr[2 * p - 1] = g[st[p]];
+      if (p < P - 1) gr[2 * p] = g[st[p + 1] - 1];
+    }
+    pl.grow.push_back(gr);
+    pl.nlev.push_back(nr);
+    m = nr;
+  }
+  // workspace: per level l >= 1 arrays D, Lo, Ar; per partitioned level Bf, U, ldp; tables; counters
+  int64_t o = 0;
+  auto take = [&](int64_t d) {
+    const int64_t r = o;
+    o += (std::max<int64_t>(d, 1) + 31) / 32 * 32;
+    return r;
+  };
+  const int L = nl + 1;
+  pl.off_D.assign(L, -1);
+  pl.off_Lo.assign(L, -1);
+  pl.off_Ar.assign(L, -1);
+  pl.off_Bf.assign(L, -1);
+  pl.off_U.assign(L, -1);
+  pl.off_ldp.assign(L, -1);
+  for (int l = 1; l < L; ++l) {
+    const int64_t nr = pl.nlev[l];
+    pl.off_D[l] = take(nr * b * b);
+    pl.off_Lo[l] = take(std::max<int64_t>(nr - 1, 1) * b * b);
+    pl.off_Ar[l] = take(nr * a * b);
+  }
+  for (int l = 0; l < L; ++l) {
+    const int P = l < nl ? Ps[l] : 1;
+    if (l < nl) {
+      pl.off_Bf[l] = take(pl.nlev[l] * b * b);
+      pl.off_U[l] = take((int64_t)P * a * a);
+    }
+  }
+  // all log-det partials contiguous (summed in level order, partition order)
+  {
+    int64_t tot = 0;
+    for (int l = 0; l < L; ++l) tot += l < nl ? Ps[l] : 1;
+    const int64_t base = take(tot);
+    int64_t q = base;
+    for (int l = 0; l < L; ++l) {
+      pl.off_ldp[l] = q;
+      q += l < nl ? Ps[l] : 1;
+    }
+  }
+  int64_t t = 0;  // offsets into the plan's index table (int64, library-owned device copy)
+  pl.off_starts.assign(L, -1);
+  pl.off_grow.assign(L, -1);
+  for (int l = 0; l < L; ++l) {
+    pl.off_starts[l] = t;
+    t += l < nl ? Ps[l] + 1 : 2;
+    pl.off_grow[l] = t;
+    t += pl.nlev[l];
+  }
+  pl.off_ctr = take(L);
+  pl.ws_doubles = o;
+  return true;
+}
+
+std::vector<int64_t> plan_tables(const Plan &pl) {
+  std::vector<int64_t> tab;
+  const int nl = (int)pl.Ps.size();
+  for (int l = 0; l <= nl; ++l) {
+    if (l < nl)
+      tab.insert(tab.end(), pl.starts[l].begin(), pl.starts[l].end());
+    else {
+      tab.push_back(0);
+      tab.push_back(pl.nlev[l]);
+    }
+    tab.insert(tab.end(), pl.grow[l].begin(), pl.grow[l].end());
+  }
+  return tab;
+}
+
+// Level 0: one partition per SM (the chain of ~n/148 blocks is the level's
+// critical path; the factor kernel's 2 CTAs per SM overlap their Cholesky
+// latencies).  Deeper levels: short partitions (~6 blocks) until the reduced
+// system has <= 12 blocks, which the last level solves as one chain.
+std::vector<int> auto_plan(int64_t n, int64_t b, int sms) {
+  (void)b;
+  std::vector<int> Ps;
+  int64_t m = n;
+  const int64_t seq_max = 12;
+  bool first = true;
+  while (m > seq_max) {
+    int64_t P = first ? std::min<int64_t>(sms, m / 8) : m / 6;
+    if (P < 2) break;
+    std::vector<int64_t> st;
+    while (P >= 2 && !plan_partitions_ends(m, (int)P, 1.0, st)) --P;
+    if (P < 2) break;
+    Ps.push_back((int)P);
+    m = 2 * P - 2;
+    first = false;
+    if (Ps.size() > 12) break;
+  }
+  return Ps;
+}
+
+int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, double *arrow, double *tip, double *ws,
+        int *d_info, double *d_logdet, int sms, cudaStream_t st, int *launches) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(dev::sb_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dev::F_SMEM_DOUBLES * 8) != cudaSuccess ||
+        cudaFuncSetAttribute(dev::sb_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dev::I_SMEM_DOUBLES * 8) != cudaSuccess)
+      return 1;
+    attr = true;
+  }
+  const int nl = (int)pl.Ps.size();
+  const int L = nl + 1;
+  if (cudaMemsetAsync(ws + pl.off_ctr, 0, (size_t)L * sizeof(int), st) != cudaSuccess ||
+      cudaMemsetAsync(d_info, 0, sizeof(int), st) != cudaSuccess)
+    return 1;
+  const int64_t b = pl.b, a = pl.a;
+  std::vector<Params> prm(L);
+  for (int l = 0; l < L; ++l) {
+    Params &q = prm[l];
+    Level &v = q.L;
+    v.n = pl.nlev[l];
+    v.P = l < nl ? pl.Ps[l] : 1;
+    v.starts = d_tab + pl.off_starts[l];
+    v.grow = d_tab + pl.off_grow[l];
+    if (l == 0) {
+      v.D = diag;
+      v.Lo = lower;
+      v.Ar = arrow;
+    } else {
+      v.D = ws + pl.off_D[l];
+      v.Lo = ws + pl.off_Lo[l];
+      v.Ar = ws + pl.off_Ar[l];
+    }
+    v.Bf = l < nl ? ws + pl.off_Bf[l] : nullptr;
+    v.U = l < nl ? ws + pl.off_U[l] : nullptr;
+    v.ldp = ws + pl.off_ldp[l];
+    v.done = (int *)(ws + pl.off_ctr) + l;
+    if (l < nl) {
+      v.Dn = ws + pl.off_D[l + 1];
+      v.Lon = ws + pl.off_Lo[l + 1];
+      v.Arn = ws + pl.off_Ar[l + 1];
+    } else {
+      v.Dn = v.Lon = v.Arn = nullptr;
+    }
+    q.tip = tip;
+    q.b = (int)b;
+    q.a = (int)a;
+    q.info = d_info;
+    q.logdet = d_logdet;
+    q.ldp_all = ws + pl.off_ldp[0];
+    int64_t tot = 0;
+    for (int k = 0; k < L; ++k) tot += k < nl ? pl.Ps[k] : 1;
+    q.n_ldp = (int)tot;
+    q.tip_row = pl.n * b;
+  }
+  int nlaunch = 0;
+  for (int l = 0; l < L; ++l) {
+    const int grid = std::max(1, std::min(prm[l].L.P, 2 * sms));
+    dev::sb_factor_kernel<<<grid, dev::NT, dev::F_SMEM_DOUBLES * 8, st>>>(prm[l]);
+    ++nlaunch;
+  }
+  for (int l = L - 1; l >= 0; --l) {
+    const int grid = std::max(1, std::min(prm[l].L.P, sms));
+    dev::sb_inverse_kernel<<<grid, dev::NT, dev::I_SMEM_DOUBLES * 8, st>>>(prm[l]);
+    ++nlaunch;
+  }
+  if (launches) *launches += nlaunch;
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+}  // namespace sb
+}  // namespace serinv

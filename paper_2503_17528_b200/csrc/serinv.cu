@@ -24,6 +24,7 @@
 #include "task.h"
 
 #include "exec.h"
+#include "sb.h"
 
 using namespace serinv;
 
@@ -59,7 +60,19 @@ inline std::string opt_string() {
 
 }  // namespace
 
+namespace {
+// a cached small-block engine plan and its device index table (serinv_sb_*)
+struct SbEntry {
+  sb::Plan pl;
+  int64_t *d_tab = nullptr;
+  ~SbEntry() {
+    if (d_tab) cudaFree(d_tab);
+  }
+};
+}  // namespace
+
 struct serinv_ctx {
+  std::map<std::vector<int64_t>, std::unique_ptr<SbEntry>> sb_cache;
   int device = 0;
   int sms = 0;
   int grid = 0;
@@ -308,6 +321,7 @@ int serinv_destroy(serinv_handle_t h) {
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
   h->cache.clear();
+  h->sb_cache.clear();
   if (h->dummy) cudaFree(h->dummy);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamDestroy(h->s_out);
@@ -992,6 +1006,80 @@ int serinv_set_trace(serinv_handle_t h, void *d_trace, size_t bytes) {
   if (d_trace && ((uintptr_t)d_trace & 7)) return SERINV_ERR_ALIGN;
   h->trace = (unsigned long long *)d_trace;
   h->trace_cap = d_trace ? bytes / 96 : 0;  // 4 + 8 u64 per task
+  return SERINV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// small-block engine (sb.cu)
+// ---------------------------------------------------------------------------
+static int sb_levels(int64_t n, int64_t b, int64_t a, int nlev, const int *Ps, std::vector<int> &v) {
+  if (n < 1 || b < 1 || a < 0) return SERINV_ERR_SHAPE;
+  if (b > sb::kMaxB || a > sb::kMaxA) return SERINV_ERR_SHAPE;
+  if (nlev < 0) {
+    v = sb::auto_plan(n, b, 148);  // B200: 148 SMs (fixed, so the ws query needs no device)
+  } else {
+    if (nlev > 0 && !Ps) return -5;
+    v.assign(Ps, Ps + nlev);
+  }
+  return SERINV_OK;
+}
+
+int serinv_sb_auto_plan(int64_t n, int64_t b, int64_t a, int *Ps, int cap) {
+  if (!Ps || cap < 0) return -4;
+  std::vector<int> v;
+  int rc = sb_levels(n, b, a, -1, nullptr, v);
+  if (rc) return -rc;
+  for (int i = 0; i < (int)v.size() && i < cap; ++i) Ps[i] = v[i];
+  return (int)v.size();
+}
+
+int serinv_sb_ws(int64_t n, int64_t b, int64_t a, int nlev, const int *Ps, size_t *bytes) {
+  if (!bytes) return -6;
+  std::vector<int> v;
+  int rc = sb_levels(n, b, a, nlev, Ps, v);
+  if (rc) return rc;
+  sb::Plan pl;
+  if (!sb::make_plan(n, b, a, v, pl)) return SERINV_ERR_PLAN;
+  *bytes = (size_t)pl.ws_doubles * 8;
+  return SERINV_OK;
+}
+
+int serinv_sb_selinv(serinv_handle_t h, const serinv_bta_t *A, int nlev, const int *Ps, void *d_ws, size_t ws_bytes,
+                     int *d_info, double *d_logdet, void *stream) {
+  if (!h) return SERINV_ERR_HANDLE;
+  int rc = check_bta(A);
+  if (rc) return rc;
+  if (!d_info) return -8;
+  if (!d_ws || !aligned16(d_ws)) return SERINV_ERR_WS;
+  if (cudaSetDevice(h->device) != cudaSuccess) return SERINV_ERR_CUDA;
+  std::vector<int> v;
+  rc = sb_levels(A->n, A->b, A->a, nlev, Ps, v);
+  if (rc) return rc;
+  std::vector<int64_t> key{A->n, A->b, A->a};
+  key.insert(key.end(), v.begin(), v.end());
+  SbEntry *e = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    auto it = h->sb_cache.find(key);
+    if (it == h->sb_cache.end()) {
+      std::unique_ptr<SbEntry> ne(new SbEntry);
+      if (!sb::make_plan(A->n, A->b, A->a, v, ne->pl)) return SERINV_ERR_PLAN;
+      const std::vector<int64_t> tab = sb::plan_tables(ne->pl);
+      if (cudaMalloc(&ne->d_tab, tab.size() * sizeof(int64_t)) != cudaSuccess ||
+          cudaMemcpy(ne->d_tab, tab.data(), tab.size() * sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess)
+        return SERINV_ERR_CUDA;
+      it = h->sb_cache.emplace(key, std::move(ne)).first;
+    }
+    e = it->second.get();
+  }
+  if ((int64_t)ws_bytes < e->pl.ws_doubles * 8) return SERINV_ERR_WS;
+  cudaStream_t st = (cudaStream_t)stream;
+  CallGuard guard(h, st);
+  int nl = 0;
+  if (sb::run(e->pl, e->d_tab, A->diag, A->lower, A->arrow, A->tip, (double *)d_ws, d_info,
+              d_logdet ? d_logdet : h->dummy, h->sms, st, &nl))
+    return SERINV_ERR_CUDA;
+  h->last_launches += nl;
   return SERINV_OK;
 }
 
