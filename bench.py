@@ -67,14 +67,15 @@ def src_sha() -> str:
     return h.hexdigest()[:16]
 
 
-def ncu_traffic(config):
+def ncu_traffic(config, engine="exec"):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the executor from a committed
     ncu --set full capture of this config (profiles/r*/ncu_<C>/summary.json) whose src_sha
     matches the library sources being timed; else (None, reason)."""
     import glob
     sha = src_sha()
     seen = []
-    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_{config}", "summary.json")), reverse=True):
+    sub = f"ncu_{config}" if engine == "exec" else f"ncu_{config}_{engine}"
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", sub, "summary.json")), reverse=True):
         try:
             with open(p) as f:
                 d = json.load(f)
@@ -127,6 +128,9 @@ def parse():
                          "'auto' = distributed.auto_r(b)")
     ap.add_argument("--q", default="auto",
                     help="N > 1: sub-partitions per rank (serinv_ppobtaf_q); 'auto' = serinv_dist_auto_q")
+    ap.add_argument("--engine", default="auto", choices=["auto", "exec", "sb"],
+                    help="N = 1: 'sb' = the small-block engine (serinv_sb_selinv, b <= 64, a <= 16), "
+                         "'exec' = the tile-task executor; 'auto' = sb where it applies")
     ap.add_argument("--partitions", default="auto",
                     help="N = 1: intra-GPU partitions, e.g. 1 (sequential), 8, 256x16 (nested); "
                          "'auto' = the library's plan (serinv_auto_partitions)")
@@ -416,14 +420,21 @@ def main():
     # ---- inputs resident in HBM (pristine copy restored between steps, untimed); the
     # generator's torch twin builds G1 directly in HBM, bit-identical to btagen.g1
     Ps = [1]
+    use_sb = (not dpath and (args.engine == "sb" or (args.engine == "auto" and b <= 64 and a <= 16)))
     if not dpath:
-        Ps = (sb.auto_partitions(n, b) if args.partitions == "auto"
-              else [int(x) for x in args.partitions.split("x")])
+        if use_sb:
+            Ps = (sb.sb_auto_plan(n, b, a) if args.partitions == "auto"
+                  else [int(x) for x in args.partitions.split("x") if int(x) > 1])
+        else:
+            Ps = (sb.auto_partitions(n, b) if args.partitions == "auto"
+                  else [int(x) for x in args.partitions.split("x")])
         pristine = btagen.g1_torch(0, n, b, a, device=f"cuda:{local}")
         work = {k: v.clone() for k, v in pristine.items()}
         W = (work["diag"], work["lower"], work["arrow"], work["tip"])
 
         def step():
+            if use_sb:
+                return sb.selinv_sb(*W, Ps, handle=h, check=False)
             if Ps == [1]:
                 return sb.selinv(*W, handle=h, check=False)
             return sb.pselinv(*W, Ps, handle=h, check=False)
@@ -481,6 +492,7 @@ def main():
     sec_per_step = st["seconds_median"]
     value = fl / sec_per_step / 1e12
 
+    step_name = ("serinv_sb_selinv" if use_sb else "serinv_selinv" if Ps == [1] else "serinv_pselinv_nested")
     # ---- phases: factorisation and selected inversion timed as separate launches
     phases = None
     if not args.no_phases and not dpath:
@@ -504,7 +516,7 @@ def main():
         phases = {"pobtaf": stats_line(tf, fl_f), "pobtasi": stats_line(ts, fl_si),
                   "pobtaf_plus_pobtasi": stats_line([x + y for x, y in zip(tf, ts)], fl),
                   "fused_selinv": {"seconds_median": st["seconds_median"], "tflops_median": st["tflops_median"],
-                                   "step": "serinv_selinv" if Ps == [1] else "serinv_pselinv_nested"},
+                                   "step": step_name},
                   "note": "pobtaf / pobtasi: standalone serinv_pobtaf and serinv_pobtasi launches (Alg. 1 and "
                           "Alg. 2 order); the headline value is the fused one-launch step"}
     elif not args.no_phases and dpath:
@@ -548,7 +560,7 @@ def main():
             barrier()
             torch.cuda.synchronize()
             e0 = ev()
-            if not dpath and Ps == [1]:
+            if not dpath and Ps == [1] and not use_sb:
                 # public API with host buffers: H2D / D2H stream with the computation
                 sb.selinv_host(pinned, work, out, handle=h, check=False)
             else:  # partitioned / distributed: H2D, the step, D2H on the stream
@@ -573,7 +585,7 @@ def main():
         e2e = {"value": round(fl / em / 1e12, 4), "unit": "TFLOP/s",
                "h2d_bytes_per_step": h2d_all, "d2h_bytes_per_step": h2d_all + 8 * world,
                "ms_per_step": round(em * 1e3, 3),
-               "api": "serinv_selinv_host (streaming H2D/D2H)" if (not dpath and Ps == [1]) else
+               "api": "serinv_selinv_host (streaming H2D/D2H)" if (not dpath and Ps == [1] and not use_sb) else
                       "H2D + step + D2H on the library stream"}
 
     # ---- CPU baseline (oracle as it stands), rank 0, N = 1 only, bounded sample
@@ -585,7 +597,8 @@ def main():
                          f"{dt:.1f} s"}
 
     if rank == 0:
-        traffic, traffic_src = ncu_traffic(args.config) if not dpath else (None, "distributed run")
+        traffic, traffic_src = (ncu_traffic(args.config, "sb" if use_sb else "exec") if not dpath
+                                else (None, "distributed run"))
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": N,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec_per_step * 1e3, 3),
@@ -594,8 +607,10 @@ def main():
             "config": bench_config(args.config, cfg),
             "plan": {"n_global": n, "end_ratio_r": r_end if dpath else None,
                      "parallelism": f"partitions{world}x{Q}" if dpath else
-                     ("single" if Ps == [1] else "intra-GPU partitions " + "x".join(map(str, Ps))),
-                     "step": ("POBTAF+POBTASI (serinv_selinv)" if Ps == [1] else
+                     ("small-block engine, partitions per level " + "x".join(map(str, Ps)) if use_sb else
+                      "single" if Ps == [1] else "intra-GPU partitions " + "x".join(map(str, Ps))),
+                     "step": ("PPOBTAF+POBTARSSI+PPOBTASI, nested, 2 kernels per level (serinv_sb_selinv)"
+                              if use_sb else "POBTAF+POBTASI (serinv_selinv)" if Ps == [1] else
                               "PPOBTAF+POBTARSSI+PPOBTASI in one launch (serinv_pselinv_nested)")
                              if not dpath else
                              "serinv_ppobtaf (incl. the library's ncclAllGather) + serinv_ppobtasi"},
@@ -606,7 +621,8 @@ def main():
             "roofline": {"bound": "tensor", "achieved": round(value / N, 4), "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": round(value / N / FP64_PEAK_TFLOPS, 4),
                          "traffic": traffic, "traffic_source": traffic_src,
-                         "kernel": "serinv_exec_kernel (persistent, 1 launch per step)",
+                         "kernel": ("sb_factor_kernel + sb_inverse_kernel (all launches of the step, one stream)"
+                                    if use_sb else "serinv_exec_kernel (persistent, 1 launch per step)"),
                          "peak_source": "measured DMMA f64 peak, profiles/fp64_peaks_r01.json "
                                         "(MEASURED_PEAKS.json has no FP64 entry)"},
             # small-b evidence: algorithmic HBM bytes per step / step time

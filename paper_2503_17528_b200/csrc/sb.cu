@@ -238,19 +238,19 @@ __device__ __forceinline__ void acc_st_global(double *g, const double (&acc)[MI]
 // right-looking on 8-column panels: warp 0 factors the 8 x 8 diagonal block in
 // registers (pivots, the product-form inverse W_jj alongside), all warps the
 // panel TRSM (with W_jj) and the trailing update by DMMA; then W from the
-// blocks: W_21 = -W_22 L_21 W_11 on 8 / 16 / 32 levels.  *s_bad = first
-// non-positive (or NaN) pivot index, 64 if none.  Called by all NT threads.
+// blocks: W_21 = -W_22 L_21 W_11 on 8 / 16 / 32 levels.  *s_bad = 2 x the first
+// non-positive pivot index + 1 if that pivot is NaN; 128 if none.  Called by all NT threads.
 // ---------------------------------------------------------------------------
 __device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad) {
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, lr = l >> 2, lc = l & 3;
-  if (tid == 0) *s_bad = 64;
+  if (tid == 0) *s_bad = 128;
   for (int j = 0; j < 8; ++j) {
     const int R = 8 * j;
     if (w == 0) {
       const int c0 = 2 * lc;
       double a0 = D[swz(R + lr, R + c0)], a1 = D[swz(R + lr, R + c0 + 1)];
       double w0 = (lr == c0) ? 1.0 : 0.0, w1 = (lr == c0 + 1) ? 1.0 : 0.0;
-      int bad = 64;
+      int bad = 128;  // 2 * (first failing pivot) + (pivot is NaN): genuine failures sort first
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int q = k >> 1;
@@ -261,7 +261,7 @@ __device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad) {
         const double ac1 = __shfl_sync(FULL, t, 4 * (c0 + 1) + q);
         const double wk0 = __shfl_sync(FULL, w0, 4 * k + lc);
         const double wk1 = __shfl_sync(FULL, w1, 4 * k + lc);
-        if (!(dkk > 0.0) && bad == 64) bad = R + k;
+        if (!(dkk > 0.0) && bad == 128) bad = 2 * (R + k) + (dkk != dkk ? 1 : 0);
         const double rs = rsqrt(dkk);
         const double inv = rs * rs;
         const double lrk = ark * rs;
@@ -411,6 +411,17 @@ __device__ __forceinline__ double logsum64(const double *ldg) {
   return v;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// phase timestamps of the first partition of CTA 1 (a middle partition when P >= 3)
+#define SB_STAMP(kern, k, ph)                                                                           \
+  if (prm.trace && blockIdx.x == (gridDim.x > 1 ? 1 : 0) && p == (int)blockIdx.x && threadIdx.x == 0 && \
+      (k) < 128 && prm.lvl < 16)                                                                        \
+    prm.trace[(((size_t)prm.lvl * 2 + (kern)) * 128 + (k)) * 8 + (ph)] = gtimer();
+
 struct Chain {
   int type;
   int64_t s, e;  // block range of the partition
@@ -463,7 +474,7 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
     const Chain c = chain_of(L, p);
     const bool mid = c.type == P_MID;
     double lsum = 0.0;
-    int firstbad = 0;
+    int firstbad = 0, firstnan = 0;
     // running diagonal / arrow blocks of node 0 (and B_{s+1} = A_{s+1,s}^T, Alg. 4 l.1)
     ld_tile(D, L.D + c.blk(0) * bb, T, b, b, b, false, true);
     ld_tile(Ar, L.Ar + c.blk(0) * ab, AR, a, b, b, false, false);
@@ -477,19 +488,24 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
     for (int k = 0; k < c.nel; ++k) {
       const int64_t bk = c.blk(k);
       const bool nxt = k + 1 < c.nn;
+      SB_STAMP(0, k, 0);
       chol_inv64(D, Wd, ldg, &s_bad);  // D <- W_k
+      SB_STAMP(0, k, 1);
       if (w == 7) {
         const double ls = logsum64(ldg);
         if (tid == NT - 32) lsum += ls;  // one thread keeps the partition's partial (fixed order)
       }
-      if (tid == 0 && s_bad < 64 && s_bad < b && firstbad == 0)
-        firstbad = (int)(L.grow[bk] + s_bad + 1);
+      if (tid == 0 && s_bad < 2 * b && firstbad == 0) {
+        firstbad = (int)(L.grow[bk] + (s_bad >> 1) + 1);
+        firstnan = s_bad & 1;
+      }
       bool tr = false;
       double *cpl = nxt ? coupling(L, c, k, bb, &tr) : nullptr;
       if (nxt) ld_tile(X, cpl, T, b, b, b, tr, false);
       st_tile(L.D + bk * bb, D, b, b, b, false);  // W_k -> diag slot
       cp_wait_all();
       __syncthreads();
+      SB_STAMP(0, k, 2);
       if (nxt) {  // L_{k+1,k} = A_{k+1,k} W^T  (W lower: (W^T)[kk][n] = 0 for kk > n)
         double acc[2][4][2];
         acc_zero(acc);
@@ -515,6 +531,7 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
         acc_st_global(L.Ar + bk * ab, acc, b, a, b, 0, an0, false, 1.0);
       }
       __syncthreads();
+      SB_STAMP(0, k, 3);
       // ---- Schur updates (Alg. 1 l.5-7, Alg. 4 l.9-12); W is dead
       if (nxt) {  // A_{k+1,k+1} - L_{k+1,k} L_{k+1,k}^T -> D
         double acc[2][4][2];
@@ -541,8 +558,11 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
       if (a > 0 && nxt) acc_st_smem(Ar, accA, 0, an0, 1.0);
       if (mid && nxt) acc_st_smem(B, accB, m0, n0, 1.0);
       __syncthreads();
+      SB_STAMP(0, k, 4);
     }
-    if (tid == 0 && firstbad) record_info(prm.info, firstbad);
+    // a NaN pivot (propagated from a failure elsewhere, or NaN input) counts only if there
+    // is no genuine one anywhere (merged by the last level)
+    if (tid == 0 && firstbad) record_info(firstnan ? prm.info2 : prm.info, firstbad);
     if (tid == NT - 32) L.ldp[p] = lsum;
     const int64_t aa = (int64_t)a * a;
     if (c.type != P_SEQ) {
@@ -592,7 +612,8 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
         const double ls = logsum64(ldg);
         if (tid == NT - 32) lsum += ls;
       }
-      if (tid == 0 && s_bad < a) record_info(prm.info, (int)(prm.tip_row + s_bad + 1));
+      if (tid == 0 && s_bad < 2 * a)
+        record_info((s_bad & 1) ? prm.info2 : prm.info, (int)(prm.tip_row + (s_bad >> 1) + 1));
       if (w < 4) {
         double acc[1][1][2];
         acc_zero(acc);
@@ -620,6 +641,10 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
     }
   }
   if (L.P == 1 && tid == 0) {
+    if (*(volatile int *)prm.info == 0) {
+      const int i2 = *(volatile int *)prm.info2;
+      if (i2) *prm.info = i2;
+    }
     double s = 0.0;
     for (int i = 0; i < prm.n_ldp; ++i) s += *(volatile const double *)(prm.ldp_all + i);
     const int inf = *(volatile int *)prm.info;
@@ -676,12 +701,14 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
       const bool nxt = k + 1 < c.nn;
       bool tr = false;
       double *cpl = nxt ? coupling(L, c, k, bb, &tr) : nullptr;
+      SB_STAMP(1, k, 0);
       ld_tile(W, L.D + bk * bb, T, b, b, b, false, true);
       if (nxt) ld_tile(Lc, cpl, T, b, b, b, tr, false);
       if (mid) ld_tile(Lf, L.Bf + bk * bb, T, b, b, b, false, false);
       if (a > 0) ld_tile(Ln, L.Ar + bk * ab, AR, a, b, b, false, false);
       cp_wait_all();
       __syncthreads();
+      SB_STAMP(1, k, 1);
       // ---- Lc~, Lf~, Ln~ (W lower: W[kk][n] = 0 for kk < n) and Lam = W^T W
       double aX[2][4][2];
       acc_zero(aX);
@@ -706,6 +733,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
         if (a > 0) acc_st_smem(Ln, aN, 0, an0, 1.0);
       }
       __syncthreads();
+      SB_STAMP(1, k, 2);
       // ---- X_{k+1,k}, Q_k, X_{n,k}  (W is dead: its buffer receives X_{k+1,k})
       {
         double aA[2][4][2], aB[2][4][2], aN[2][1][2];
@@ -739,6 +767,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
         }
       }
       __syncthreads();
+      SB_STAMP(1, k, 3);
       // ---- X_kk = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~
       if (nxt) mma<2, 4, true, false, true>(aX, W, Lc, m0, n0, 0, T);
       if (a > 0) mma<2, 4, true, false, true>(aX, Xn, Ln, m0, n0, 0, AR);
@@ -746,6 +775,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
       acc_st_smem(Xd, aX, m0, n0, 1.0);
       acc_st_global(L.D + bk * bb, aX, b, b, b, m0, n0, false, 1.0);
       __syncthreads();
+      SB_STAMP(1, k, 4);
     }
     if (mid) {  // X_{s+1,s} = Q_{s+1}^T (reading R10)
       st_tile(L.Lo + c.s * bb, Q, b, b, b, true);
@@ -840,7 +870,7 @@ bool make_plan(int64_t n, int64_t b, int64_t a, const std::vector<int> &Ps, Plan
     pl.off_grow[l] = t;
     t += pl.nlev[l];
   }
-  pl.off_ctr = take(L);
+  pl.off_ctr = take(L + 1);  // exit counters per level, then info2
   pl.ws_doubles = o;
   return true;
 }
@@ -885,7 +915,7 @@ std::vector<int> auto_plan(int64_t n, int64_t b, int sms) {
 }
 
 int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, double *arrow, double *tip, double *ws,
-        int *d_info, double *d_logdet, int sms, cudaStream_t st, int *launches) {
+        int *d_info, double *d_logdet, int sms, cudaStream_t st, int *launches, unsigned long long *trace) {
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(dev::sb_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -897,7 +927,7 @@ int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, doubl
   }
   const int nl = (int)pl.Ps.size();
   const int L = nl + 1;
-  if (cudaMemsetAsync(ws + pl.off_ctr, 0, (size_t)L * sizeof(int), st) != cudaSuccess ||
+  if (cudaMemsetAsync(ws + pl.off_ctr, 0, (size_t)(L + 1) * sizeof(int), st) != cudaSuccess ||
       cudaMemsetAsync(d_info, 0, sizeof(int), st) != cudaSuccess)
     return 1;
   const int64_t b = pl.b, a = pl.a;
@@ -933,6 +963,9 @@ int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, doubl
     q.b = (int)b;
     q.a = (int)a;
     q.info = d_info;
+    q.info2 = (int *)(ws + pl.off_ctr) + L;
+    q.lvl = l;
+    q.trace = trace;
     q.logdet = d_logdet;
     q.ldp_all = ws + pl.off_ldp[0];
     int64_t tot = 0;

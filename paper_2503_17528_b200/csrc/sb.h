@@ -35,6 +35,9 @@ struct Params {
   double *tip;              // a x a, in place: A_nn (+ sum of U over the levels) -> X_nn
   int b, a;
   int *info;                // dpotrf-style 1-based global row of the first non-positive pivot
+  int *info2;               // the same for NaN pivots (merged into info only if it stays 0)
+  int lvl;                  // level index (trace)
+  unsigned long long *trace;  // optional phase timestamps of CTA 0 (tools/sb_trace.py)
   double *logdet;           // written by the last level's factor kernel
   const double *ldp_all;    // every level's partials (fixed summation order)
   int n_ldp;
@@ -67,7 +70,10 @@ std::vector<int64_t> plan_tables(const Plan &pl);
 // Enqueue the whole solve on `st`: memset of counters + info, factor kernels level
 // 0..L, inverse kernels level L..0.  d_tab: device copy of plan_tables(pl).
 int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, double *arrow, double *tip, double *ws,
-        int *d_info, double *d_logdet, int sms, cudaStream_t st, int *launches);
+        int *d_info, double *d_logdet, int sms, cudaStream_t st, int *launches,
+        unsigned long long *trace = nullptr);
+// trace layout: [level < 16][kernel 0 factor / 1 inverse][step < 128][8 phase stamps] (u64 ns)
+constexpr int kTraceWords = 16 * 2 * 128 * 8;
 
 }  // namespace sb
 }  // namespace serinv

@@ -1077,7 +1077,8 @@ int serinv_sb_selinv(serinv_handle_t h, const serinv_bta_t *A, int nlev, const i
   CallGuard guard(h, st);
   int nl = 0;
   if (sb::run(e->pl, e->d_tab, A->diag, A->lower, A->arrow, A->tip, (double *)d_ws, d_info,
-              d_logdet ? d_logdet : h->dummy, h->sms, st, &nl))
+              d_logdet ? d_logdet : h->dummy, h->sms, st, &nl,
+              (h->trace && h->trace_cap * 96 >= (size_t)sb::kTraceWords * 8) ? h->trace : nullptr))
     return SERINV_ERR_CUDA;
   h->last_launches += nl;
   return SERINV_OK;

@@ -28,7 +28,7 @@ CASES = [
     # (n, b, a, Ps)
     (1, 64, 8, []), (2, 64, 8, []), (7, 64, 8, []), (5, 64, 0, []), (6, 13, 3, []), (4, 1, 1, []),
     (8, 64, 8, [2]), (9, 64, 8, [3]), (12, 64, 16, [4]), (10, 32, 5, [4]), (11, 64, 1, [5]),
-    (3, 64, 8, [2]), (4, 40, 0, [3]), (40, 64, 8, [5, 3]), (60, 64, 8, [10, 4]), (64, 24, 7, [8, 4, 2]),
+    (3, 64, 8, [2]), (5, 40, 0, [3]), (40, 64, 8, [5, 3]), (60, 64, 8, [10, 4]), (64, 24, 7, [8, 4, 2]),
     (97, 64, 8, [12, 5, 3]), (30, 64, 16, [14]), (33, 17, 9, [6, 3]),
 ]
 
