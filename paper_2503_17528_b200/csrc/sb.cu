@@ -140,26 +140,137 @@ __device__ void cp_block(double *dst, const double *src, int64_t count) {
 }
 
 // ---------------------------------------------------------------------------
-// Warp-level DMMA products on smem tiles: acc[MI][NI] (8 x 8 fragments, lane l
-// holds (l/4, 2(l%4) + {0,1})) of the (8MI x 8NI) block at (m0, n0)
-//   acc += sgn * sum_{k in [k0, k1)} op(A)[m][k] op(B)[k][n]
+// Warp-level DMMA products on smem tiles.  A warp owns the 8 x 8 output
+// fragments (rf[i], cf[j]) (lane l holds (l/4, 2(l%4) + {0,1}) of each):
+//   acc[i][j] += sgn * sum_k op(A)[8 rf[i] + .][k] op(B)[k][8 cf[j] + .]
+// Layout of 64 x 64 outputs (lay64): warp w = 2 rg + h owns row fragments
+// {rg, 7 - rg} and column fragments {0,1,6,7} (h = 0) or {2,3,4,5} (h = 1).  It
+// balances the warps for the triangular operands (W = L^{-1}: the k range of
+// column fragment c is [8c, 64) or [0, 8c + 8)) and for lower-triangle-only
+// products of symmetric results (5 or 4 of the 36 lower fragments per warp), and
+// each A row strip is shared by exactly one warp pair (pair barriers).
+// Operand k-range modes: A_GE (A[m][k] = 0 for k < m: A = W^T), B_GE (B[k][n] = 0
+// for k < n: B = W), B_LE (B[k][n] = 0 for k > n: B = W^T); LOW: only fragments
+// with rf >= cf.
 // ---------------------------------------------------------------------------
-template <int MI, int NI, bool TA, bool TB, bool NEG>
-__device__ __forceinline__ void mma(double (&acc)[MI][NI][2], const double *A, const double *B, int m0, int n0,
-                                    int k0, int k1) {
+enum { K_FULL = 0, A_GE = 1, B_GE = 2, B_LE = 3 };
+
+template <int MI, int NI>
+struct Frags {
+  int rf[MI], cf[NI];
+};
+
+__device__ __forceinline__ Frags<2, 4> lay64(int w) {
+  Frags<2, 4> F;
+  const int rg = w >> 1, h = w & 1;
+  F.rf[0] = rg;
+  F.rf[1] = 7 - rg;
+  F.cf[0] = h ? 2 : 0;
+  F.cf[1] = h ? 3 : 1;
+  F.cf[2] = h ? 4 : 6;
+  F.cf[3] = h ? 5 : 7;
+  return F;
+}
+// 16 x 64 outputs (arrow rows): row fragment w & 1, column fragments {w/2, 7 - w/2}
+__device__ __forceinline__ Frags<1, 2> layAR(int w) {
+  Frags<1, 2> F;
+  F.rf[0] = w & 1;
+  F.cf[0] = w >> 1;
+  F.cf[1] = 7 - (w >> 1);
+  return F;
+}
+// 16 x 16 outputs (tip-sized), warps 0..3
+__device__ __forceinline__ Frags<1, 1> layU(int w) {
+  Frags<1, 1> F;
+  F.rf[0] = (w >> 1) & 1;
+  F.cf[0] = w & 1;
+  return F;
+}
+
+// column fragments of the two lay64 column sets
+__device__ __forceinline__ constexpr int colfrag(int h, int j) { return h ? 2 + j : (j < 2 ? j : j + 4); }
+
+// 64 x 64 products in lay64 for the warp's column set H (compile time): the k loop
+// is unrolled, so the triangular k ranges (BM) are compile-time per fragment; LOW
+// skips the warp-uniform strictly-upper fragments (rf < cf).  KK = contraction
+// length (64, or AR for the arrow contractions).
+template <int H, bool TA, bool TB, bool NEG, int BM, bool LOW, int KK>
+__device__ __forceinline__ void mma_h(double (&acc)[2][4][2], const double *A, const double *B, const int rf0,
+                                      const int rf1) {
   const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
+  const int rf[2] = {rf0, rf1};
+  bool on[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) on[i][j] = !LOW || rf[i] >= colfrag(H, j);
+#pragma unroll
+  for (int k = 0; k < KK; k += 4) {
+    bool col[4];
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = colfrag(H, j);
+      col[j] = BM == B_LE ? k < 8 * c + 8 : (BM == B_GE ? k >= 8 * c : true);
+      any |= col[j];
+    }
+    if (!any) continue;
+    const int kk = k + lc;
+    double af[2], bf[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int m = 8 * rf[i] + lr;
+      const double v = TA ? A[swz(kk, m)] : A[swz(m, kk)];
+      af[i] = NEG ? -v : v;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      bf[j] = 0.0;
+      if (!col[j]) continue;
+      const int n = 8 * colfrag(H, j) + lr;
+      bf[j] = TB ? B[swz(n, kk)] : B[swz(kk, n)];
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (col[j] && on[i][j]) dmma(acc[i][j], af[i], bf[j]);
+  }
+}
+
+template <bool TA, bool TB, bool NEG, int BM = K_FULL, bool LOW = false, int KK = T>
+__device__ __forceinline__ void mma64(double (&acc)[2][4][2], const double *A, const double *B,
+                                      const Frags<2, 4> &F) {
+  if (threadIdx.x & 32)
+    mma_h<1, TA, TB, NEG, BM, LOW, KK>(acc, A, B, F.rf[0], F.rf[1]);
+  else
+    mma_h<0, TA, TB, NEG, BM, LOW, KK>(acc, A, B, F.rf[0], F.rf[1]);
+}
+
+// small products (arrow / tip outputs) with run-time fragments: warp-level k range only
+template <int MI, int NI, bool TA, bool TB, bool NEG, int BM = K_FULL>
+__device__ __forceinline__ void mma(double (&acc)[MI][NI][2], const double *A, const double *B,
+                                    const Frags<MI, NI> &F, int K) {
+  const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
+  int klo = K, khi = 0;
+#pragma unroll
+  for (int j = 0; j < NI; ++j) {
+    klo = min(klo, BM == B_GE ? 8 * F.cf[j] : 0);
+    khi = max(khi, BM == B_LE ? min(K, 8 * F.cf[j] + 8) : K);
+  }
 #pragma unroll 2
-  for (int k = k0; k < k1; k += 4) {
+  for (int k = klo; k < khi; k += 4) {
     double af[MI], bf[NI];
+    const int kk = k + lc;
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
-      const int m = m0 + 8 * i + lr, kk = k + lc;
+      const int m = 8 * F.rf[i] + lr;
       const double v = TA ? A[swz(kk, m)] : A[swz(m, kk)];
       af[i] = NEG ? -v : v;
     }
 #pragma unroll
     for (int j = 0; j < NI; ++j) {
-      const int n = n0 + 8 * j + lr, kk = k + lc;
+      const int n = 8 * F.cf[j] + lr;
       bf[j] = TB ? B[swz(n, kk)] : B[swz(kk, n)];
     }
 #pragma unroll
@@ -180,13 +291,13 @@ __device__ __forceinline__ void acc_zero(double (&acc)[MI][NI][2]) {
 // acc <- g (rows x cols block, ld), padded with the identity (pad) or zeros
 template <int MI, int NI>
 __device__ __forceinline__ void acc_ld(double (&acc)[MI][NI][2], const double *g, int ld, int rows, int cols,
-                                       int m0, int n0, bool pad) {
+                                       const Frags<MI, NI> &F, bool pad) {
   const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NI; ++j) {
-      const int m = m0 + 8 * i + lr, n = n0 + 8 * j + 2 * lc;
+      const int m = 8 * F.rf[i] + lr, n = 8 * F.cf[j] + 2 * lc;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = n + e;
@@ -195,139 +306,257 @@ __device__ __forceinline__ void acc_ld(double (&acc)[MI][NI][2], const double *g
     }
 }
 
+// acc <- s (a swizzled smem tile)
 template <int MI, int NI>
-__device__ __forceinline__ void acc_st_smem(double *s, const double (&acc)[MI][NI][2], int m0, int n0,
+__device__ __forceinline__ void acc_ld_smem(double (&acc)[MI][NI][2], const double *s, const Frags<MI, NI> &F) {
+  const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const double2 v = *(const double2 *)(s + swz(8 * F.rf[i] + lr, 8 * F.cf[j] + 2 * lc));
+      acc[i][j][0] = v.x;
+      acc[i][j][1] = v.y;
+    }
+}
+
+// s <- sgn * acc; LOW: only fragments rf >= cf, mirrored to (cf, rf) when MIR
+template <int MI, int NI, bool LOW = false, bool MIR = false>
+__device__ __forceinline__ void acc_st_smem(double *s, const double (&acc)[MI][NI][2], const Frags<MI, NI> &F,
                                             double sgn) {
   const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NI; ++j) {
-      const int m = m0 + 8 * i + lr, n = n0 + 8 * j + 2 * lc;
-      *(double2 *)(s + swz(m, n)) = make_double2(sgn * acc[i][j][0], sgn * acc[i][j][1]);
+      if (LOW && F.rf[i] < F.cf[j]) continue;
+      const int m = 8 * F.rf[i] + lr, n = 8 * F.cf[j] + 2 * lc;
+      const double v0 = sgn * acc[i][j][0], v1 = sgn * acc[i][j][1];
+      *(double2 *)(s + swz(m, n)) = make_double2(v0, v1);
+      if (MIR && F.rf[i] != F.cf[j]) {
+        s[swz(n, m)] = v0;
+        s[swz(n + 1, m)] = v1;
+      }
     }
 }
 
-// g <- sgn * acc (rows x cols of the block; trans: g[c*ld + r] = value (r, c))
-template <int MI, int NI>
+// g <- sgn * acc (rows x cols of the block; trans: g[c*ld + r] = value (r, c)); LOW / MIR as above
+template <int MI, int NI, bool LOW = false, bool MIR = false>
 __device__ __forceinline__ void acc_st_global(double *g, const double (&acc)[MI][NI][2], int ld, int rows,
-                                              int cols, int m0, int n0, bool trans, double sgn) {
+                                              int cols, const Frags<MI, NI> &F, bool trans, double sgn) {
   const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NI; ++j) {
-      const int m = m0 + 8 * i + lr, n = n0 + 8 * j + 2 * lc;
-      if (m >= rows) continue;
+      if (LOW && F.rf[i] < F.cf[j]) continue;
+      const int m = 8 * F.rf[i] + lr, n = 8 * F.cf[j] + 2 * lc;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = n + e;
-        if (c < cols) {
-          if (trans)
-            g[(int64_t)c * ld + m] = sgn * acc[i][j][e];
-          else
-            g[(int64_t)m * ld + c] = sgn * acc[i][j][e];
-        }
+        if (m >= rows || c >= cols) continue;
+        const double v = sgn * acc[i][j][e];
+        if (trans || (MIR && F.rf[i] != F.cf[j])) g[(int64_t)c * ld + m] = v;
+        if (!trans) g[(int64_t)m * ld + c] = v;
       }
     }
 }
 
+// barrier of the warp pair sharing a row strip in lay64 (warps 2rg, 2rg+1)
+__device__ __forceinline__ void pair_sync() {
+  asm volatile("bar.sync %0, 64;\n" ::"r"(1 + (int)(threadIdx.x >> 6)) : "memory");
+}
+
+// 1 / sqrt(x): MUFU approximation + 2 Newton steps (full double precision; NaN for x <= 0)
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
 // ---------------------------------------------------------------------------
 // In-place Cholesky + triangular inverse of a 64 x 64 SPD tile (lower triangle
-// read): D <- W = L^{-1} (lower, strict upper zero).  ldg[t] = L_tt.  Blocked
-// right-looking on 8-column panels: warp 0 factors the 8 x 8 diagonal block in
-// registers (pivots, the product-form inverse W_jj alongside), all warps the
-// panel TRSM (with W_jj) and the trailing update by DMMA; then W from the
-// blocks: W_21 = -W_22 L_21 W_11 on 8 / 16 / 32 levels.  *s_bad = 2 x the first
-// non-positive pivot index + 1 if that pivot is NaN; 128 if none.  Called by all NT threads.
+// read): D <- W = L^{-1} (lower, strict upper zero).  ldg[t] = L_tt.
+// Right-looking on 8-column panels with look-ahead:
+//   warp 0 (the critical chain), round j: factors the 8 x 8 diagonal block (j,j)
+//     on ONE thread in registers (8 rsqrt + FMA steps, the product-form inverse
+//     W_jj alongside), publishes L_jj / W_jj (named barrier, arrive), waits for
+//     the workers' round j-1, then computes L_{j+1,j} = A_{j+1,j} W_jj^T and the
+//     panel-j update of the next diagonal block (j+1,j+1) itself;
+//   warps 1..7 (workers), round j: wait for W_jj, update every other trailing
+//     tile (i,k), j < k <= i, computing the panel blocks they need themselves
+//     (L_ij = A_ij W_jj^T, written transposed into the free upper block (j,i) --
+//     the same values from every warp that computes them -- and read back as
+//     fragments), then arrive on the round's barrier.
+// The panel blocks move from the scratch into place at the end; then
+// W = L^{-1} by W_21 = -W_22 L_21 W_11 on 8 / 16 / 32 levels.  *s_bad = 2 x the
+// first non-positive pivot index + 1 if that pivot is NaN; 128 if none.
+// Called by all NT threads; needs the registers of one thread for the leaf (the
+// kernels that call it run 1 CTA per SM).
 // ---------------------------------------------------------------------------
-__device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad) {
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void nbar_arrive(int id) { asm volatile("bar.arrive %0, 256;\n" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void nbar_sync(int id) { asm volatile("bar.sync %0, 256;\n" ::"r"(id) : "memory"); }
+
+// the trailing update of tile (i, k) by panel j (R = 8j): L_ij, L_kj computed in-warp
+// into the transposed scratch (j, i), (j, k), then A_ik -= L_ij L_kj^T.  Up to 4 tiles
+// of one warp in flight together.
+__device__ __forceinline__ void trail_tiles(double *D, const double *Wd, int R, const int (&ti)[4],
+                                            const int (&tk)[4], const bool (&on)[4]) {
+  const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
+  double li[4][2], lk[4][2];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    li[u][0] = li[u][1] = lk[u][0] = lk[u][1] = 0.0;
+    if (!on[u]) continue;
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 4) {
+      const double wv = Wd[swz(lr, R + kk + lc)];
+      dmma(li[u], D[swz(8 * ti[u] + lr, R + kk + lc)], wv);
+      if (tk[u] != ti[u]) dmma(lk[u], D[swz(8 * tk[u] + lr, R + kk + lc)], wv);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (!on[u]) continue;
+    D[swz(R + 2 * lc, 8 * ti[u] + lr)] = li[u][0];
+    D[swz(R + 2 * lc + 1, 8 * ti[u] + lr)] = li[u][1];
+    if (tk[u] != ti[u]) {
+      D[swz(R + 2 * lc, 8 * tk[u] + lr)] = lk[u][0];
+      D[swz(R + 2 * lc + 1, 8 * tk[u] + lr)] = lk[u][1];
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (!on[u]) continue;
+    const int i = ti[u], k = tk[u];
+    double2 cv = *(const double2 *)(D + swz(8 * i + lr, 8 * k + 2 * lc));
+    double acc[2] = {cv.x, cv.y};
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 4)
+      dmma(acc, -D[swz(R + kk + lc, 8 * i + lr)], D[swz(R + kk + lc, 8 * k + lr)]);
+    *(double2 *)(D + swz(8 * i + lr, 8 * k + 2 * lc)) = make_double2(acc[0], acc[1]);
+  }
+}
+
+__device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad, unsigned long long *stamp = nullptr) {
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, lr = l >> 2, lc = l & 3;
-  if (tid == 0) *s_bad = 128;
-  for (int j = 0; j < 8; ++j) {
-    const int R = 8 * j;
-    if (w == 0) {
-      const int c0 = 2 * lc;
-      double a0 = D[swz(R + lr, R + c0)], a1 = D[swz(R + lr, R + c0 + 1)];
-      double w0 = (lr == c0) ? 1.0 : 0.0, w1 = (lr == c0 + 1) ? 1.0 : 0.0;
-      int bad = 128;  // 2 * (first failing pivot) + (pivot is NaN): genuine failures sort first
+  if (w == 0) {
+    int bad = 128;  // 2 * (first failing pivot) + (pivot is NaN): genuine failures sort first (lane 0)
+    for (int j = 0; j < 8; ++j) {
+      const int R = 8 * j;
+      // element (R + i, R + c) of the swizzled tile = (row base)[c ^ (i & 4)]: R = 8j has no bits
+      // below 3, so the XOR splits into a per-row base and a compile-time column offset
+      if (l == 0) {
+        double a[8][8], wv[8][8];  // lower triangles used (indices are compile-time after unrolling)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int q = k >> 1;
-        const double t = (k & 1) ? a1 : a0;  // own row's column-k value on lanes with l%4 == k/2
-        const double dkk = __shfl_sync(FULL, t, 4 * k + q);
-        const double ark = __shfl_sync(FULL, t, 4 * lr + q);
-        const double ac0 = __shfl_sync(FULL, t, 4 * c0 + q);
-        const double ac1 = __shfl_sync(FULL, t, 4 * (c0 + 1) + q);
-        const double wk0 = __shfl_sync(FULL, w0, 4 * k + lc);
-        const double wk1 = __shfl_sync(FULL, w1, 4 * k + lc);
-        if (!(dkk > 0.0) && bad == 128) bad = 2 * (R + k) + (dkk != dkk ? 1 : 0);
-        const double rs = rsqrt(dkk);
-        const double inv = rs * rs;
-        const double lrk = ark * rs;
-        if (c0 == k) {
-          if (lr > k) a0 = lrk;
-          else if (lr == k) a0 = dkk * rs;
-        } else if (c0 > k && lr >= c0) {
-          a0 -= ark * ac0 * inv;
+        for (int i = 0; i < 8; ++i) {
+          const double *rp = D + (R + i) * T + (R ^ ((i & 3) << 3));
+#pragma unroll
+          for (int c = 0; c <= i; c += 2) {  // 16-byte loads: positions (c, c+1) ^ (i & 4) stay paired
+            const double2 v = *(const double2 *)(rp + (c ^ (i & 4)));
+            a[i][c] = v.x;
+            a[i][c + 1] = v.y;
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            if (c > i) a[i][c] = 0.0;
+            wv[i][c] = i == c ? 1.0 : 0.0;
+          }
         }
-        if (c0 + 1 == k) {
-          if (lr > k) a1 = lrk;
-          else if (lr == k) a1 = dkk * rs;
-        } else if (c0 + 1 > k && lr >= c0 + 1) {
-          a1 -= ark * ac1 * inv;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double dkk = a[k][k];
+          if (!(dkk > 0.0) && bad == 128) bad = 2 * (R + k) + (dkk != dkk ? 1 : 0);
+          const double rs = rsqrt_nr(dkk);
+          a[k][k] = dkk * rs;
+#pragma unroll
+          for (int i = k + 1; i < 8; ++i) a[i][k] *= rs;
+#pragma unroll
+          for (int i = k + 1; i < 8; ++i)
+#pragma unroll
+            for (int c = k + 1; c <= i; ++c) a[i][c] = fma(-a[i][k], a[c][k], a[i][c]);
+          // W <- E_k^{-1} W: row k scaled by 1/l_kk, rows i > k minus l_ik * (new row k)
+#pragma unroll
+          for (int c = 0; c <= k; ++c) wv[k][c] *= rs;
+#pragma unroll
+          for (int i = k + 1; i < 8; ++i)
+#pragma unroll
+            for (int c = 0; c <= k; ++c) wv[i][c] = fma(-a[i][k], wv[k][c], wv[i][c]);
         }
-        if (lr == k) {
-          w0 *= rs;
-          w1 *= rs;
-        } else if (lr > k) {
-          const double f = lrk * rs;
-          w0 -= f * wk0;
-          w1 -= f * wk1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          ldg[R + i] = a[i][i];
+          double *rp = D + (R + i) * T + (R ^ ((i & 3) << 3));
+          double *wp = Wd + i * T + (R ^ ((i & 3) << 3));
+#pragma unroll
+          for (int c = 0; c < 8; c += 2) {
+            *(double2 *)(rp + (c ^ (i & 4))) =
+                make_double2(c <= i ? a[i][c] : 0.0, c + 1 <= i ? a[i][c + 1] : 0.0);
+            *(double2 *)(wp + (c ^ (i & 4))) =
+                make_double2(c <= i ? wv[i][c] : 0.0, c + 1 <= i ? wv[i][c + 1] : 0.0);
+          }
         }
       }
-      D[swz(R + lr, R + c0)] = (c0 <= lr) ? a0 : 0.0;
-      D[swz(R + lr, R + c0 + 1)] = (c0 + 1 <= lr) ? a1 : 0.0;
-      Wd[swz(lr, R + c0)] = w0;
-      Wd[swz(lr, R + c0 + 1)] = w1;
-      if (lr == c0) ldg[R + lr] = a0;
-      if (lr == c0 + 1) ldg[R + lr] = a1;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) bad = min(bad, __shfl_xor_sync(FULL, bad, o));
-      if (l == 0 && bad < *s_bad) *s_bad = bad;
-    }
-    __syncthreads();
-    if (j == 7) break;
-    {  // panel TRSM: L_ij = A_ij W_jj^T, i = j+1+w
-      const int i = j + 1 + w;
-      if (i < 8) {
-        double acc[2] = {0.0, 0.0};
-#pragma unroll
-        for (int kk = 0; kk < 8; kk += 4)
-          dmma(acc, D[swz(8 * i + lr, R + kk + lc)], Wd[swz(lr, R + kk + lc)]);
-        *(double2 *)(D + swz(8 * i + lr, R + 2 * lc)) = make_double2(acc[0], acc[1]);
+      __syncwarp();
+      if (stamp && l == 0) stamp[2 * j] = gtimer();
+      if (j == 7) {
+        nbar_sync(3 + (6 & 1));  // the workers' last round (complete every barrier generation)
+        break;
       }
+      nbar_arrive(1 + (j & 1));                 // L_jj, W_jj published
+      if (j > 0) nbar_sync(3 + ((j - 1) & 1));  // the workers' round j-1 is done
+      // look-ahead: the next diagonal block gets its panel-j update from this warp
+      const int ti[4] = {j + 1, 0, 0, 0}, tk[4] = {j + 1, 0, 0, 0};
+      const bool on[4] = {true, false, false, false};
+      trail_tiles(D, Wd, R, ti, tk, on);
+      __syncwarp();
+      if (stamp && l == 0) stamp[2 * j + 1] = gtimer();
     }
-    __syncthreads();
-    {  // trailing update A_ik -= L_ij L_kj^T, j < k <= i
-      const int nb = 7 - j, np = nb * (nb + 1) / 2;
-      for (int t = w; t < np; t += 8) {
-        int ii = 0, tt = t;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+    if (l == 0) *s_bad = bad;
+  } else {
+    for (int j = 0; j < 7; ++j) {
+      const int R = 8 * j;
+      nbar_sync(1 + (j & 1));  // W_jj ready
+      // tiles (i, k), j < k <= i, except (j+1, j+1), round-robin over warps 1..7
+      const int nb = 7 - j, np = nb * (nb + 1) / 2 - 1;
+      int ti[4], tk[4];
+      bool on[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = (w - 1) + 7 * u;
+        on[u] = t < np;
+        int ii = 0, tt = on[u] ? t + 1 : 1;  // skip tile 0 = (j+1, j+1)
         while (tt > ii) {
           tt -= ii + 1;
           ++ii;
         }
-        const int i = j + 1 + ii, k = j + 1 + tt;
-        double2 c = *(const double2 *)(D + swz(8 * i + lr, 8 * k + 2 * lc));
-        double acc[2] = {c.x, c.y};
-#pragma unroll
-        for (int kk = 0; kk < 8; kk += 4)
-          dmma(acc, -D[swz(8 * i + lr, R + kk + lc)], D[swz(8 * k + lr, R + kk + lc)]);
-        *(double2 *)(D + swz(8 * i + lr, 8 * k + 2 * lc)) = make_double2(acc[0], acc[1]);
+        ti[u] = j + 1 + ii;
+        tk[u] = j + 1 + tt;
       }
+      trail_tiles(D, Wd, R, ti, tk, on);
+      nbar_arrive(3 + (j & 1));  // round j done
     }
-    __syncthreads();
   }
+  __syncthreads();
+  // panel blocks into place: scratch (j, i) holds L_ij^T, i > j (rows 8j+8.. of column block j)
+#pragma unroll
+  for (int j = 0; j < 7; ++j)
+    for (int e = tid; e < (56 - 8 * j) * 8; e += NT) {
+      const int r = 8 * j + 8 + (e >> 3), c = 8 * j + (e & 7);
+      D[swz(r, c)] = D[swz(c, r)];
+    }
+  __syncthreads();
   // ---- W = L^{-1}: diagonal blocks from Wd
   for (int i = tid; i < 8 * T; i += NT) {
     const int r = i >> 6, c = i & 63, jb = c >> 3;
@@ -341,11 +570,8 @@ __device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad) {
 #pragma unroll
     for (int kk = 0; kk < 8; kk += 4) dmma(acc, D[swz(b0 + 8 + lr, b0 + kk + lc)], D[swz(b0 + kk + lc, b0 + lr)]);
     *(double2 *)(D + swz(b0 + lr, b0 + 8 + 2 * lc)) = make_double2(acc[0], acc[1]);
-  }
-  __syncthreads();
-  if (w < 4) {
-    const int b0 = 16 * w;
-    double acc[2] = {0.0, 0.0};
+    __syncwarp();
+    acc[0] = acc[1] = 0.0;
 #pragma unroll
     for (int kk = 0; kk < 8; kk += 4)
       dmma(acc, -D[swz(b0 + 8 + lr, b0 + 8 + kk + lc)], D[swz(b0 + kk + lc, b0 + 8 + lr)]);
@@ -353,9 +579,9 @@ __device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad) {
   }
   __syncthreads();
   // level 16: quads q (base 32q): T = L21 W11 -> rows 32q.., cols 32q+16.. ; W21 = -W22 T
+  // (block-lower k ranges: the strict-upper blocks hold the previous level's T)
   {
     const int q = w >> 2, fi = (w >> 1) & 1, fj = w & 1, b0 = 32 * q;
-    // block-lower k ranges: the strict-upper blocks hold the previous level's T
     double acc[2] = {0.0, 0.0};
     for (int kk = 8 * fj; kk < 16; kk += 4)
       dmma(acc, D[swz(b0 + 16 + 8 * fi + lr, b0 + kk + lc)], D[swz(b0 + kk + lc, b0 + 8 * fj + lr)]);
@@ -400,6 +626,7 @@ __device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad) {
     if ((c >> 3) > (r >> 3)) D[swz(r, c)] = 0.0;
   }
   __syncthreads();
+  if (stamp && tid == 0) stamp[15] = gtimer();
 }
 
 // sum_t log(ldg[t]) in a fixed order (warp w of the caller; all lanes get it)
@@ -411,11 +638,6 @@ __device__ __forceinline__ double logsum64(const double *ldg) {
   return v;
 }
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 // phase timestamps of the first partition of CTA 1 (a middle partition when P >= 3)
 #define SB_STAMP(kern, k, ph)                                                                           \
   if (prm.trace && blockIdx.x == (gridDim.x > 1 ? 1 : 0) && p == (int)blockIdx.x && threadIdx.x == 0 && \
@@ -458,17 +680,19 @@ __device__ __forceinline__ double *coupling(const Level &L, const Chain &c, int 
 // ---------------------------------------------------------------------------
 // PPOBTAF (Alg. 3-4; Alg. 1 for the last level) of the partitions of one level.
 // ---------------------------------------------------------------------------
-constexpr int F_SMEM_DOUBLES = 3 * TD + AD + 8 * T + T;
+constexpr int F_SMEM_DOUBLES = 3 * TD + AD + 8 * T + T + 8 + TD + AD;
 
-extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm) {
+extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm) {
   extern __shared__ __align__(16) double sm[];
   double *D = sm, *X = D + TD, *B = X + TD, *Ar = B + TD, *Wd = Ar + AD, *ldg = Wd + 8 * T;
+  double *Dn = ldg + T + 8, *An = Dn + TD;  // the next node's diagonal / arrow blocks (prefetched)
   __shared__ int s_bad;
   const Level &L = prm.L;
   const int b = prm.b, a = prm.a, tid = threadIdx.x, w = tid >> 5;
   const int64_t bb = (int64_t)b * b, ab = (int64_t)a * b;
-  const int m0 = 16 * (w >> 1), n0 = 32 * (w & 1);  // 64 x 64 warp tile
-  const int an0 = 8 * w;                              // 16 x 64 warp tile (arrow rows)
+  const Frags<2, 4> F = lay64(w);
+  const Frags<1, 2> FA = layAR(w);
+  const Frags<1, 1> FU = layU(w);
 
   for (int p = blockIdx.x; p < L.P; p += gridDim.x) {
     const Chain c = chain_of(L, p);
@@ -481,7 +705,7 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
     if (mid) ld_tile(B, L.Lo + c.s * bb, T, b, b, b, true, false);
     cp_wait_all();
     __syncthreads();
-    double Aff[2][4][2], Anf[2][1][2], Uac[1][1][2];
+    double Aff[2][4][2], Anf[1][2][2], Uac[1][1][2];
     acc_zero(Aff);
     acc_zero(Anf);
     acc_zero(Uac);
@@ -489,7 +713,18 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
       const int64_t bk = c.blk(k);
       const bool nxt = k + 1 < c.nn;
       SB_STAMP(0, k, 0);
-      chol_inv64(D, Wd, ldg, &s_bad);  // D <- W_k
+      bool tr = false;
+      double *cpl = nxt ? coupling(L, c, k, bb, &tr) : nullptr;
+      if (nxt) {  // the step's HBM inputs, in flight while the Cholesky runs
+        ld_tile(X, cpl, T, b, b, b, tr, false);
+        ld_tile(Dn, L.D + c.blk(k + 1) * bb, T, b, b, b, false, true);
+        if (a > 0) ld_tile(An, L.Ar + c.blk(k + 1) * ab, AR, a, b, b, false, false);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      unsigned long long *cst = nullptr;  // chol-internal stamps of the traced partition (level slot 8 + lvl)
+      if (prm.trace && blockIdx.x == (gridDim.x > 1 ? 1 : 0) && p == (int)blockIdx.x && k < 64 && prm.lvl < 8)
+        cst = prm.trace + (((size_t)(8 + prm.lvl) * 2) * 128 + 2 * k) * 8;
+      chol_inv64(D, Wd, ldg, &s_bad, cst);  // D <- W_k
       SB_STAMP(0, k, 1);
       if (w == 7) {
         const double ls = logsum64(ldg);
@@ -499,64 +734,62 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
         firstbad = (int)(L.grow[bk] + (s_bad >> 1) + 1);
         firstnan = s_bad & 1;
       }
-      bool tr = false;
-      double *cpl = nxt ? coupling(L, c, k, bb, &tr) : nullptr;
-      if (nxt) ld_tile(X, cpl, T, b, b, b, tr, false);
       st_tile(L.D + bk * bb, D, b, b, b, false);  // W_k -> diag slot
       cp_wait_all();
       __syncthreads();
       SB_STAMP(0, k, 2);
-      if (nxt) {  // L_{k+1,k} = A_{k+1,k} W^T  (W lower: (W^T)[kk][n] = 0 for kk > n)
+      // ---- TRSMs (products with W^T; in place, row strips shared by warp pairs only)
+      if (nxt) {  // L_{k+1,k} = A_{k+1,k} W^T
         double acc[2][4][2];
         acc_zero(acc);
-        mma<2, 4, false, true, false>(acc, X, D, m0, n0, 0, n0 + 32);
-        __syncthreads();
-        acc_st_smem(X, acc, m0, n0, 1.0);
-        acc_st_global(cpl, acc, b, b, b, m0, n0, tr, 1.0);
+        mma64<false, true, false, B_LE>(acc, X, D, F);
+        pair_sync();
+        acc_st_smem(X, acc, F, 1.0);
+        acc_st_global(cpl, acc, b, b, b, F, tr, 1.0);
       }
       if (mid) {  // L_{f,k} = B_k W^T (Alg. 4, fill-in TRSM)
         double acc[2][4][2];
         acc_zero(acc);
-        mma<2, 4, false, true, false>(acc, B, D, m0, n0, 0, n0 + 32);
-        __syncthreads();
-        acc_st_smem(B, acc, m0, n0, 1.0);
-        acc_st_global(L.Bf + bk * bb, acc, b, b, b, m0, n0, false, 1.0);
+        mma64<false, true, false, B_LE>(acc, B, D, F);
+        pair_sync();
+        acc_st_smem(B, acc, F, 1.0);
+        acc_st_global(L.Bf + bk * bb, acc, b, b, b, F, false, 1.0);
       }
       if (a > 0) {  // L_{n,k} = A_{n,k} W^T
-        double acc[2][1][2];
+        double acc[1][2][2];
         acc_zero(acc);
-        mma<2, 1, false, true, false>(acc, Ar, D, 0, an0, 0, an0 + 8);
+        mma<1, 2, false, true, false, B_LE>(acc, Ar, D, FA, T);
         __syncthreads();
-        acc_st_smem(Ar, acc, 0, an0, 1.0);
-        acc_st_global(L.Ar + bk * ab, acc, b, a, b, 0, an0, false, 1.0);
+        acc_st_smem(Ar, acc, FA, 1.0);
+        acc_st_global(L.Ar + bk * ab, acc, b, a, b, FA, false, 1.0);
       }
       __syncthreads();
       SB_STAMP(0, k, 3);
       // ---- Schur updates (Alg. 1 l.5-7, Alg. 4 l.9-12); W is dead
-      if (nxt) {  // A_{k+1,k+1} - L_{k+1,k} L_{k+1,k}^T -> D
+      if (nxt) {  // A_{k+1,k+1} - L_{k+1,k} L_{k+1,k}^T -> D (lower fragments: POTRF reads the lower triangle)
         double acc[2][4][2];
-        acc_ld(acc, L.D + c.blk(k + 1) * bb, b, b, b, m0, n0, true);
-        mma<2, 4, false, true, true>(acc, X, X, m0, n0, 0, T);
-        acc_st_smem(D, acc, m0, n0, 1.0);
+        acc_ld_smem(acc, Dn, F);
+        mma64<false, true, true, K_FULL, true>(acc, X, X, F);
+        acc_st_smem<2, 4, true>(D, acc, F, 1.0);
       }
       if (a > 0) {
-        if (w < 4) mma<1, 1, false, true, true>(Uac, Ar, Ar, 8 * (w >> 1), 8 * (w & 1), 0, T);  // U -= Ln Ln^T
-        if (mid) mma<2, 1, false, true, true>(Anf, Ar, B, 0, an0, 0, T);                      // A_nf -= Ln B^T
+        if (w < 4) mma<1, 1, false, true, true>(Uac, Ar, Ar, FU, T);  // U -= Ln Ln^T
+        if (mid) mma<1, 2, false, true, true>(Anf, Ar, B, FA, T);       // A_nf -= Ln B^T
       }
-      if (mid) mma<2, 4, false, true, true>(Aff, B, B, m0, n0, 0, T);  // A_ff -= B B^T
-      double accA[2][1][2];
+      if (mid) mma64<false, true, true, K_FULL, true>(Aff, B, B, F);  // A_ff -= B B^T (lower)
+      double accA[1][2][2];
       if (a > 0 && nxt) {  // A_{n,k+1} - L_{n,k} L_{k+1,k}^T
-        acc_ld(accA, L.Ar + c.blk(k + 1) * ab, b, a, b, 0, an0, false);
-        mma<2, 1, false, true, true>(accA, Ar, X, 0, an0, 0, T);
+        acc_ld_smem(accA, An, FA);
+        mma<1, 2, false, true, true>(accA, Ar, X, FA, T);
       }
       double accB[2][4][2];
       if (mid && nxt) {  // B_{k+1} = -B_k L_{k+1,k}^T
         acc_zero(accB);
-        mma<2, 4, false, true, true>(accB, B, X, m0, n0, 0, T);
+        mma64<false, true, true>(accB, B, X, F);
       }
       __syncthreads();
-      if (a > 0 && nxt) acc_st_smem(Ar, accA, 0, an0, 1.0);
-      if (mid && nxt) acc_st_smem(B, accB, m0, n0, 1.0);
+      if (a > 0 && nxt) acc_st_smem(Ar, accA, FA, 1.0);
+      if (mid && nxt) acc_st_smem(B, accB, F, 1.0);
       __syncthreads();
       SB_STAMP(0, k, 4);
     }
@@ -572,9 +805,9 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
       if (a > 0) st_tile(L.Arn + ib * ab, Ar, a, b, b, false);
       if (c.type != P_BOT) cp_block(L.Lon + (int64_t)(c.type == P_TOP ? 0 : 2 * p) * bb, L.Lo + (c.e - 1) * bb, bb);
       if (mid) {
-        // A_ff + sum(-B B^T), A_{n,f} + sum(-Ln B^T), (L_p, F_p) coupling = B_{e-1}^T
+        // A_ff + sum(-B B^T) (lower), A_{n,f} + sum(-Ln B^T), (L_p, F_p) coupling = B_{e-1}^T
         double acc[2][4][2];
-        acc_ld(acc, L.D + c.s * bb, b, b, b, m0, n0, false);
+        acc_ld(acc, L.D + c.s * bb, b, b, b, F, false);
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -582,27 +815,27 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
             acc[i][j][0] += Aff[i][j][0];
             acc[i][j][1] += Aff[i][j][1];
           }
-        acc_st_global(L.Dn + (2 * p - 1) * bb, acc, b, b, b, m0, n0, false, 1.0);
+        acc_st_global<2, 4, true>(L.Dn + (2 * p - 1) * bb, acc, b, b, b, F, false, 1.0);
         if (a > 0) {
-          double acn[2][1][2];
-          acc_ld(acn, L.Ar + c.s * ab, b, a, b, 0, an0, false);
+          double acn[1][2][2];
+          acc_ld(acn, L.Ar + c.s * ab, b, a, b, FA, false);
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            acn[i][0][0] += Anf[i][0][0];
-            acn[i][0][1] += Anf[i][0][1];
+          for (int j = 0; j < 2; ++j) {
+            acn[0][j][0] += Anf[0][j][0];
+            acn[0][j][1] += Anf[0][j][1];
           }
-          acc_st_global(L.Arn + (2 * p - 1) * ab, acn, b, a, b, 0, an0, false, 1.0);
+          acc_st_global(L.Arn + (2 * p - 1) * ab, acn, b, a, b, FA, false, 1.0);
         }
         st_tile(L.Lon + (int64_t)(2 * p - 1) * bb, B, b, b, b, true);
       }
-      if (a > 0 && w < 4) acc_st_global(L.U + p * aa, Uac, a, a, a, 8 * (w >> 1), 8 * (w & 1), false, 1.0);
+      if (a > 0 && w < 4) acc_st_global(L.U + p * aa, Uac, a, a, a, FU, false, 1.0);
     } else if (a > 0) {
       // ---- tip (Alg. 1 l.12): L_nn = chol(A_nn + sum of every level's U), X_nn = W^T W (Alg. 2 l.1)
       __syncthreads();
       ld_tile(D, prm.tip, T, a, a, a, false, true);
       __syncthreads();
       if (w < 4) {
-        const int l = tid & 31, mm = 8 * (w >> 1) + (l >> 2), nn2 = 8 * (w & 1) + 2 * (l & 3);
+        const int l = tid & 31, mm = 8 * FU.rf[0] + (l >> 2), nn2 = 8 * FU.cf[0] + 2 * (l & 3);
         D[swz(mm, nn2)] += Uac[0][0][0];
         D[swz(mm, nn2 + 1)] += Uac[0][0][1];
       }
@@ -617,8 +850,8 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
       if (w < 4) {
         double acc[1][1][2];
         acc_zero(acc);
-        mma<1, 1, true, false, false>(acc, D, D, 8 * (w >> 1), 8 * (w & 1), 0, T);
-        acc_st_global(prm.tip, acc, a, a, a, 8 * (w >> 1), 8 * (w & 1), false, 1.0);
+        mma<1, 1, true, false, false>(acc, D, D, FU, T);
+        acc_st_global(prm.tip, acc, a, a, a, FU, false, 1.0);
       }
       if (tid == NT - 32) L.ldp[p] = lsum;
     }
@@ -658,7 +891,7 @@ extern "C" __global__ void __launch_bounds__(NT, 2) sb_factor_kernel(Params prm)
 //   X_{k+1,k} = -(X_{k+1,k+1} Lc~ + X_{n,k+1}^T Ln~ + Q_{k+1}^T Lf~)
 //   Q_k       = -(Q_{k+1} Lc~ + X_ff Lf~ + X_nf^T Ln~)                 (middle)
 //   X_{n,k}   = -(X_{n,k+1} Lc~ + X_nn Ln~ + X_nf Lf~)
-//   X_kk      = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~
+//   X_kk      = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~      (lower half, mirrored)
 // (reading R11: l.7's L_{0,i} is the factor fill-in block; Q_k = X_{f,k}).
 // ---------------------------------------------------------------------------
 constexpr int I_SMEM_DOUBLES = 6 * TD + 4 * AD;
@@ -670,8 +903,8 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
   const Level &L = prm.L;
   const int b = prm.b, a = prm.a, tid = threadIdx.x, w = tid >> 5;
   const int64_t bb = (int64_t)b * b, ab = (int64_t)a * b;
-  const int m0 = 16 * (w >> 1), n0 = 32 * (w & 1);
-  const int an0 = 8 * w;
+  const Frags<2, 4> F = lay64(w);
+  const Frags<1, 2> FA = layAR(w);
 
   for (int p = blockIdx.x; p < L.P; p += gridDim.x) {
     const Chain c = chain_of(L, p);
@@ -703,78 +936,82 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
       double *cpl = nxt ? coupling(L, c, k, bb, &tr) : nullptr;
       SB_STAMP(1, k, 0);
       ld_tile(W, L.D + bk * bb, T, b, b, b, false, true);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
       if (nxt) ld_tile(Lc, cpl, T, b, b, b, tr, false);
       if (mid) ld_tile(Lf, L.Bf + bk * bb, T, b, b, b, false, false);
       if (a > 0) ld_tile(Ln, L.Ar + bk * ab, AR, a, b, b, false, false);
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;\n" ::: "memory");
+      __syncthreads();
+      // ---- Lam = W^T W (lower half) while the other operands arrive
+      double aX[2][4][2];
+      acc_zero(aX);
+      mma64<true, false, false, B_GE, true>(aX, W, W, F);
       cp_wait_all();
       __syncthreads();
       SB_STAMP(1, k, 1);
-      // ---- Lc~, Lf~, Ln~ (W lower: W[kk][n] = 0 for kk < n) and Lam = W^T W
-      double aX[2][4][2];
-      acc_zero(aX);
-      mma<2, 4, true, false, false>(aX, W, W, m0, n0, max(m0, n0), T);
+      // ---- Lc~, Lf~, Ln~ (W lower)
       {
-        double aL[2][4][2], aF[2][4][2], aN[2][1][2];
+        double aL[2][4][2], aF[2][4][2], aN[1][2][2];
         if (nxt) {
           acc_zero(aL);
-          mma<2, 4, false, false, false>(aL, Lc, W, m0, n0, n0, T);
+          mma64<false, false, false, B_GE>(aL, Lc, W, F);
         }
         if (mid) {
           acc_zero(aF);
-          mma<2, 4, false, false, false>(aF, Lf, W, m0, n0, n0, T);
+          mma64<false, false, false, B_GE>(aF, Lf, W, F);
         }
         if (a > 0) {
           acc_zero(aN);
-          mma<2, 1, false, false, false>(aN, Ln, W, 0, an0, an0, T);
+          mma<1, 2, false, false, false, B_GE>(aN, Ln, W, FA, T);
         }
         __syncthreads();
-        if (nxt) acc_st_smem(Lc, aL, m0, n0, 1.0);
-        if (mid) acc_st_smem(Lf, aF, m0, n0, 1.0);
-        if (a > 0) acc_st_smem(Ln, aN, 0, an0, 1.0);
+        if (nxt) acc_st_smem(Lc, aL, F, 1.0);
+        if (mid) acc_st_smem(Lf, aF, F, 1.0);
+        if (a > 0) acc_st_smem(Ln, aN, FA, 1.0);
       }
       __syncthreads();
       SB_STAMP(1, k, 2);
       // ---- X_{k+1,k}, Q_k, X_{n,k}  (W is dead: its buffer receives X_{k+1,k})
       {
-        double aA[2][4][2], aB[2][4][2], aN[2][1][2];
+        double aA[2][4][2], aB[2][4][2], aN[1][2][2];
         if (nxt) {
           acc_zero(aA);
-          mma<2, 4, false, false, false>(aA, Xd, Lc, m0, n0, 0, T);
-          if (a > 0) mma<2, 4, true, false, false>(aA, Xn, Ln, m0, n0, 0, AR);
-          if (mid) mma<2, 4, true, false, false>(aA, Q, Lf, m0, n0, 0, T);
+          mma64<false, false, false>(aA, Xd, Lc, F);
+          if (a > 0) mma64<true, false, false, K_FULL, false, AR>(aA, Xn, Ln, F);
+          if (mid) mma64<true, false, false>(aA, Q, Lf, F);
         }
         if (mid) {
           acc_zero(aB);
-          mma<2, 4, false, false, false>(aB, Q, Lc, m0, n0, 0, T);
-          mma<2, 4, false, false, false>(aB, Xff, Lf, m0, n0, 0, T);
-          if (a > 0) mma<2, 4, true, false, false>(aB, Xnf, Ln, m0, n0, 0, AR);
+          mma64<false, false, false>(aB, Q, Lc, F);
+          mma64<false, false, false>(aB, Xff, Lf, F);
+          if (a > 0) mma64<true, false, false, K_FULL, false, AR>(aB, Xnf, Ln, F);
         }
         if (a > 0) {
           acc_zero(aN);
-          if (nxt) mma<2, 1, false, false, false>(aN, Xn, Lc, 0, an0, 0, T);
-          mma<2, 1, false, false, false>(aN, Xnn, Ln, 0, an0, 0, AR);
-          if (mid) mma<2, 1, false, false, false>(aN, Xnf, Lf, 0, an0, 0, T);
+          if (nxt) mma<1, 2, false, false, false>(aN, Xn, Lc, FA, T);
+          mma<1, 2, false, false, false>(aN, Xnn, Ln, FA, AR);
+          if (mid) mma<1, 2, false, false, false>(aN, Xnf, Lf, FA, T);
         }
         __syncthreads();
         if (nxt) {
-          acc_st_smem(W, aA, m0, n0, -1.0);
-          acc_st_global(cpl, aA, b, b, b, m0, n0, tr, -1.0);
+          acc_st_smem(W, aA, F, -1.0);
+          acc_st_global(cpl, aA, b, b, b, F, tr, -1.0);
         }
-        if (mid) acc_st_smem(Q, aB, m0, n0, -1.0);
+        if (mid) acc_st_smem(Q, aB, F, -1.0);
         if (a > 0) {
-          acc_st_smem(Xn, aN, 0, an0, -1.0);
-          acc_st_global(L.Ar + bk * ab, aN, b, a, b, 0, an0, false, -1.0);
+          acc_st_smem(Xn, aN, FA, -1.0);
+          acc_st_global(L.Ar + bk * ab, aN, b, a, b, FA, false, -1.0);
         }
       }
       __syncthreads();
       SB_STAMP(1, k, 3);
-      // ---- X_kk = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~
-      if (nxt) mma<2, 4, true, false, true>(aX, W, Lc, m0, n0, 0, T);
-      if (a > 0) mma<2, 4, true, false, true>(aX, Xn, Ln, m0, n0, 0, AR);
-      if (mid) mma<2, 4, true, false, true>(aX, Q, Lf, m0, n0, 0, T);
-      acc_st_smem(Xd, aX, m0, n0, 1.0);
-      acc_st_global(L.D + bk * bb, aX, b, b, b, m0, n0, false, 1.0);
+      // ---- X_kk = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~ (lower half, mirrored: symmetric)
+      if (nxt) mma64<true, false, true, K_FULL, true>(aX, W, Lc, F);
+      if (a > 0) mma64<true, false, true, K_FULL, true, AR>(aX, Xn, Ln, F);
+      if (mid) mma64<true, false, true, K_FULL, true>(aX, Q, Lf, F);
+      acc_st_smem<2, 4, true, true>(Xd, aX, F, 1.0);
       __syncthreads();
+      st_tile(L.D + bk * bb, Xd, b, b, b, false);  // coalesced (the lower half was mirrored in smem)
       SB_STAMP(1, k, 4);
     }
     if (mid) {  // X_{s+1,s} = Q_{s+1}^T (reading R10)
@@ -975,7 +1212,7 @@ int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, doubl
   }
   int nlaunch = 0;
   for (int l = 0; l < L; ++l) {
-    const int grid = std::max(1, std::min(prm[l].L.P, 2 * sms));
+    const int grid = std::max(1, std::min(prm[l].L.P, sms));
     dev::sb_factor_kernel<<<grid, dev::NT, dev::F_SMEM_DOUBLES * 8, st>>>(prm[l]);
     ++nlaunch;
   }

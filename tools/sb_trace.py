@@ -13,6 +13,13 @@ import paper_2503_17528_b200 as sb  # noqa: E402
 from paper_2503_17528_b200 import _lib  # noqa: E402
 
 
+def chol_rounds(buf, lvl, k):
+    """chol_inv64 internal stamps of step k at level lvl (factor kernel, traced partition)."""
+    t = buf.view(-1).cpu().numpy().astype(np.int64)
+    base = ((8 + lvl) * 2 * 128 + 2 * k) * 8
+    return t[base:base + 16]
+
+
 def main():
     n, b, a = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
     Ps = sb.sb_auto_plan(n, b, a) if len(sys.argv) < 5 else [int(x) for x in sys.argv[4].split("x")]
@@ -42,7 +49,21 @@ def main():
             parts = "  ".join(f"{names[kern][i]} {d[:, i].mean():6.2f}" for i in range(4))
             print(f"level {lvl} {'factor ' if kern == 0 else 'inverse'} steps {len(steps):3d}  "
                   f"step {tot.mean():6.2f} us:  {parts}")
+            if kern == 0 and lvl < 8:
+                # chol_inv64 rounds: leaf(+copy) and trailing phases, then the W = L^{-1} phase
+                rows = []
+                for k in steps[:16]:
+                    c = chol_rounds(buf, lvl, k)
+                    t0 = T[k, 0]
+                    if not c[15]:
+                        continue
+                    ev = [t0] + [c[i] for i in range(15)] + [c[15]]
+                    rows.append(np.diff(np.array(ev, dtype=np.int64)) / 1e3)
+                if rows:
+                    r = np.array(rows).mean(axis=0)
+                    print("    chol: " + " ".join(f"{x:5.2f}" for x in r) + "  (leaf_j trail_j ..., leaf_7, W)")
 
 
 if __name__ == "__main__":
     main()
+
