@@ -1685,7 +1685,9 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
     s_q = q;
   }
   __syncthreads();
-  if (s_q >= 0) run_tasks(p, smem, s_task, s_q);
+  const int q0 = s_q;  // read before run_tasks' thread 0 reuses s_q
+  __syncthreads();
+  if (q0 >= 0) run_tasks(p, smem, s_task, s_q);
   // the last CTA out merges the NaN-pivot failures into *info (only if there was
   // no genuine failure): every other CTA's records are ordered before its
   // fence + increment of the exit counter

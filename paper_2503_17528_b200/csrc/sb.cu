@@ -258,6 +258,31 @@ __device__ __forceinline__ void mma(double (&acc)[MI][NI][2], const double *A, c
     klo = min(klo, BM == B_GE ? 8 * F.cf[j] : 0);
     khi = max(khi, BM == B_LE ? min(K, 8 * F.cf[j] + 8) : K);
   }
+  if (BM == K_FULL && (K == T || K == AR)) {  // full products: fully unrolled k loop
+    if (K == T) {
+#pragma unroll
+      for (int k = 0; k < T; k += 4) {
+        double af[MI], bf[NI];
+        const int kk = k + lc;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int m = 8 * F.rf[i] + lr;
+          const double v = TA ? A[swz(kk, m)] : A[swz(m, kk)];
+          af[i] = NEG ? -v : v;
+        }
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const int n = 8 * F.cf[j] + lr;
+          bf[j] = TB ? B[swz(n, kk)] : B[swz(kk, n)];
+        }
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NI; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
+      return;
+    }
+  }
 #pragma unroll 2
   for (int k = klo; k < khi; k += 4) {
     double af[MI], bf[NI];
@@ -383,19 +408,19 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 // Right-looking on 8-column panels with look-ahead:
 //   warp 0 (the critical chain), round j: factors the 8 x 8 diagonal block (j,j)
 //     on ONE thread in registers (8 rsqrt + FMA steps, the product-form inverse
-//     W_jj alongside), publishes L_jj / W_jj (named barrier, arrive), waits for
-//     the workers' round j-1, then computes L_{j+1,j} = A_{j+1,j} W_jj^T and the
-//     panel-j update of the next diagonal block (j+1,j+1) itself;
-//   warps 1..7 (workers), round j: wait for W_jj, update every other trailing
+//     W_jj alongside; W_jj replaces the block), publishes it (named barrier,
+//     arrive), waits for the workers' round j-1, then computes L_{j+1,j} =
+//     A_{j+1,j} W_jj^T and the panel-j update of the next diagonal block itself;
+//   warps 1..7 (workers), round j: wait for W_jj; update every other trailing
 //     tile (i,k), j < k <= i, computing the panel blocks they need themselves
 //     (L_ij = A_ij W_jj^T, written transposed into the free upper block (j,i) --
 //     the same values from every warp that computes them -- and read back as
-//     fragments), then arrive on the round's barrier.
-// The panel blocks move from the scratch into place at the end; then
-// W = L^{-1} by W_21 = -W_22 L_21 W_11 on 8 / 16 / 32 levels.  *s_bad = 2 x the
-// first non-positive pivot index + 1 if that pivot is NaN; 128 if none.
-// Called by all NT threads; needs the registers of one thread for the leaf (the
-// kernels that call it run 1 CTA per SM).
+//     fragments); and block row j of W: W_jm = -W_jj sum_{k=m}^{j-1} L_jk W_km
+//     (m < j), written over the dead A_jm; then arrive on the round's barrier.
+// L itself is never assembled: only W = L^{-1} and the pivots are outputs.
+// *s_bad = 2 x the first non-positive pivot index + 1 if that pivot is NaN; 128 if
+// none.  Wd: 8 x 64 per-warp scratch.  Called by all NT threads; needs the
+// registers of one thread for the leaf (the kernels that call it run 1 CTA / SM).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -408,8 +433,8 @@ __device__ __forceinline__ void nbar_sync(int id) { asm volatile("bar.sync %0, 2
 // the trailing update of tile (i, k) by panel j (R = 8j): L_ij, L_kj computed in-warp
 // into the transposed scratch (j, i), (j, k), then A_ik -= L_ij L_kj^T.  Up to 4 tiles
 // of one warp in flight together.
-__device__ __forceinline__ void trail_tiles(double *D, const double *Wd, int R, const int (&ti)[4],
-                                            const int (&tk)[4], const bool (&on)[4]) {
+__device__ __forceinline__ void trail_tiles(double *D, int R, const int (&ti)[4], const int (&tk)[4],
+                                            const bool (&on)[4]) {
   const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
   double li[4][2], lk[4][2];
 #pragma unroll
@@ -418,7 +443,7 @@ __device__ __forceinline__ void trail_tiles(double *D, const double *Wd, int R, 
     if (!on[u]) continue;
 #pragma unroll
     for (int kk = 0; kk < 8; kk += 4) {
-      const double wv = Wd[swz(lr, R + kk + lc)];
+      const double wv = D[swz(R + lr, R + kk + lc)];  // (W_jj^T)[kk][n] = W_jj[n][kk]
       dmma(li[u], D[swz(8 * ti[u] + lr, R + kk + lc)], wv);
       if (tk[u] != ti[u]) dmma(lk[u], D[swz(8 * tk[u] + lr, R + kk + lc)], wv);
     }
@@ -496,28 +521,24 @@ __device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad, unsig
         for (int i = 0; i < 8; ++i) {
           ldg[R + i] = a[i][i];
           double *rp = D + (R + i) * T + (R ^ ((i & 3) << 3));
-          double *wp = Wd + i * T + (R ^ ((i & 3) << 3));
 #pragma unroll
-          for (int c = 0; c < 8; c += 2) {
+          for (int c = 0; c < 8; c += 2)
             *(double2 *)(rp + (c ^ (i & 4))) =
-                make_double2(c <= i ? a[i][c] : 0.0, c + 1 <= i ? a[i][c + 1] : 0.0);
-            *(double2 *)(wp + (c ^ (i & 4))) =
                 make_double2(c <= i ? wv[i][c] : 0.0, c + 1 <= i ? wv[i][c + 1] : 0.0);
-          }
         }
       }
       __syncwarp();
       if (stamp && l == 0) stamp[2 * j] = gtimer();
+      nbar_arrive(1 + (j & 1));  // W_jj published
       if (j == 7) {
-        nbar_sync(3 + (6 & 1));  // the workers' last round (complete every barrier generation)
+        nbar_sync(3 + (6 & 1));  // the workers' round 6 (complete every barrier generation)
         break;
       }
-      nbar_arrive(1 + (j & 1));                 // L_jj, W_jj published
       if (j > 0) nbar_sync(3 + ((j - 1) & 1));  // the workers' round j-1 is done
       // look-ahead: the next diagonal block gets its panel-j update from this warp
       const int ti[4] = {j + 1, 0, 0, 0}, tk[4] = {j + 1, 0, 0, 0};
       const bool on[4] = {true, false, false, false};
-      trail_tiles(D, Wd, R, ti, tk, on);
+      trail_tiles(D, R, ti, tk, on);
       __syncwarp();
       if (stamp && l == 0) stamp[2 * j + 1] = gtimer();
     }
@@ -525,16 +546,19 @@ __device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad, unsig
     for (int o = 16; o; o >>= 1) bad = min(bad, __shfl_xor_sync(FULL, bad, o));
     if (l == 0) *s_bad = bad;
   } else {
-    for (int j = 0; j < 7; ++j) {
+    const int wk = w - 1;
+    // this warp's 8 x 8 scratch: columns 8w..8w+7 of Wd
+    for (int j = 0; j < 8; ++j) {
       const int R = 8 * j;
       nbar_sync(1 + (j & 1));  // W_jj ready
-      // tiles (i, k), j < k <= i, except (j+1, j+1), round-robin over warps 1..7
-      const int nb = 7 - j, np = nb * (nb + 1) / 2 - 1;
+      // items: trailing tiles (i, k), j < k <= i, except (j+1, j+1); then the blocks
+      // (j, m), m < j, of W; round-robin over the 7 workers (<= 4 each)
+      const int nb = 7 - j, np = j < 7 ? nb * (nb + 1) / 2 - 1 : 0;
       int ti[4], tk[4];
       bool on[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int t = (w - 1) + 7 * u;
+        const int t = wk + 7 * u;
         on[u] = t < np;
         int ii = 0, tt = on[u] ? t + 1 : 1;  // skip tile 0 = (j+1, j+1)
         while (tt > ii) {
@@ -544,83 +568,31 @@ __device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad, unsig
         ti[u] = j + 1 + ii;
         tk[u] = j + 1 + tt;
       }
-      trail_tiles(D, Wd, R, ti, tk, on);
-      nbar_arrive(3 + (j & 1));  // round j done
-    }
-  }
-  __syncthreads();
-  // panel blocks into place: scratch (j, i) holds L_ij^T, i > j (rows 8j+8.. of column block j)
+      if (np > 0) trail_tiles(D, R, ti, tk, on);
+#pragma unroll 1
+      for (int u = 0; u < 4; ++u) {
+        const int m = wk + 7 * u - np;
+        if (m < 0 || m >= j) continue;
+        // T = sum_{k=m}^{j-1} L_jk W_km (L_jk^T in the scratch block (k, j))
+        double t2[2] = {0.0, 0.0};
+        for (int k = m; k < j; ++k) {
 #pragma unroll
-  for (int j = 0; j < 7; ++j)
-    for (int e = tid; e < (56 - 8 * j) * 8; e += NT) {
-      const int r = 8 * j + 8 + (e >> 3), c = 8 * j + (e & 7);
-      D[swz(r, c)] = D[swz(c, r)];
-    }
-  __syncthreads();
-  // ---- W = L^{-1}: diagonal blocks from Wd
-  for (int i = tid; i < 8 * T; i += NT) {
-    const int r = i >> 6, c = i & 63, jb = c >> 3;
-    D[swz(8 * jb + r, c)] = Wd[swz(r, c)];
-  }
-  __syncthreads();
-  // level 8: W_{2p+1,2p} = -W_{2p+1,2p+1} (L_{2p+1,2p} W_{2p,2p}); T in block (2p, 2p+1)
-  if (w < 4) {
-    const int b0 = 16 * w;
-    double acc[2] = {0.0, 0.0};
+          for (int kk = 0; kk < 8; kk += 4)
+            dmma(t2, D[swz(8 * k + kk + lc, R + lr)], D[swz(8 * k + kk + lc, 8 * m + lr)]);
+        }
+        *(double2 *)(Wd + swz(lr, 8 * w + 2 * lc)) = make_double2(t2[0], t2[1]);
+        __syncwarp();
+        double w2[2] = {0.0, 0.0};
 #pragma unroll
-    for (int kk = 0; kk < 8; kk += 4) dmma(acc, D[swz(b0 + 8 + lr, b0 + kk + lc)], D[swz(b0 + kk + lc, b0 + lr)]);
-    *(double2 *)(D + swz(b0 + lr, b0 + 8 + 2 * lc)) = make_double2(acc[0], acc[1]);
-    __syncwarp();
-    acc[0] = acc[1] = 0.0;
-#pragma unroll
-    for (int kk = 0; kk < 8; kk += 4)
-      dmma(acc, -D[swz(b0 + 8 + lr, b0 + 8 + kk + lc)], D[swz(b0 + kk + lc, b0 + 8 + lr)]);
-    *(double2 *)(D + swz(b0 + 8 + lr, b0 + 2 * lc)) = make_double2(acc[0], acc[1]);
-  }
-  __syncthreads();
-  // level 16: quads q (base 32q): T = L21 W11 -> rows 32q.., cols 32q+16.. ; W21 = -W22 T
-  // (block-lower k ranges: the strict-upper blocks hold the previous level's T)
-  {
-    const int q = w >> 2, fi = (w >> 1) & 1, fj = w & 1, b0 = 32 * q;
-    double acc[2] = {0.0, 0.0};
-    for (int kk = 8 * fj; kk < 16; kk += 4)
-      dmma(acc, D[swz(b0 + 16 + 8 * fi + lr, b0 + kk + lc)], D[swz(b0 + kk + lc, b0 + 8 * fj + lr)]);
-    *(double2 *)(D + swz(b0 + 8 * fi + lr, b0 + 16 + 8 * fj + 2 * lc)) = make_double2(acc[0], acc[1]);
-    __syncthreads();
-    acc[0] = acc[1] = 0.0;
-    for (int kk = 0; kk < 8 * (fi + 1); kk += 4)
-      dmma(acc, -D[swz(b0 + 16 + 8 * fi + lr, b0 + 16 + kk + lc)], D[swz(b0 + kk + lc, b0 + 16 + 8 * fj + lr)]);
-    *(double2 *)(D + swz(b0 + 16 + 8 * fi + lr, b0 + 8 * fj + 2 * lc)) = make_double2(acc[0], acc[1]);
-    __syncthreads();
-  }
-  // level 32: T = L21 W11 (32 x 32) -> rows 0..31, cols 32..63 ; W21 = -W22 T
-  {
-    const int fi = w >> 1, fj0 = (w & 1) * 2;
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    for (int kk = 8 * fj0; kk < 32; kk += 4) {
-      const double a = D[swz(32 + 8 * fi + lr, kk + lc)];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const double bv = D[swz(kk + lc, 8 * (fj0 + e) + lr)];
-        dmma(acc[e], a, (kk >> 3) >= fj0 + e ? bv : 0.0);
+        for (int kk = 0; kk < 8; kk += 4) dmma(w2, -D[swz(R + lr, R + kk + lc)], Wd[swz(kk + lc, 8 * w + lr)]);
+        *(double2 *)(D + swz(R + lr, 8 * m + 2 * lc)) = make_double2(w2[0], w2[1]);
+        __syncwarp();
       }
+      if (j < 7) nbar_arrive(3 + (j & 1));  // round j done
     }
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-      *(double2 *)(D + swz(8 * fi + lr, 32 + 8 * (fj0 + e) + 2 * lc)) = make_double2(acc[e][0], acc[e][1]);
-    __syncthreads();
-    acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.0;
-    for (int kk = 0; kk < 8 * (fi + 1); kk += 4) {
-      const double a = -D[swz(32 + 8 * fi + lr, 32 + kk + lc)];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) dmma(acc[e], a, D[swz(kk + lc, 32 + 8 * (fj0 + e) + lr)]);
-    }
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-      *(double2 *)(D + swz(32 + 8 * fi + lr, 8 * (fj0 + e) + 2 * lc)) = make_double2(acc[e][0], acc[e][1]);
-    __syncthreads();
   }
-  // strict-upper blocks -> 0 (W is lower triangular)
+  __syncthreads();
+  // strict-upper blocks (the panel scratch) -> 0: W is lower triangular
   for (int i = tid; i < TD; i += NT) {
     const int r = i >> 6, c = i & 63;
     if ((c >> 3) > (r >> 3)) D[swz(r, c)] = 0.0;
@@ -766,17 +738,17 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
       __syncthreads();
       SB_STAMP(0, k, 3);
       // ---- Schur updates (Alg. 1 l.5-7, Alg. 4 l.9-12); W is dead
-      if (nxt) {  // A_{k+1,k+1} - L_{k+1,k} L_{k+1,k}^T -> D (lower fragments: POTRF reads the lower triangle)
+      if (nxt) {  // A_{k+1,k+1} - L_{k+1,k} L_{k+1,k}^T -> D
         double acc[2][4][2];
         acc_ld_smem(acc, Dn, F);
-        mma64<false, true, true, K_FULL, true>(acc, X, X, F);
-        acc_st_smem<2, 4, true>(D, acc, F, 1.0);
+        mma64<false, true, true>(acc, X, X, F);
+        acc_st_smem(D, acc, F, 1.0);
       }
       if (a > 0) {
         if (w < 4) mma<1, 1, false, true, true>(Uac, Ar, Ar, FU, T);  // U -= Ln Ln^T
         if (mid) mma<1, 2, false, true, true>(Anf, Ar, B, FA, T);       // A_nf -= Ln B^T
       }
-      if (mid) mma64<false, true, true, K_FULL, true>(Aff, B, B, F);  // A_ff -= B B^T (lower)
+      if (mid) mma64<false, true, true>(Aff, B, B, F);  // A_ff -= B B^T
       double accA[1][2][2];
       if (a > 0 && nxt) {  // A_{n,k+1} - L_{n,k} L_{k+1,k}^T
         acc_ld_smem(accA, An, FA);
@@ -805,7 +777,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
       if (a > 0) st_tile(L.Arn + ib * ab, Ar, a, b, b, false);
       if (c.type != P_BOT) cp_block(L.Lon + (int64_t)(c.type == P_TOP ? 0 : 2 * p) * bb, L.Lo + (c.e - 1) * bb, bb);
       if (mid) {
-        // A_ff + sum(-B B^T) (lower), A_{n,f} + sum(-Ln B^T), (L_p, F_p) coupling = B_{e-1}^T
+        // A_ff + sum(-B B^T), A_{n,f} + sum(-Ln B^T), (L_p, F_p) coupling = B_{e-1}^T
         double acc[2][4][2];
         acc_ld(acc, L.D + c.s * bb, b, b, b, F, false);
 #pragma unroll
@@ -815,7 +787,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
             acc[i][j][0] += Aff[i][j][0];
             acc[i][j][1] += Aff[i][j][1];
           }
-        acc_st_global<2, 4, true>(L.Dn + (2 * p - 1) * bb, acc, b, b, b, F, false, 1.0);
+        acc_st_global(L.Dn + (2 * p - 1) * bb, acc, b, b, b, F, false, 1.0);
         if (a > 0) {
           double acn[1][2][2];
           acc_ld(acn, L.Ar + c.s * ab, b, a, b, FA, false);
@@ -891,7 +863,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
 //   X_{k+1,k} = -(X_{k+1,k+1} Lc~ + X_{n,k+1}^T Ln~ + Q_{k+1}^T Lf~)
 //   Q_k       = -(Q_{k+1} Lc~ + X_ff Lf~ + X_nf^T Ln~)                 (middle)
 //   X_{n,k}   = -(X_{n,k+1} Lc~ + X_nn Ln~ + X_nf Lf~)
-//   X_kk      = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~      (lower half, mirrored)
+//   X_kk      = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~
 // (reading R11: l.7's L_{0,i} is the factor fill-in block; Q_k = X_{f,k}).
 // ---------------------------------------------------------------------------
 constexpr int I_SMEM_DOUBLES = 6 * TD + 4 * AD;
@@ -945,7 +917,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
       // ---- Lam = W^T W (lower half) while the other operands arrive
       double aX[2][4][2];
       acc_zero(aX);
-      mma64<true, false, false, B_GE, true>(aX, W, W, F);
+      mma64<true, false, false, B_GE>(aX, W, W, F);
       cp_wait_all();
       __syncthreads();
       SB_STAMP(1, k, 1);
@@ -1005,13 +977,13 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
       }
       __syncthreads();
       SB_STAMP(1, k, 3);
-      // ---- X_kk = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~ (lower half, mirrored: symmetric)
-      if (nxt) mma64<true, false, true, K_FULL, true>(aX, W, Lc, F);
-      if (a > 0) mma64<true, false, true, K_FULL, true, AR>(aX, Xn, Ln, F);
-      if (mid) mma64<true, false, true, K_FULL, true>(aX, Q, Lf, F);
-      acc_st_smem<2, 4, true, true>(Xd, aX, F, 1.0);
+      // ---- X_kk = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~
+      if (nxt) mma64<true, false, true>(aX, W, Lc, F);
+      if (a > 0) mma64<true, false, true, K_FULL, false, AR>(aX, Xn, Ln, F);
+      if (mid) mma64<true, false, true>(aX, Q, Lf, F);
+      acc_st_smem(Xd, aX, F, 1.0);
       __syncthreads();
-      st_tile(L.D + bk * bb, Xd, b, b, b, false);  // coalesced (the lower half was mirrored in smem)
+      st_tile(L.D + bk * bb, Xd, b, b, b, false);  // coalesced
       SB_STAMP(1, k, 4);
     }
     if (mid) {  // X_{s+1,s} = Q_{s+1}^T (reading R10)

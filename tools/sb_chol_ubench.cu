@@ -74,7 +74,14 @@ __global__ void k_gemm(double *out, unsigned long long *st, int reps, int mode) 
     if (mode == 0) mma64<false, true, false>(acc, A, B, F);
     else if (mode == 1) mma64<false, false, false>(acc, A, B, F);
     else if (mode == 2) mma64<true, false, false>(acc, A, B, F);
-    else mma64<false, true, false, B_LE>(acc, A, B, F);
+    else if (mode == 3) mma64<false, true, false, B_LE>(acc, A, B, F);
+    else if (mode == 4) mma64<true, false, true, K_FULL, true>(acc, A, B, F);
+    else if (mode == 5) mma64<true, false, false, K_FULL, false, AR>(acc, A, B, F);
+    else if (mode == 6) {
+      double a2[1][2][2] = {};
+      mma<1, 2, false, false, false>(a2, A, B, layAR(threadIdx.x >> 5), T);
+      acc[0][0][0] += a2[0][0][0] + a2[0][1][1];
+    } else mma64<true, false, false, B_GE, true>(acc, A, B, F);
   }
   __syncthreads();
   long long t1 = clock64();
@@ -91,8 +98,9 @@ struct GemmBench {
     cudaMalloc(&o, 4096 * 8);
     cudaMalloc(&s, 8);
     cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TD * 8);
-    const char *nm[4] = {"NT (A B^T)", "NN (A B)", "TN (A^T B)", "NT, B = W^T (B_LE)"};
-    for (int m = 0; m < 4; ++m) {
+    const char *nm[8] = {"NT (A B^T)", "NN (A B)", "TN (A^T B)", "NT, B = W^T (B_LE)", "TN LOW (X_kk terms)",
+                         "TN K=16 (arrow contraction)", "arrow out 16x64 K=64", "TN B_GE LOW (Lam)"};
+    for (int m = 0; m < 8; ++m) {
       k_gemm<<<1, NT, 2 * TD * 8>>>(o, s, 200, m);
       cudaDeviceSynchronize();
       cudaMemcpy(&h, s, 8, cudaMemcpyDeviceToHost);
