@@ -1623,7 +1623,6 @@ __device__ void run_logdet(const Params &p, const Task &T, double *smem) {
   }
 }
 
-__device__ void run_tasks(const Params &p, double *smem, int &s_task, int &s_q);
 }  // namespace dev
 
 extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev::Params p) {
@@ -1685,9 +1684,85 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
     s_q = q;
   }
   __syncthreads();
-  const int q0 = s_q;  // read before run_tasks' thread 0 reuses s_q
+  const int q0 = s_q;  // read before thread 0 reuses s_q for the claims
   __syncthreads();
-  if (q0 >= 0) run_tasks(p, smem, s_task, s_q);
+  if (q0 >= 0) {
+    unsigned long long t_claim = 0, t_start = 0;
+    for (;;) {
+      if (threadIdx.x == 0) {
+        int q = s_q, t = -1;
+        for (;;) {
+          const int idx = atomicAdd(p.qclaim + q, 1);
+          if (idx < p.qoff[q + 1] - p.qoff[q]) {
+            t = p.qlist[p.qoff[q] + idx];
+            break;
+          }
+          if (q == 0) break;
+          q = 0;  // critical queue drained: help with the bulk queue
+        }
+        s_q = q;
+        s_task = t;
+      }
+      __syncthreads();
+      const int t = s_task;
+      if (t < 0) break;
+      const Task T = p.tasks[t];
+      if (p.trace && threadIdx.x == 0) t_claim = globaltimer();
+      if (threadIdx.x == 0) {
+        for (int w = 0; w < T.nwait - T.nlate; ++w) {
+          const Wait W = p.waits[T.wait0 + w];
+          if (ld_acquire(p.ctr + W.ctr) >= W.target) continue;
+          int ns = 32;
+          const unsigned long long t0 = globaltimer();
+          while (ld_acquire(p.ctr + W.ctr) < W.target) {
+            __nanosleep(ns);
+            ns = min(ns * 2, 256);
+            if (globaltimer() - t0 > 20000000000ULL) {  // 20 s watchdog: never hang the GPU
+              atomicExch(p.info, -1);
+              break;
+            }
+          }
+        }
+      }
+      if (p.trace && threadIdx.x == 0) t_start = globaltimer();
+      __syncthreads();
+      switch (T.type) {
+        case TK_GEMM:
+          if (T.m > SERINV_TILE) run_gemm_wide(p, T, smem);
+          else run_gemm(p, T, smem, t);
+          break;
+        case TK_POTRF: run_potrf_trtri(p, T, smem, true, t); break;
+        case TK_TRTRI: run_potrf_trtri(p, T, smem, false, t); break;
+        case TK_REDUCE: run_reduce(p, T); break;
+        case TK_COPY: run_copy(p, T); break;
+        case TK_LOGDET: run_logdet(p, T, smem); break;
+        default: break;
+      }
+      // publish: barrier (CTA-scope ordering of every thread's stores) then one
+      // gpu-scope fence by the signalling thread (cumulative) and the increments.
+      // The last warp publishes while thread 0 already claims the next task.
+      __syncthreads();
+      if (threadIdx.x == NT - 32) {
+        __threadfence();
+        const bool ew = T.type == TK_POTRF && (T.flags & TF_EARLY_SIG) && (T.flags & TF_W_OUT);
+        const bool cs = ew && (T.flags & TF_CHAINSTEP);
+        // early-published signals: sigs[0] (W), or sigs[1] (W) and sigs[2] (sub-diagonal tile) of a chain step
+        for (int s = (ew && !cs) ? 1 : 0; s < T.nsig; ++s)
+          if (!(cs && (s == 1 || s == 2))) atomicAdd(p.ctr + p.sigs[T.sig0 + s], 1);
+        if (p.trace) {
+          unsigned long long *rec = p.trace + 4 * (size_t)t;
+          rec[2] = globaltimer();
+          rec[3] = (unsigned long long)(unsigned)T.type | ((unsigned long long)smid() << 16) |
+                   ((unsigned long long)(unsigned)T.m << 32) | ((unsigned long long)(unsigned)T.flags << 48);
+        }
+      }
+      if (threadIdx.x == 0 && p.trace) {
+        unsigned long long *rec = p.trace + 4 * (size_t)t;
+        rec[0] = t_claim;
+        rec[1] = t_start;
+      }
+    }
+  }
   // the last CTA out merges the NaN-pivot failures into *info (only if there was
   // no genuine failure): every other CTA's records are ordered before its
   // fence + increment of the exit counter
@@ -1701,85 +1776,6 @@ extern "C" __global__ void __launch_bounds__(dev::NT, 2) serinv_exec_kernel(dev:
   }
 }
 
-namespace dev {
-__device__ void run_tasks(const Params &p, double *smem, int &s_task, int &s_q) {
-  unsigned long long t_claim = 0, t_start = 0;
-  for (;;) {
-    if (threadIdx.x == 0) {
-      int q = s_q, t = -1;
-      for (;;) {
-        const int idx = atomicAdd(p.qclaim + q, 1);
-        if (idx < p.qoff[q + 1] - p.qoff[q]) {
-          t = p.qlist[p.qoff[q] + idx];
-          break;
-        }
-        if (q == 0) break;
-        q = 0;  // critical queue drained: help with the bulk queue
-      }
-      s_q = q;
-      s_task = t;
-    }
-    __syncthreads();
-    const int t = s_task;
-    if (t < 0) break;
-    const Task T = p.tasks[t];
-    if (p.trace && threadIdx.x == 0) t_claim = globaltimer();
-    if (threadIdx.x == 0) {
-      for (int w = 0; w < T.nwait - T.nlate; ++w) {
-        const Wait W = p.waits[T.wait0 + w];
-        if (ld_acquire(p.ctr + W.ctr) >= W.target) continue;
-        int ns = 32;
-        const unsigned long long t0 = globaltimer();
-        while (ld_acquire(p.ctr + W.ctr) < W.target) {
-          __nanosleep(ns);
-          ns = min(ns * 2, 256);
-          if (globaltimer() - t0 > 20000000000ULL) {  // 20 s watchdog: never hang the GPU
-            atomicExch(p.info, -1);
-            break;
-          }
-        }
-      }
-    }
-    if (p.trace && threadIdx.x == 0) t_start = globaltimer();
-    __syncthreads();
-    switch (T.type) {
-      case TK_GEMM:
-        if (T.m > SERINV_TILE) run_gemm_wide(p, T, smem);
-        else run_gemm(p, T, smem, t);
-        break;
-      case TK_POTRF: run_potrf_trtri(p, T, smem, true, t); break;
-      case TK_TRTRI: run_potrf_trtri(p, T, smem, false, t); break;
-      case TK_REDUCE: run_reduce(p, T); break;
-      case TK_COPY: run_copy(p, T); break;
-      case TK_LOGDET: run_logdet(p, T, smem); break;
-      default: break;
-    }
-    // publish: barrier (CTA-scope ordering of every thread's stores) then one
-    // gpu-scope fence by the signalling thread (cumulative) and the increments.
-    // The last warp publishes while thread 0 already claims the next task.
-    __syncthreads();
-    if (threadIdx.x == NT - 32) {
-      __threadfence();
-      const bool ew = T.type == TK_POTRF && (T.flags & TF_EARLY_SIG) && (T.flags & TF_W_OUT);
-      const bool cs = ew && (T.flags & TF_CHAINSTEP);
-      // early-published signals: sigs[0] (W), or sigs[1] (W) and sigs[2] (sub-diagonal tile) of a chain step
-      for (int s = (ew && !cs) ? 1 : 0; s < T.nsig; ++s)
-        if (!(cs && (s == 1 || s == 2))) atomicAdd(p.ctr + p.sigs[T.sig0 + s], 1);
-      if (p.trace) {
-        unsigned long long *rec = p.trace + 4 * (size_t)t;
-        rec[2] = globaltimer();
-        rec[3] = (unsigned long long)(unsigned)T.type | ((unsigned long long)smid() << 16) |
-                 ((unsigned long long)(unsigned)T.m << 32) | ((unsigned long long)(unsigned)T.flags << 48);
-      }
-    }
-    if (threadIdx.x == 0 && p.trace) {
-      unsigned long long *rec = p.trace + 4 * (size_t)t;
-      rec[0] = t_claim;
-      rec[1] = t_start;
-    }
-  }
-}
-}  // namespace dev
 
 int exec_smem_bytes() { return dev::SMEM_DOUBLES * 8; }
 

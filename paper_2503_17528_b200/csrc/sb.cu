@@ -419,7 +419,7 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 //     (m < j), written over the dead A_jm; then arrive on the round's barrier.
 // L itself is never assembled: only W = L^{-1} and the pivots are outputs.
 // *s_bad = 2 x the first non-positive pivot index + 1 if that pivot is NaN; 128 if
-// none.  Wd: 8 x 64 per-warp scratch.  Called by all NT threads; needs the
+// none.  Wd: 8 x 64 per-warp scratch; Pscr: 8 x 512 doubles of per-warp scratch.  Called by all NT threads; needs the
 // registers of one thread for the leaf (the kernels that call it run 1 CTA / SM).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -431,11 +431,15 @@ __device__ __forceinline__ void nbar_arrive(int id) { asm volatile("bar.arrive %
 __device__ __forceinline__ void nbar_sync(int id) { asm volatile("bar.sync %0, 256;\n" ::"r"(id) : "memory"); }
 
 // the trailing update of tile (i, k) by panel j (R = 8j): L_ij, L_kj computed in-warp
-// into the transposed scratch (j, i), (j, k), then A_ik -= L_ij L_kj^T.  Up to 4 tiles
-// of one warp in flight together.
-__device__ __forceinline__ void trail_tiles(double *D, int R, const int (&ti)[4], const int (&tk)[4],
+// (through the warp's private scratch Pw: 8 blocks of 8 x 8, stored transposed with
+// row stride 8, conflict-free for both fragment reads), then A_ik -= L_ij L_kj^T; the
+// owner of tile (i, j+1) also writes L_ij^T to the shared scratch block (j, i) (the
+// upper triangle, free) for block row i of W later.  Up to 4 tiles of one warp in
+// flight together.
+__device__ __forceinline__ void trail_tiles(double *D, double *Pw, int R, const int (&ti)[4], const int (&tk)[4],
                                             const bool (&on)[4]) {
   const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
+  const int j1 = R / 8 + 1;
   double li[4][2], lk[4][2];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -451,11 +455,12 @@ __device__ __forceinline__ void trail_tiles(double *D, int R, const int (&ti)[4]
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     if (!on[u]) continue;
-    D[swz(R + 2 * lc, 8 * ti[u] + lr)] = li[u][0];
-    D[swz(R + 2 * lc + 1, 8 * ti[u] + lr)] = li[u][1];
-    if (tk[u] != ti[u]) {
-      D[swz(R + 2 * lc, 8 * tk[u] + lr)] = lk[u][0];
-      D[swz(R + 2 * lc + 1, 8 * tk[u] + lr)] = lk[u][1];
+    double *pi = Pw + 128 * u, *pk = pi + 64;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      pi[(2 * lc + e) * 8 + lr] = li[u][e];
+      pk[(2 * lc + e) * 8 + lr] = lk[u][e];
+      if (tk[u] == j1) D[swz(R + 2 * lc + e, 8 * ti[u] + lr)] = li[u][e];  // shared copy, one writer
     }
   }
   __syncwarp();
@@ -463,16 +468,18 @@ __device__ __forceinline__ void trail_tiles(double *D, int R, const int (&ti)[4]
   for (int u = 0; u < 4; ++u) {
     if (!on[u]) continue;
     const int i = ti[u], k = tk[u];
+    const double *pi = Pw + 128 * u, *pk = (k != i) ? pi + 64 : pi;
     double2 cv = *(const double2 *)(D + swz(8 * i + lr, 8 * k + 2 * lc));
     double acc[2] = {cv.x, cv.y};
 #pragma unroll
-    for (int kk = 0; kk < 8; kk += 4)
-      dmma(acc, -D[swz(R + kk + lc, 8 * i + lr)], D[swz(R + kk + lc, 8 * k + lr)]);
+    for (int kk = 0; kk < 8; kk += 4) dmma(acc, -pi[(kk + lc) * 8 + lr], pk[(kk + lc) * 8 + lr]);
     *(double2 *)(D + swz(8 * i + lr, 8 * k + 2 * lc)) = make_double2(acc[0], acc[1]);
   }
+  __syncwarp();
 }
 
-__device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad, unsigned long long *stamp = nullptr) {
+__device__ void chol_inv64(double *D, double *Wd, double *Pscr, double *ldg, int *s_bad,
+                           unsigned long long *stamp = nullptr) {
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, lr = l >> 2, lc = l & 3;
   if (w == 0) {
     int bad = 128;  // 2 * (first failing pivot) + (pivot is NaN): genuine failures sort first (lane 0)
@@ -538,8 +545,7 @@ __device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad, unsig
       // look-ahead: the next diagonal block gets its panel-j update from this warp
       const int ti[4] = {j + 1, 0, 0, 0}, tk[4] = {j + 1, 0, 0, 0};
       const bool on[4] = {true, false, false, false};
-      trail_tiles(D, R, ti, tk, on);
-      __syncwarp();
+      trail_tiles(D, Pscr, R, ti, tk, on);
       if (stamp && l == 0) stamp[2 * j + 1] = gtimer();
     }
 #pragma unroll
@@ -568,7 +574,7 @@ __device__ void chol_inv64(double *D, double *Wd, double *ldg, int *s_bad, unsig
         ti[u] = j + 1 + ii;
         tk[u] = j + 1 + tt;
       }
-      if (np > 0) trail_tiles(D, R, ti, tk, on);
+      if (np > 0) trail_tiles(D, Pscr + 512 * w, R, ti, tk, on);
 #pragma unroll 1
       for (int u = 0; u < 4; ++u) {
         const int m = wk + 7 * u - np;
@@ -652,12 +658,13 @@ __device__ __forceinline__ double *coupling(const Level &L, const Chain &c, int 
 // ---------------------------------------------------------------------------
 // PPOBTAF (Alg. 3-4; Alg. 1 for the last level) of the partitions of one level.
 // ---------------------------------------------------------------------------
-constexpr int F_SMEM_DOUBLES = 3 * TD + AD + 8 * T + T + 8 + TD + AD;
+constexpr int F_SMEM_DOUBLES = 3 * TD + AD + 8 * T + T + 8 + TD + AD + 8 * 512;
 
 extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm) {
   extern __shared__ __align__(16) double sm[];
   double *D = sm, *X = D + TD, *B = X + TD, *Ar = B + TD, *Wd = Ar + AD, *ldg = Wd + 8 * T;
   double *Dn = ldg + T + 8, *An = Dn + TD;  // the next node's diagonal / arrow blocks (prefetched)
+  double *Pscr = An + AD;                   // Cholesky per-warp scratch
   __shared__ int s_bad;
   const Level &L = prm.L;
   const int b = prm.b, a = prm.a, tid = threadIdx.x, w = tid >> 5;
@@ -696,7 +703,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
       unsigned long long *cst = nullptr;  // chol-internal stamps of the traced partition (level slot 8 + lvl)
       if (prm.trace && blockIdx.x == (gridDim.x > 1 ? 1 : 0) && p == (int)blockIdx.x && k < 64 && prm.lvl < 8)
         cst = prm.trace + (((size_t)(8 + prm.lvl) * 2) * 128 + 2 * k) * 8;
-      chol_inv64(D, Wd, ldg, &s_bad, cst);  // D <- W_k
+      chol_inv64(D, Wd, Pscr, ldg, &s_bad, cst);  // D <- W_k
       SB_STAMP(0, k, 1);
       if (w == 7) {
         const double ls = logsum64(ldg);
@@ -812,7 +819,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
         D[swz(mm, nn2 + 1)] += Uac[0][0][1];
       }
       __syncthreads();
-      chol_inv64(D, Wd, ldg, &s_bad);
+      chol_inv64(D, Wd, Pscr, ldg, &s_bad);
       if (w == 7) {
         const double ls = logsum64(ldg);
         if (tid == NT - 32) lsum += ls;

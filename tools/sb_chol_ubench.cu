@@ -10,13 +10,13 @@ using namespace serinv::sb::dev;
 
 __global__ void k_chol(const double *A, double *out, unsigned long long *st, int reps) {
   extern __shared__ __align__(16) double sm[];
-  double *D = sm, *Wd = D + TD, *ldg = Wd + 8 * T;
+  double *D = sm, *Wd = D + TD, *ldg = Wd + 8 * T, *Ps = ldg + T + 8;
   __shared__ int s_bad;
   for (int r = 0; r < reps; ++r) {
     for (int i = threadIdx.x; i < TD; i += NT) D[swz(i >> 6, i & 63)] = A[i];
     __syncthreads();
     unsigned long long t0 = gtimer();
-    chol_inv64(D, Wd, ldg, &s_bad, r == reps - 1 ? st + 1 : nullptr);
+    chol_inv64(D, Wd, Ps, ldg, &s_bad, r == reps - 1 ? st + 1 : nullptr);
     if (threadIdx.x == 0 && r == reps - 1) st[0] = t0;
   }
   for (int i = threadIdx.x; i < TD; i += NT) out[i] = D[swz(i >> 6, i & 63)];
@@ -32,7 +32,7 @@ int main() {
   cudaMalloc(&dO, 4096 * 8);
   cudaMalloc(&dS, 32 * 8);
   cudaMemcpy(dA, A.data(), 4096 * 8, cudaMemcpyHostToDevice);
-  const int smem = (TD + 8 * T + T + 8) * 8;
+  const int smem = (TD + 8 * T + T + 8 + 8 * 512) * 8;
   cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   k_chol<<<1, NT, smem>>>(dA, dO, dS, 20);
   cudaDeviceSynchronize();
