@@ -378,16 +378,26 @@ struct Builder {
     st.written = true;
   }
 
-  void flush(int Yi, int qi, int Yj, int qj, const BlkRef &tb, TileState &st, size_t keep_last) {
+  // pending updates of a tile -> update tasks of up to update_group columns, except the
+  // last keep_last (fused by the caller).  split_last: the newest opt.split_last flushed
+  // columns are tasks of their own -- for tiles a carried chain task awaits: a grouped
+  // task starts only when its newest column is ready and then runs G x longer, on the
+  // chain (measured at C3: a 4-column update, 26 us, bound every chain step).
+  void flush(int Yi, int qi, int Yj, int qj, const BlkRef &tb, TileState &st, size_t keep_last,
+             bool split_last = false) {
     size_t upto = st.pending.size() - std::min(keep_last, st.pending.size());
     size_t s = 0;
     const int G = cx.opt.update_group;
     const bool whole = P.accum[Yj] != 0;
+    const size_t ns = (size_t)std::max(0, cx.opt.split_last);  // newest columns as single tasks
+    const size_t cut = (split_last && !whole) ? upto - std::min(ns, upto) : upto;
     while (s < upto) {
       std::vector<std::pair<int, int>> g;
       int X0 = st.pending[s].first;
       size_t e = s;
-      while (e < upto && st.pending[e].first == X0 && (whole || (int)g.size() < G)) g.push_back(st.pending[e++]);
+      const size_t lim = s < cut ? cut : upto;
+      const int gmax = s < cut ? G : 1;
+      while (e < lim && st.pending[e].first == X0 && (whole || (int)g.size() < gmax)) g.push_back(st.pending[e++]);
       update_task(Yi, qi, Yj, qj, tb, st, g);
       s = e;
     }
@@ -568,7 +578,7 @@ struct Builder {
           const TileState &sd0 = tstate[tkey(r.Y, r.Y, r.q, r.q)];
           chain_carry = !(bd.zero_init && !sd0.written) && r.h == TILE && w == TILE;
         }
-        flush(r.Y, r.q, X, c, tb, st, chain_carry ? 0 : 1);
+        flush(r.Y, r.q, X, c, tb, st, chain_carry ? 0 : 1, chain_carry && cx.opt.split_last > 0);
         RawTask rt;
         rt.t.type = TK_GEMM;
         rt.t.m = (int16_t)r.h;
@@ -593,7 +603,7 @@ struct Builder {
             // so the next POTRF starts from a fully updated tile.  The update of E runs
             // while POTRF(K) is still busy: W_K and the diagonal tile's earlier updates
             // are awaited late.
-            flush(r.Y, r.q, r.Y, r.q, bd, sd, 0);
+            flush(r.Y, r.q, r.Y, r.q, bd, sd, 0, chain_carry && cx.opt.split_last > 0);
             flush_queue = 0;
             rt.t.flags = TF_SYRK3;
             rt.t.out3 = tileloc(bd.base, r.q, r.q);
@@ -1890,6 +1900,7 @@ void BuildOptions::apply_env() {
       else if (k == "chain_step") chain_step = v != 0;
       else if (k == "dist_len") dist_len = (int)v;
       else if (k == "twist_reduced") twist_reduced = v != 0;
+      else if (k == "split_last") split_last = (int)v;
     }
     i = j + 1;
   }

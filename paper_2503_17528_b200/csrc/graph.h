@@ -113,6 +113,7 @@ struct BuildOptions {
   int twist_max_b = 1024;       // ... and b <= twist_max_b (larger blocks: the one-sided chain hides under the work)
   bool twist_reduced = true;    // reduced systems (>= 4 blocks) solved in the twisted order (two chains)
   int dist_len = 0;             // distributed reduced system: nested partitions of ~dist_len blocks (0: measured default)
+  int split_last = 0;           // carried chain: the newest N updates of the tiles it awaits as single-column tasks (measured: no gain at C3)
   // overrides from the environment (SERINV_OPT="key=value,..."), for tuning runs
   void apply_env();
 };

@@ -45,7 +45,12 @@ def _host(D):
 
 
 def _bench_launch(sb, D, n, b):
-    """The launch bench.py times at N = 1 for (n, b)."""
+    """The launch bench.py times at N = 1 for (n, b) (engine 'auto': the small-block
+    engine where it applies, b <= 64 and a <= 16)."""
+    a = D["tip"].shape[0]
+    if b <= 64 and a <= 16:
+        Ps = sb.sb_auto_plan(n, b, a)
+        return sb.selinv_sb(*args(D), Ps), ["sb"] + Ps
     Ps = sb.auto_partitions(n, b)
     if Ps == [1]:
         return sb.selinv(*args(D)), Ps
