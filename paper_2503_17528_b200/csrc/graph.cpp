@@ -71,12 +71,12 @@ double gemm_flops(int m, int n, const std::vector<Seg> &segs) {
 // Scheduler cost model (ns) for one CTA of a 2-CTA/SM persistent grid.
 // Calibrated on B200 task traces (tools/trace.py): bulk GEMM ~85 GFLOP/s per CTA with
 // two CTAs per SM, POTRF tile task ~21 us, REDUCE ~10 us.
-double task_cost(const RawTask &rt) {
-  const double ns_per_flop = 1.0 / 85.0;
+double task_cost(const RawTask &rt, const BuildOptions &o) {
+  const double ns_per_flop = 1.0 / o.cost_gflops;
   switch (rt.t.type) {
-    case TK_POTRF: return 19000.0 + rt.flops * ns_per_flop * 0.5;
+    case TK_POTRF: return o.cost_potrf + rt.flops * ns_per_flop * 0.5;
     case TK_TRTRI: return 6000.0;
-    case TK_GEMM: return 2500.0 + rt.flops * ns_per_flop;
+    case TK_GEMM: return o.cost_gemm_fixed + rt.flops * ns_per_flop;
     case TK_REDUCE: return 6000.0;
     default: return 2000.0;
   }
@@ -145,7 +145,7 @@ struct Ctx {
                  2.0 * rt.t.m * rt.t.m * rt.t.m / 3.0 + ((rt.t.flags & TF_TRSM2) ? 2.0 * rt.t.m3 * rt.t.m * rt.t.m : 0.0) +
                  ((rt.t.flags & TF_TRSM3) ? 2.0 * rt.t.m4 * rt.t.m * rt.t.m : 0.0);
     if (rt.t.type == TK_TRTRI) rt.flops = rt.t.m * (double)rt.t.m * rt.t.m / 3.0;
-    rt.cost = task_cost(rt);
+    rt.cost = task_cost(rt, opt);
     std::sort(rt.waits.begin(), rt.waits.end());
     rt.waits.erase(std::unique(rt.waits.begin(), rt.waits.end()), rt.waits.end());
     std::sort(rt.late.begin(), rt.late.end());
@@ -1860,6 +1860,13 @@ int64_t sequential_ws_bytes(int kind, int64_t n, int64_t b, int64_t a, const Bui
 Graph build_sequential(int kind, int64_t n, int64_t b, int64_t a, const BuildOptions &opt) {
   Ctx cx;
   cx.opt = opt;
+  // scheduler cost model per block size (measured, profiles/r02/knobs/): the claim order
+  // starts the chain's bulk inputs earlier with a larger GEMM fixed cost at b >= 2048 (C3
+  // 936 -> 927 ms) and a lower bulk rate at b = 1024 (C2 56.9 -> 55.6 ms)
+  if (!opt.cost_set) {
+    if (b >= 2048) cx.opt.cost_gemm_fixed = 7000.0;
+    else if (b >= 1024) cx.opt.cost_gflops = 50.0;
+  }
   Graph g = build_seq_ctx(cx, kind, n, b, a);
   if (g.error.empty() && g.ws_doubles * 8 > sequential_ws_bytes(kind, n, b, a, opt))
     g.error = "workspace accounting mismatch";
@@ -1901,6 +1908,9 @@ void BuildOptions::apply_env() {
       else if (k == "dist_len") dist_len = (int)v;
       else if (k == "twist_reduced") twist_reduced = v != 0;
       else if (k == "split_last") split_last = (int)v;
+      else if (k == "cost_gemm_fixed") cost_gemm_fixed = (double)v, cost_set = true;
+      else if (k == "cost_potrf") cost_potrf = (double)v, cost_set = true;
+      else if (k == "cost_gflops") cost_gflops = (double)v, cost_set = true;
     }
     i = j + 1;
   }

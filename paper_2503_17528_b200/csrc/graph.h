@@ -113,6 +113,10 @@ struct BuildOptions {
   int twist_max_b = 1024;       // ... and b <= twist_max_b (larger blocks: the one-sided chain hides under the work)
   bool twist_reduced = true;    // reduced systems (>= 4 blocks) solved in the twisted order (two chains)
   int dist_len = 0;             // distributed reduced system: nested partitions of ~dist_len blocks (0: measured default)
+  double cost_gemm_fixed = 2500.0;  // scheduler cost model: GEMM task fixed ns
+  double cost_potrf = 19000.0;      // ... POTRF tile task ns
+  double cost_gflops = 85.0;        // ... bulk GEMM GFLOP/s per CTA
+  bool cost_set = false;            // cost model set through SERINV_OPT (else per block size, build_sequential)
   int split_last = 0;           // carried chain: the newest N updates of the tiles it awaits as single-column tasks (measured: no gain at C3)
   // overrides from the environment (SERINV_OPT="key=value,..."), for tuning runs
   void apply_env();

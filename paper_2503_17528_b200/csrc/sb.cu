@@ -1107,17 +1107,19 @@ std::vector<int64_t> plan_tables(const Plan &pl) {
 }
 
 // Level 0: one partition per SM (the chain of ~n/148 blocks is the level's
-// critical path; the factor kernel's 2 CTAs per SM overlap their Cholesky
-// latencies).  Deeper levels: short partitions (~6 blocks) until the reduced
-// system has <= 12 blocks, which the last level solves as one chain.
+// critical path).  Deeper levels: short partitions (~6 blocks) until the reduced
+// system has <= 12 blocks, then its two ends (P = 2), then the last level solves the
+// remaining <= 4 blocks as one chain.
 std::vector<int> auto_plan(int64_t n, int64_t b, int sms) {
   (void)b;
   std::vector<int> Ps;
   int64_t m = n;
-  const int64_t seq_max = 12;
+  const int64_t seq_max = 4;
   bool first = true;
   while (m > seq_max) {
-    int64_t P = first ? std::min<int64_t>(sms, m / 8) : m / 6;
+    // level 0: one partition per SM; then ~6-block partitions; a short last system
+    // (<= 12 blocks) is split once more into its two fill-in-free ends (measured ~1 %)
+    int64_t P = first ? std::min<int64_t>(sms, m / 8) : (m <= 12 ? 2 : m / 6);
     if (P < 2) break;
     std::vector<int64_t> st;
     while (P >= 2 && !plan_partitions_ends(m, (int)P, 1.0, st)) --P;
