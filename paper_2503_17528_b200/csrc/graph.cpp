@@ -1863,9 +1863,11 @@ Graph build_sequential(int kind, int64_t n, int64_t b, int64_t a, const BuildOpt
   // scheduler cost model per block size (measured, profiles/r02/knobs/): the claim order
   // starts the chain's bulk inputs earlier with a larger GEMM fixed cost at b >= 2048 (C3
   // 936 -> 927 ms) and a lower bulk rate at b = 1024 (C2 56.9 -> 55.6 ms)
+  // (not for the streaming-IO graph at b = 1024: its modelled arrivals favour the default;
+  // C2 e2e 91.5 vs 115 ms)
   if (!opt.cost_set) {
     if (b >= 2048) cx.opt.cost_gemm_fixed = 7000.0;
-    else if (b >= 1024) cx.opt.cost_gflops = 50.0;
+    else if (b >= 1024 && kind != 6) cx.opt.cost_gflops = 50.0;
   }
   Graph g = build_seq_ctx(cx, kind, n, b, a);
   if (g.error.empty() && g.ws_doubles * 8 > sequential_ws_bytes(kind, n, b, a, opt))
