@@ -171,19 +171,27 @@ __device__ __forceinline__ Frags<2, 4> lay64(int w) {
   F.cf[3] = h ? 5 : 7;
   return F;
 }
-// 16 x 64 outputs (arrow rows): row fragment w & 1, column fragments {w/2, 7 - w/2}
-__device__ __forceinline__ Frags<1, 2> layAR(int w) {
-  Frags<1, 2> F;
-  F.rf[0] = w & 1;
-  F.cf[0] = w >> 1;
-  F.cf[1] = 7 - (w >> 1);
+// ARR x 64 outputs (arrow rows, ARR = 8 or 16): ARR = 16: row fragment w & 1, column
+// fragments {w/2, 7 - w/2}; ARR = 8: the one row fragment, column fragment w
+template <int ARR>
+__device__ __forceinline__ Frags<1, ARR / 8> layA(int w) {
+  Frags<1, ARR / 8> F;
+  if (ARR == 16) {
+    F.rf[0] = w & 1;
+    F.cf[0] = w >> 1;
+    F.cf[ARR / 8 - 1] = 7 - (w >> 1);
+  } else {
+    F.rf[0] = 0;
+    F.cf[0] = w;
+  }
   return F;
 }
-// 16 x 16 outputs (tip-sized), warps 0..3
+// ARR x ARR outputs (tip-sized): warps 0 .. (ARR/8)^2 - 1
+template <int ARR>
 __device__ __forceinline__ Frags<1, 1> layU(int w) {
   Frags<1, 1> F;
-  F.rf[0] = (w >> 1) & 1;
-  F.cf[0] = w & 1;
+  F.rf[0] = ARR == 16 ? (w >> 1) & 1 : 0;
+  F.cf[0] = ARR == 16 ? w & 1 : 0;
   return F;
 }
 
@@ -258,7 +266,7 @@ __device__ __forceinline__ void mma(double (&acc)[MI][NI][2], const double *A, c
     klo = min(klo, BM == B_GE ? 8 * F.cf[j] : 0);
     khi = max(khi, BM == B_LE ? min(K, 8 * F.cf[j] + 8) : K);
   }
-  if (BM == K_FULL && (K == T || K == AR)) {  // full products: fully unrolled k loop
+  if (BM == K_FULL && K == T) {  // full products: fully unrolled k loop
     if (K == T) {
 #pragma unroll
       for (int k = 0; k < T; k += 4) {
@@ -658,9 +666,12 @@ __device__ __forceinline__ double *coupling(const Level &L, const Chain &c, int 
 // ---------------------------------------------------------------------------
 // PPOBTAF (Alg. 3-4; Alg. 1 for the last level) of the partitions of one level.
 // ---------------------------------------------------------------------------
-constexpr int F_SMEM_DOUBLES = 3 * TD + AD + 8 * T + T + 8 + TD + AD + 8 * 512;
+template <int ARR>
+constexpr int f_smem_doubles() { return 3 * TD + ARR * T + 8 * T + T + 8 + TD + ARR * T + 8 * 512; }
 
-extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm) {
+template <int ARR>
+__global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm) {
+  constexpr int AR = ARR, AD = ARR * T, NA = ARR / 8, NU = NA * NA;
   extern __shared__ __align__(16) double sm[];
   double *D = sm, *X = D + TD, *B = X + TD, *Ar = B + TD, *Wd = Ar + AD, *ldg = Wd + 8 * T;
   double *Dn = ldg + T + 8, *An = Dn + TD;  // the next node's diagonal / arrow blocks (prefetched)
@@ -670,8 +681,8 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
   const int b = prm.b, a = prm.a, tid = threadIdx.x, w = tid >> 5;
   const int64_t bb = (int64_t)b * b, ab = (int64_t)a * b;
   const Frags<2, 4> F = lay64(w);
-  const Frags<1, 2> FA = layAR(w);
-  const Frags<1, 1> FU = layU(w);
+  const Frags<1, NA> FA = layA<ARR>(w);
+  const Frags<1, 1> FU = layU<ARR>(w);
 
   for (int p = blockIdx.x; p < L.P; p += gridDim.x) {
     const Chain c = chain_of(L, p);
@@ -684,7 +695,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
     if (mid) ld_tile(B, L.Lo + c.s * bb, T, b, b, b, true, false);
     cp_wait_all();
     __syncthreads();
-    double Aff[2][4][2], Anf[1][2][2], Uac[1][1][2];
+    double Aff[2][4][2], Anf[1][NA][2], Uac[1][1][2];
     acc_zero(Aff);
     acc_zero(Anf);
     acc_zero(Uac);
@@ -735,9 +746,9 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
         acc_st_global(L.Bf + bk * bb, acc, b, b, b, F, false, 1.0);
       }
       if (a > 0) {  // L_{n,k} = A_{n,k} W^T
-        double acc[1][2][2];
+        double acc[1][NA][2];
         acc_zero(acc);
-        mma<1, 2, false, true, false, B_LE>(acc, Ar, D, FA, T);
+        mma<1, NA, false, true, false, B_LE>(acc, Ar, D, FA, T);
         __syncthreads();
         acc_st_smem(Ar, acc, FA, 1.0);
         acc_st_global(L.Ar + bk * ab, acc, b, a, b, FA, false, 1.0);
@@ -752,14 +763,14 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
         acc_st_smem(D, acc, F, 1.0);
       }
       if (a > 0) {
-        if (w < 4) mma<1, 1, false, true, true>(Uac, Ar, Ar, FU, T);  // U -= Ln Ln^T
-        if (mid) mma<1, 2, false, true, true>(Anf, Ar, B, FA, T);       // A_nf -= Ln B^T
+        if (w < NU) mma<1, 1, false, true, true>(Uac, Ar, Ar, FU, T);  // U -= Ln Ln^T
+        if (mid) mma<1, NA, false, true, true>(Anf, Ar, B, FA, T);       // A_nf -= Ln B^T
       }
       if (mid) mma64<false, true, true>(Aff, B, B, F);  // A_ff -= B B^T
-      double accA[1][2][2];
+      double accA[1][NA][2];
       if (a > 0 && nxt) {  // A_{n,k+1} - L_{n,k} L_{k+1,k}^T
         acc_ld_smem(accA, An, FA);
-        mma<1, 2, false, true, true>(accA, Ar, X, FA, T);
+        mma<1, NA, false, true, true>(accA, Ar, X, FA, T);
       }
       double accB[2][4][2];
       if (mid && nxt) {  // B_{k+1} = -B_k L_{k+1,k}^T
@@ -796,10 +807,10 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
           }
         acc_st_global(L.Dn + (2 * p - 1) * bb, acc, b, b, b, F, false, 1.0);
         if (a > 0) {
-          double acn[1][2][2];
+          double acn[1][NA][2];
           acc_ld(acn, L.Ar + c.s * ab, b, a, b, FA, false);
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
+          for (int j = 0; j < NA; ++j) {
             acn[0][j][0] += Anf[0][j][0];
             acn[0][j][1] += Anf[0][j][1];
           }
@@ -807,13 +818,13 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
         }
         st_tile(L.Lon + (int64_t)(2 * p - 1) * bb, B, b, b, b, true);
       }
-      if (a > 0 && w < 4) acc_st_global(L.U + p * aa, Uac, a, a, a, FU, false, 1.0);
+      if (a > 0 && w < NU) acc_st_global(L.U + p * aa, Uac, a, a, a, FU, false, 1.0);
     } else if (a > 0) {
       // ---- tip (Alg. 1 l.12): L_nn = chol(A_nn + sum of every level's U), X_nn = W^T W (Alg. 2 l.1)
       __syncthreads();
       ld_tile(D, prm.tip, T, a, a, a, false, true);
       __syncthreads();
-      if (w < 4) {
+      if (w < NU) {
         const int l = tid & 31, mm = 8 * FU.rf[0] + (l >> 2), nn2 = 8 * FU.cf[0] + 2 * (l & 3);
         D[swz(mm, nn2)] += Uac[0][0][0];
         D[swz(mm, nn2 + 1)] += Uac[0][0][1];
@@ -826,7 +837,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
       }
       if (tid == 0 && s_bad < 2 * a)
         record_info((s_bad & 1) ? prm.info2 : prm.info, (int)(prm.tip_row + (s_bad >> 1) + 1));
-      if (w < 4) {
+      if (w < NU) {
         double acc[1][1][2];
         acc_zero(acc);
         mma<1, 1, true, false, false>(acc, D, D, FU, T);
@@ -873,9 +884,12 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm)
 //   X_kk      = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~
 // (reading R11: l.7's L_{0,i} is the factor fill-in block; Q_k = X_{f,k}).
 // ---------------------------------------------------------------------------
-constexpr int I_SMEM_DOUBLES = 6 * TD + 4 * AD;
+template <int ARR>
+constexpr int i_smem_doubles() { return 6 * TD + 4 * ARR * T; }
 
-extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm) {
+template <int ARR>
+__global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm) {
+  constexpr int AR = ARR, AD = ARR * T, NA = ARR / 8;
   extern __shared__ __align__(16) double sm[];
   double *W = sm, *Lc = W + TD, *Lf = Lc + TD, *Xd = Lf + TD, *Q = Xd + TD, *Xff = Q + TD;
   double *Ln = Xff + TD, *Xn = Ln + AD, *Xnf = Xn + AD, *Xnn = Xnf + AD;
@@ -883,7 +897,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
   const int b = prm.b, a = prm.a, tid = threadIdx.x, w = tid >> 5;
   const int64_t bb = (int64_t)b * b, ab = (int64_t)a * b;
   const Frags<2, 4> F = lay64(w);
-  const Frags<1, 2> FA = layAR(w);
+  const Frags<1, NA> FA = layA<ARR>(w);
 
   for (int p = blockIdx.x; p < L.P; p += gridDim.x) {
     const Chain c = chain_of(L, p);
@@ -930,7 +944,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
       SB_STAMP(1, k, 1);
       // ---- Lc~, Lf~, Ln~ (W lower)
       {
-        double aL[2][4][2], aF[2][4][2], aN[1][2][2];
+        double aL[2][4][2], aF[2][4][2], aN[1][NA][2];
         if (nxt) {
           acc_zero(aL);
           mma64<false, false, false, B_GE>(aL, Lc, W, F);
@@ -941,7 +955,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
         }
         if (a > 0) {
           acc_zero(aN);
-          mma<1, 2, false, false, false, B_GE>(aN, Ln, W, FA, T);
+          mma<1, NA, false, false, false, B_GE>(aN, Ln, W, FA, T);
         }
         __syncthreads();
         if (nxt) acc_st_smem(Lc, aL, F, 1.0);
@@ -952,7 +966,7 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
       SB_STAMP(1, k, 2);
       // ---- X_{k+1,k}, Q_k, X_{n,k}  (W is dead: its buffer receives X_{k+1,k})
       {
-        double aA[2][4][2], aB[2][4][2], aN[1][2][2];
+        double aA[2][4][2], aB[2][4][2], aN[1][NA][2];
         if (nxt) {
           acc_zero(aA);
           mma64<false, false, false>(aA, Xd, Lc, F);
@@ -967,9 +981,9 @@ extern "C" __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm
         }
         if (a > 0) {
           acc_zero(aN);
-          if (nxt) mma<1, 2, false, false, false>(aN, Xn, Lc, FA, T);
-          mma<1, 2, false, false, false>(aN, Xnn, Ln, FA, AR);
-          if (mid) mma<1, 2, false, false, false>(aN, Xnf, Lf, FA, T);
+          if (nxt) mma<1, NA, false, false, false>(aN, Xn, Lc, FA, T);
+          mma<1, NA, false, false, false>(aN, Xnn, Ln, FA, AR);
+          if (mid) mma<1, NA, false, false, false>(aN, Xnf, Lf, FA, T);
         }
         __syncthreads();
         if (nxt) {
@@ -1136,13 +1150,18 @@ int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, doubl
         int *d_info, double *d_logdet, int sms, cudaStream_t st, int *launches, unsigned long long *trace) {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(dev::sb_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             dev::F_SMEM_DOUBLES * 8) != cudaSuccess ||
-        cudaFuncSetAttribute(dev::sb_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             dev::I_SMEM_DOUBLES * 8) != cudaSuccess)
+    if (cudaFuncSetAttribute(dev::sb_factor_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dev::f_smem_doubles<8>() * 8) != cudaSuccess ||
+        cudaFuncSetAttribute(dev::sb_factor_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dev::f_smem_doubles<16>() * 8) != cudaSuccess ||
+        cudaFuncSetAttribute(dev::sb_inverse_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dev::i_smem_doubles<8>() * 8) != cudaSuccess ||
+        cudaFuncSetAttribute(dev::sb_inverse_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dev::i_smem_doubles<16>() * 8) != cudaSuccess)
       return 1;
     attr = true;
   }
+  const bool a8 = pl.a <= 8;  // arrow tiles of 8 rows (a <= 8) or 16
   const int nl = (int)pl.Ps.size();
   const int L = nl + 1;
   if (cudaMemsetAsync(ws + pl.off_ctr, 0, (size_t)(L + 1) * sizeof(int), st) != cudaSuccess ||
@@ -1194,12 +1213,18 @@ int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, doubl
   int nlaunch = 0;
   for (int l = 0; l < L; ++l) {
     const int grid = std::max(1, std::min(prm[l].L.P, sms));
-    dev::sb_factor_kernel<<<grid, dev::NT, dev::F_SMEM_DOUBLES * 8, st>>>(prm[l]);
+    if (a8)
+      dev::sb_factor_kernel<8><<<grid, dev::NT, dev::f_smem_doubles<8>() * 8, st>>>(prm[l]);
+    else
+      dev::sb_factor_kernel<16><<<grid, dev::NT, dev::f_smem_doubles<16>() * 8, st>>>(prm[l]);
     ++nlaunch;
   }
   for (int l = L - 1; l >= 0; --l) {
     const int grid = std::max(1, std::min(prm[l].L.P, sms));
-    dev::sb_inverse_kernel<<<grid, dev::NT, dev::I_SMEM_DOUBLES * 8, st>>>(prm[l]);
+    if (a8)
+      dev::sb_inverse_kernel<8><<<grid, dev::NT, dev::i_smem_doubles<8>() * 8, st>>>(prm[l]);
+    else
+      dev::sb_inverse_kernel<16><<<grid, dev::NT, dev::i_smem_doubles<16>() * 8, st>>>(prm[l]);
     ++nlaunch;
   }
   if (launches) *launches += nlaunch;

@@ -79,7 +79,7 @@ __global__ void k_gemm(double *out, unsigned long long *st, int reps, int mode) 
     else if (mode == 5) mma64<true, false, false, K_FULL, false, AR>(acc, A, B, F);
     else if (mode == 6) {
       double a2[1][2][2] = {};
-      mma<1, 2, false, false, false>(a2, A, B, layAR(threadIdx.x >> 5), T);
+      mma<1, 2, false, false, false>(a2, A, B, layA<16>(threadIdx.x >> 5), T);
       acc[0][0][0] += a2[0][0][0] + a2[0][1][1];
     } else mma64<true, false, false, B_GE, true>(acc, A, B, F);
   }
