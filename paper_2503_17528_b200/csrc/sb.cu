@@ -41,10 +41,10 @@ namespace dev {
 
 constexpr int T = 64;
 constexpr int NT = 256;
-constexpr int AR = kMaxA;  // arrow tile rows
+
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int TD = T * T;        // doubles per 64 x 64 tile
-constexpr int AD = AR * T;       // doubles per arrow tile (16 x 64)
+
 
 enum PartType { P_TOP = 0, P_MID = 1, P_BOT = 2, P_SEQ = 3 };
 
