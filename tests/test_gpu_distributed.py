@@ -272,6 +272,8 @@ print("SANITIZE_OK")
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_compute_sanitizer(tool, tmp_path):
     cs = "/usr/local/cuda/bin/compute-sanitizer"
+    if os.environ.get("SERINV_SANITIZER") != "1":
+        pytest.skip("opt-in (SERINV_SANITIZER=1): the GPU pool blocks compute-sanitizer runs")
     if not os.path.exists(cs):
         pytest.skip("compute-sanitizer not installed")
     script = tmp_path / "san.py"
