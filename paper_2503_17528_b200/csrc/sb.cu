@@ -922,18 +922,34 @@ __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm) {
     }
     cp_wait_all();
     __syncthreads();
+    // step operands: group 1 = W_k and L_{k+1,k}, group 2 = L_{f,k} and L_{n,k}.  The
+    // first step's are loaded here; every later step's are prefetched by the step
+    // before, into buffers as soon as its X_kk products are done with them.
+    auto load_wc = [&](int k) {
+      ld_tile(W, L.D + c.blk(k) * bb, T, b, b, b, false, true);
+      if (k + 1 < c.nn) {
+        bool t2 = false;
+        const double *g = coupling(L, c, k, bb, &t2);
+        ld_tile(Lc, g, T, b, b, b, t2, false);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    auto load_fn = [&](int k) {
+      if (mid) ld_tile(Lf, L.Bf + c.blk(k) * bb, T, b, b, b, false, false);
+      if (a > 0) ld_tile(Ln, L.Ar + c.blk(k) * ab, AR, a, b, b, false, false);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    if (c.nel > 0) {
+      load_wc(c.nel - 1);
+      load_fn(c.nel - 1);
+    }
     for (int k = c.nel - 1; k >= 0; --k) {
       const int64_t bk = c.blk(k);
       const bool nxt = k + 1 < c.nn;
       bool tr = false;
       double *cpl = nxt ? coupling(L, c, k, bb, &tr) : nullptr;
       SB_STAMP(1, k, 0);
-      ld_tile(W, L.D + bk * bb, T, b, b, b, false, true);
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-      if (nxt) ld_tile(Lc, cpl, T, b, b, b, tr, false);
-      if (mid) ld_tile(Lf, L.Bf + bk * bb, T, b, b, b, false, false);
-      if (a > 0) ld_tile(Ln, L.Ar + bk * ab, AR, a, b, b, false, false);
-      asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
       __syncthreads();
       // ---- Lam = W^T W (lower half) while the other operands arrive
       double aX[2][4][2];
@@ -998,12 +1014,17 @@ __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm) {
       }
       __syncthreads();
       SB_STAMP(1, k, 3);
-      // ---- X_kk = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~
+      // ---- X_kk = Lam - X_{k+1,k}^T Lc~ - X_{n,k}^T Ln~ - Q_k^T Lf~; the next step's
+      // W, L_{k,k-1} go into the W / Lc buffers once the first product has read them,
+      // its L_{f,k-1}, L_{n,k-1} into Lf / Ln after the last
       if (nxt) mma64<true, false, true>(aX, W, Lc, F);
+      __syncthreads();
+      if (k > 0) load_wc(k - 1);
       if (a > 0) mma64<true, false, true, K_FULL, false, AR>(aX, Xn, Ln, F);
       if (mid) mma64<true, false, true>(aX, Q, Lf, F);
       acc_st_smem(Xd, aX, F, 1.0);
       __syncthreads();
+      if (k > 0) load_fn(k - 1);
       st_tile(L.D + bk * bb, Xd, b, b, b, false);  // coalesced
       SB_STAMP(1, k, 4);
     }
