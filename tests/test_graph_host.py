@@ -338,3 +338,19 @@ def test_distributed_info_is_global_and_agreed(P, Q, where):
     assert rc == 0, rc
     assert info.value == expect, (info.value, expect)
     assert np.isnan(ldv.value)
+
+
+@pytest.mark.parametrize("opt", ["carry_min_b=64", "carry_min_b=64,split_last=1",
+                                 "carry_min_b=64,rts1_chain=1,split_last=2,update_group=3",
+                                 "carry_min_b=64,twist_min_n=3,twist_max_b=4096"])
+def test_carried_chain_options(opt, monkeypatch):
+    # carried chain (C3's b >= 2048 default) at small b, with its scheduling options
+    # and in the twisted order: same results, valid emission order
+    monkeypatch.setenv("SERINV_OPT", opt if "twist" in opt else opt + ",twist_min_n=0")
+    for n, b, a in ((5, 200, 3), (5, 192, 3), (4, 128, 0)):
+        A0 = btagen.g1(5, n, b, a)
+        L, X, ld = seq.selinv(A0)
+        R, ldr, info = run_seq(2, A0)
+        assert info == 0
+        assert inv.max_block_err(cut(R, X), X)[0] < 1e-12
+        assert abs(ldr - ld) <= 1e-12 * max(1, abs(ld))
