@@ -29,6 +29,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <vector>
 
@@ -88,6 +90,17 @@ __device__ void ld_tile(double *s, const double *g, int rows_t, int rows, int co
     for (int i = tid; i < TD / 2; i += NT) {
       const int r = i >> 5, c = (i & 31) * 2;
       cp_async16(s + swz(r, c), g + r * T + c);
+    }
+    return;
+  }
+  if (!trans && cols == T && ld == T && rows <= rows_t && !(pad && rows < rows_t) && !((uintptr_t)g & 15)) {
+    // full 64-double rows (e.g. the arrow rows at b = 64): cp.async too, zero pad rows
+    for (int i = tid; i < rows_t * (T / 2); i += NT) {
+      const int r = i >> 5, c = (i & 31) * 2;
+      if (r < rows)
+        cp_async16(s + swz(r, c), g + r * T + c);
+      else
+        *(double2 *)(s + swz(r, c)) = make_double2(0.0, 0.0);
     }
     return;
   }
@@ -384,6 +397,10 @@ __device__ __forceinline__ void acc_st_global(double *g, const double (&acc)[MI]
     for (int j = 0; j < NI; ++j) {
       if (LOW && F.rf[i] < F.cf[j]) continue;
       const int m = 8 * F.rf[i] + lr, n = 8 * F.cf[j] + 2 * lc;
+      if (!trans && !MIR && m < rows && n + 1 < cols && !(ld & 1) && !((uintptr_t)g & 15)) {  // 16-byte store
+        *(double2 *)(g + (int64_t)m * ld + n) = make_double2(sgn * acc[i][j][0], sgn * acc[i][j][1]);
+        continue;
+      }
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = n + e;
@@ -887,7 +904,114 @@ __global__ void __launch_bounds__(NT, 1) sb_factor_kernel(Params prm) {
 template <int ARR>
 constexpr int i_smem_doubles() { return 6 * TD + 4 * ARR * T; }
 
+// ---------------------------------------------------------------------------
+// W-form precompute of one level (level 0), run on the SMs the nested levels leave
+// idle (a second stream, between the level's factor and inverse kernels): for every
+// eliminated node k, in place,
+//   W_k -> Lam_k = W_k^T W_k (diag slot),  L_{k+1,k} -> Lc~ = L_{k+1,k} W_k (coupling slot),
+//   L_{f,k} -> Lf~ = L_{f,k} W_k (Bf),     L_{n,k} -> Ln~ = L_{n,k} W_k (arrow slot)
+// -- the inverse's first products, which need only the factor.  Nothing else
+// reads these slots before the level's inverse kernel (the nested levels work on their
+// own arrays; the inter-partition couplings are not eliminated nodes).  2 CTAs / SM.
+// ---------------------------------------------------------------------------
 template <int ARR>
+constexpr int p_smem_doubles() { return 2 * (3 * TD + ARR * T); }
+
+// one CTA per SM (its two operand sets fill the SM's shared memory), so the nested
+// levels' kernels keep the SMs the caller leaves free.  Items (partition p, node k) are
+// claimed one by one from a shared counter (*claim), item it = (p = it % P, k = it / P),
+// so several launches of this kernel (started as the nested levels free SMs) share the
+// work; the claim of item j + 2 is in flight while item j is computed and item j + 1's
+// operands arrive.
+template <int ARR>
+__global__ void __launch_bounds__(NT, 1) sb_pre_kernel(Params prm, int kmax, int *claim) {
+  constexpr int AR = ARR, NA = ARR / 8, SET = 3 * TD + ARR * T;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_next;
+  const Level &L = prm.L;
+  const int b = prm.b, a = prm.a, w = threadIdx.x >> 5;
+  const int64_t bb = (int64_t)b * b, ab = (int64_t)a * b;
+  const Frags<2, 4> F = lay64(w);
+  const Frags<1, NA> FA = layA<ARR>(w);
+  const int nit = L.P * kmax;
+  auto node = [&](int it, Chain &c, int &k) {
+    c = chain_of(L, it % L.P);
+    k = it / L.P;
+    return k < c.nel;
+  };
+  // operands of item it into set s: W_k, L_{k+1,k}, L_{f,k}, L_{n,k}
+  auto load = [&](int it, int s) {
+    Chain c;
+    int k;
+    if (node(it, c, k)) {
+      const int64_t bk = c.blk(k);
+      double *W = sm + s * SET, *Y = W + TD, *Z = Y + TD, *N = Z + TD;
+      ld_tile(W, L.D + bk * bb, T, b, b, b, false, true);
+      if (k + 1 < c.nn) {
+        bool tr = false;
+        const double *g = coupling(L, c, k, bb, &tr);
+        ld_tile(Y, g, T, b, b, b, tr, false);
+      }
+      if (c.type == P_MID) ld_tile(Z, L.Bf + bk * bb, T, b, b, b, false, false);
+      if (a > 0) ld_tile(N, L.Ar + bk * ab, AR, a, b, b, false, false);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if (threadIdx.x == 0) s_next = atomicAdd(claim, 1);
+  __syncthreads();
+  int cur = s_next;
+  __syncthreads();
+  if (threadIdx.x == 0) s_next = atomicAdd(claim, 1);
+  __syncthreads();
+  int nx = s_next;
+  if (cur < nit) load(cur, 0);
+  for (int j = 0; cur < nit; ++j) {
+    if (nx < nit) {
+      load(nx, (j + 1) & 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    int nn = 0;
+    if (threadIdx.x == 0 && nx < nit) nn = atomicAdd(claim, 1);  // consumed after this item's products
+    __syncthreads();
+    Chain c;
+    int k;
+    if (node(cur, c, k)) {
+      const int64_t bk = c.blk(k);
+      double *W = sm + (j & 1) * SET, *Y = W + TD, *Z = Y + TD, *N = Z + TD;
+      double aX[2][4][2];
+      acc_zero(aX);
+      mma64<true, false, false, B_GE>(aX, W, W, F);  // Lam = W^T W
+      acc_st_global(L.D + bk * bb, aX, b, b, b, F, false, 1.0);
+      if (k + 1 < c.nn) {  // Lc~ = L_{k+1,k} W
+        bool tr = false;
+        double *cpl = coupling(L, c, k, bb, &tr);
+        acc_zero(aX);
+        mma64<false, false, false, B_GE>(aX, Y, W, F);
+        acc_st_global(cpl, aX, b, b, b, F, tr, 1.0);
+      }
+      if (c.type == P_MID) {  // Lf~ = L_{f,k} W
+        acc_zero(aX);
+        mma64<false, false, false, B_GE>(aX, Z, W, F);
+        acc_st_global(L.Bf + bk * bb, aX, b, b, b, F, false, 1.0);
+      }
+      if (a > 0) {  // Ln~ = L_{n,k} W
+        double aN[1][NA][2];
+        acc_zero(aN);
+        mma<1, NA, false, false, false, B_GE>(aN, N, W, FA, T);
+        acc_st_global(L.Ar + bk * ab, aN, b, a, b, FA, false, 1.0);
+      }
+    }
+    if (threadIdx.x == 0) s_next = nx < nit ? nn : nit;
+    __syncthreads();  // set j & 1 is reloaded by the next iteration's prefetch; s_next published
+    cur = nx;
+    nx = s_next;
+  }
+}
+
+// PRE: the level's Lam, Lc~, Lf~, Ln~ were precomputed in place (sb_pre_kernel)
+template <int ARR, bool PRE>
 __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm) {
   constexpr int AR = ARR, AD = ARR * T, NA = ARR / 8;
   extern __shared__ __align__(16) double sm[];
@@ -953,13 +1077,17 @@ __global__ void __launch_bounds__(NT, 1) sb_inverse_kernel(Params prm) {
       __syncthreads();
       // ---- Lam = W^T W (lower half) while the other operands arrive
       double aX[2][4][2];
-      acc_zero(aX);
-      mma64<true, false, false, B_GE>(aX, W, W, F);
+      if (PRE) {
+        acc_ld_smem(aX, W, F);  // Lam (precomputed)
+      } else {
+        acc_zero(aX);
+        mma64<true, false, false, B_GE>(aX, W, W, F);
+      }
       cp_wait_all();
       __syncthreads();
       SB_STAMP(1, k, 1);
       // ---- Lc~, Lf~, Ln~ (W lower)
-      {
+      if (!PRE) {
         double aL[2][4][2], aF[2][4][2], aN[1][NA][2];
         if (nxt) {
           acc_zero(aL);
@@ -1167,17 +1295,54 @@ std::vector<int> auto_plan(int64_t n, int64_t b, int sms) {
   return Ps;
 }
 
+namespace {
+// per device: the side stream of the level-0 precompute and its fork / join events
+struct Side {
+  cudaStream_t s = nullptr, s2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, fork2 = nullptr, join2 = nullptr;
+};
+std::mutex side_mu;
+Side *side_for_device() {
+  static std::map<int, Side> sides;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(side_mu);
+  Side &sd = sides[dev];
+  if (!sd.s) {
+    if (cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&sd.s2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sd.fork2, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sd.join2, cudaEventDisableTiming) != cudaSuccess) {
+      sd.s = nullptr;
+      return nullptr;
+    }
+  }
+  return &sd;
+}
+}  // namespace
+
 int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, double *arrow, double *tip, double *ws,
         int *d_info, double *d_logdet, int sms, cudaStream_t st, int *launches, unsigned long long *trace) {
   static bool attr = false;
   if (!attr) {
+    if (cudaFuncSetAttribute(dev::sb_pre_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dev::p_smem_doubles<8>() * 8) != cudaSuccess ||
+        cudaFuncSetAttribute(dev::sb_pre_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dev::p_smem_doubles<16>() * 8) != cudaSuccess ||
+        cudaFuncSetAttribute(dev::sb_inverse_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dev::i_smem_doubles<8>() * 8) != cudaSuccess ||
+        cudaFuncSetAttribute(dev::sb_inverse_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dev::i_smem_doubles<16>() * 8) != cudaSuccess)
+      return 1;
     if (cudaFuncSetAttribute(dev::sb_factor_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              dev::f_smem_doubles<8>() * 8) != cudaSuccess ||
         cudaFuncSetAttribute(dev::sb_factor_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              dev::f_smem_doubles<16>() * 8) != cudaSuccess ||
-        cudaFuncSetAttribute(dev::sb_inverse_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dev::sb_inverse_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              dev::i_smem_doubles<8>() * 8) != cudaSuccess ||
-        cudaFuncSetAttribute(dev::sb_inverse_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dev::sb_inverse_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              dev::i_smem_doubles<16>() * 8) != cudaSuccess)
       return 1;
     attr = true;
@@ -1185,7 +1350,8 @@ int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, doubl
   const bool a8 = pl.a <= 8;  // arrow tiles of 8 rows (a <= 8) or 16
   const int nl = (int)pl.Ps.size();
   const int L = nl + 1;
-  if (cudaMemsetAsync(ws + pl.off_ctr, 0, (size_t)(L + 1) * sizeof(int), st) != cudaSuccess ||
+  // exit counters per level, info2, the precompute's claim counter (off_ctr holds L + 1 doubles)
+  if (cudaMemsetAsync(ws + pl.off_ctr, 0, (size_t)(L + 2) * sizeof(int), st) != cudaSuccess ||
       cudaMemsetAsync(d_info, 0, sizeof(int), st) != cudaSuccess)
     return 1;
   const int64_t b = pl.b, a = pl.a;
@@ -1232,6 +1398,18 @@ int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, doubl
     q.tip_row = pl.n * b;
   }
   int nlaunch = 0;
+  // level-0 W-form precompute on the SMs the nested levels leave idle (side stream,
+  // forked after the level-0 factor kernel, joined before the level-0 inverse kernel)
+  int maxp = 1, maxp2 = 1;
+  for (int l = 1; l < L; ++l) maxp = std::max(maxp, prm[l].L.P);
+  for (int l = 2; l < L; ++l) maxp2 = std::max(maxp2, prm[l].L.P);
+  Side *sd = nl >= 1 ? side_for_device() : nullptr;
+  const bool pre = sd != nullptr && sms - maxp >= 16;
+  bool pre2 = false;
+  int *claim = (int *)(ws + pl.off_ctr) + L + 1;
+  int kmax = 0;
+  if (pre)
+    for (int p = 0; p < pl.Ps[0]; ++p) kmax = (int)std::max<int64_t>(kmax, pl.starts[0][p + 1] - pl.starts[0][p]);
   for (int l = 0; l < L; ++l) {
     const int grid = std::max(1, std::min(prm[l].L.P, sms));
     if (a8)
@@ -1239,13 +1417,48 @@ int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, doubl
     else
       dev::sb_factor_kernel<16><<<grid, dev::NT, dev::f_smem_doubles<16>() * 8, st>>>(prm[l]);
     ++nlaunch;
+    if (l == 0 && pre) {
+      // first share of the SMs the nested levels leave free: all but level 1's
+      const int pgrid = sms - prm[1].L.P;
+      if (cudaEventRecord(sd->fork, st) != cudaSuccess || cudaStreamWaitEvent(sd->s, sd->fork, 0) != cudaSuccess)
+        return 1;
+      if (a8)
+        dev::sb_pre_kernel<8><<<pgrid, dev::NT, dev::p_smem_doubles<8>() * 8, sd->s>>>(prm[0], kmax, claim);
+      else
+        dev::sb_pre_kernel<16><<<pgrid, dev::NT, dev::p_smem_doubles<16>() * 8, sd->s>>>(prm[0], kmax, claim);
+      ++nlaunch;
+      if (cudaEventRecord(sd->join, sd->s) != cudaSuccess) return 1;
+    }
+    if (l == 1 && pre && L > 2 && prm[1].L.P - maxp2 >= 8) {
+      // level 1 done: its SMs (less the deeper levels' widest) join the precompute
+      const int pgrid = prm[1].L.P - maxp2;
+      if (cudaEventRecord(sd->fork2, st) != cudaSuccess || cudaStreamWaitEvent(sd->s2, sd->fork2, 0) != cudaSuccess)
+        return 1;
+      if (a8)
+        dev::sb_pre_kernel<8><<<pgrid, dev::NT, dev::p_smem_doubles<8>() * 8, sd->s2>>>(prm[0], kmax, claim);
+      else
+        dev::sb_pre_kernel<16><<<pgrid, dev::NT, dev::p_smem_doubles<16>() * 8, sd->s2>>>(prm[0], kmax, claim);
+      ++nlaunch;
+      if (cudaEventRecord(sd->join2, sd->s2) != cudaSuccess) return 1;
+      pre2 = true;
+    }
   }
   for (int l = L - 1; l >= 0; --l) {
     const int grid = std::max(1, std::min(prm[l].L.P, sms));
-    if (a8)
-      dev::sb_inverse_kernel<8><<<grid, dev::NT, dev::i_smem_doubles<8>() * 8, st>>>(prm[l]);
-    else
-      dev::sb_inverse_kernel<16><<<grid, dev::NT, dev::i_smem_doubles<16>() * 8, st>>>(prm[l]);
+    const bool pl0 = l == 0 && pre;
+    if (pl0 && cudaStreamWaitEvent(st, sd->join, 0) != cudaSuccess) return 1;
+    if (pl0 && pre2 && cudaStreamWaitEvent(st, sd->join2, 0) != cudaSuccess) return 1;
+    if (a8) {
+      if (pl0)
+        dev::sb_inverse_kernel<8, true><<<grid, dev::NT, dev::i_smem_doubles<8>() * 8, st>>>(prm[l]);
+      else
+        dev::sb_inverse_kernel<8, false><<<grid, dev::NT, dev::i_smem_doubles<8>() * 8, st>>>(prm[l]);
+    } else {
+      if (pl0)
+        dev::sb_inverse_kernel<16, true><<<grid, dev::NT, dev::i_smem_doubles<16>() * 8, st>>>(prm[l]);
+      else
+        dev::sb_inverse_kernel<16, false><<<grid, dev::NT, dev::i_smem_doubles<16>() * 8, st>>>(prm[l]);
+    }
     ++nlaunch;
   }
   if (launches) *launches += nlaunch;

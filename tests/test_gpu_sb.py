@@ -98,7 +98,9 @@ def test_sb_launch_count():
     D = to_dev(A)
     h = sb.default_handle()
     sb.selinv_sb(*args(D), [5, 3], handle=h)
-    assert h.last_launches() == 2 * 3  # factor + inverse kernel per level (2 nested + the last chain)
+    # factor + inverse kernel per level (2 nested + the last chain), plus the level-0
+    # W-form precompute on the side stream (sb_pre_kernel)
+    assert h.last_launches() == 2 * 3 + 1
 
 
 def test_sb_rejects_unsupported_shapes():
