@@ -14,7 +14,7 @@ SUF=""
 case "$EXTRA" in *"--engine sb"*) SUF="_sb";; esac
 OUT=gpurun_out/ncu_$CFG$SUF
 mkdir -p $OUT
-KRE='regex:serinv_exec|sb_factor|sb_inverse'
+KRE='regex:serinv_exec|sb_factor|sb_inverse|sb_pre'
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" --csv --log-file $OUT/launches.csv \
   python bench.py --config $CFG --steps 2 --warmup 3 --no-e2e --no-cpu --no-phases $EXTRA > $OUT/launch_stdout.txt 2>&1
 if [ -z "$SUF" ]; then SKIP=3; CNT=1; else SKIP=$(( $(grep -c sb_ $OUT/launches.csv) * 3 / 5 )); CNT=$(( $(grep -c sb_ $OUT/launches.csv) / 5 )); fi

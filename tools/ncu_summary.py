@@ -29,7 +29,7 @@ METRICS = {
 }
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
          "ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3, "second": 1e3}
-OURS = ("serinv_exec", "sb_factor", "sb_inverse")
+OURS = ("serinv_exec", "sb_factor", "sb_inverse", "sb_pre")
 
 
 def row_metrics(names, units, data):
