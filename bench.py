@@ -393,6 +393,9 @@ def main():
     torch.cuda.set_device(local)
     dpath = world > 1 or args.dist   # distributed path (one process per GPU)
     if dpath:
+        if "RANK" not in os.environ:  # --dist at world size 1 without torchrun
+            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_loc, b, a = cfg["n"], cfg["b"], cfg["a"]
     n = n_loc * world
