@@ -29,8 +29,6 @@
 #include <stdint.h>
 
 #include <algorithm>
-#include <map>
-#include <mutex>
 #include <cmath>
 #include <vector>
 
@@ -1295,36 +1293,31 @@ std::vector<int> auto_plan(int64_t n, int64_t b, int sms) {
   return Ps;
 }
 
-namespace {
-// per device: the side stream of the level-0 precompute and its fork / join events
-struct Side {
-  cudaStream_t s = nullptr, s2 = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr, fork2 = nullptr, join2 = nullptr;
-};
-std::mutex side_mu;
-Side *side_for_device() {
-  static std::map<int, Side> sides;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  std::lock_guard<std::mutex> lk(side_mu);
-  Side &sd = sides[dev];
-  if (!sd.s) {
-    if (cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&sd.s2, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&sd.fork2, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&sd.join2, cudaEventDisableTiming) != cudaSuccess) {
-      sd.s = nullptr;
-      return nullptr;
-    }
+bool Side::ensure() {
+  if (s) return true;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&fork2, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&join2, cudaEventDisableTiming) != cudaSuccess) {
+    destroy();
+    return false;
   }
-  return &sd;
+  return true;
 }
-}  // namespace
+
+void Side::destroy() {
+  if (s) cudaStreamDestroy(s);
+  if (s2) cudaStreamDestroy(s2);
+  for (cudaEvent_t e : {fork, join, fork2, join2})
+    if (e) cudaEventDestroy(e);
+  s = s2 = nullptr;
+  fork = join = fork2 = join2 = nullptr;
+}
 
 int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, double *arrow, double *tip, double *ws,
-        int *d_info, double *d_logdet, int sms, cudaStream_t st, int *launches, unsigned long long *trace) {
+        int *d_info, double *d_logdet, int sms, cudaStream_t st, int *launches, Side *side, unsigned long long *trace) {
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(dev::sb_pre_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1403,7 +1396,7 @@ int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, doubl
   int maxp = 1, maxp2 = 1;
   for (int l = 1; l < L; ++l) maxp = std::max(maxp, prm[l].L.P);
   for (int l = 2; l < L; ++l) maxp2 = std::max(maxp2, prm[l].L.P);
-  Side *sd = nl >= 1 ? side_for_device() : nullptr;
+  Side *sd = (nl >= 1 && side && side->ensure()) ? side : nullptr;
   const bool pre = sd != nullptr && sms - maxp >= 16;
   bool pre2 = false;
   int *claim = (int *)(ws + pl.off_ctr) + L + 1;

@@ -62,6 +62,15 @@ struct Plan {
 
 // Build the plan; false if a level is infeasible (partitions of < 2 blocks in the middle,
 // < 1 at the ends) or b / a unsupported.
+// Side streams of the level-0 precompute (sb_pre_kernel) and their fork / join events;
+// owned by the caller's handle (one call at a time per handle), created on first use.
+struct Side {
+  cudaStream_t s = nullptr, s2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, fork2 = nullptr, join2 = nullptr;
+  bool ensure();   // create on the current device; false on a CUDA error
+  void destroy();
+};
+
 bool make_plan(int64_t n, int64_t b, int64_t a, const std::vector<int> &Ps, Plan &pl);
 // Default nesting for one B200 (148 SMs).
 std::vector<int> auto_plan(int64_t n, int64_t b, int sms);
@@ -70,7 +79,7 @@ std::vector<int64_t> plan_tables(const Plan &pl);
 // Enqueue the whole solve on `st`: memset of counters + info, factor kernels level
 // 0..L, inverse kernels level L..0.  d_tab: device copy of plan_tables(pl).
 int run(const Plan &pl, const int64_t *d_tab, double *diag, double *lower, double *arrow, double *tip, double *ws,
-        int *d_info, double *d_logdet, int sms, cudaStream_t st, int *launches,
+        int *d_info, double *d_logdet, int sms, cudaStream_t st, int *launches, Side *side,
         unsigned long long *trace = nullptr);
 // trace layout: [level < 16][kernel 0 factor / 1 inverse][step < 128][8 phase stamps] (u64 ns)
 constexpr int kTraceWords = 16 * 2 * 128 * 8;

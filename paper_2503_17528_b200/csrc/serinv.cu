@@ -83,6 +83,7 @@ struct serinv_ctx {
   unsigned long long *trace = nullptr;  // optional per-task trace buffer (device)
   size_t trace_cap = 0;                 // records
   cudaStream_t s_in = nullptr, s_out = nullptr;  // streaming host IO copy streams
+  sb::Side sb_side;                               // small-block engine's precompute side streams
   cudaEvent_t ev_start = nullptr, ev_in = nullptr, ev_out = nullptr;
   std::map<CKey, std::unique_ptr<DevGraph>> cache;
   std::mutex mu;
@@ -323,6 +324,7 @@ int serinv_destroy(serinv_handle_t h) {
   h->cache.clear();
   h->sb_cache.clear();
   if (h->dummy) cudaFree(h->dummy);
+  h->sb_side.destroy();
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamDestroy(h->s_out);
   if (h->ev_start) cudaEventDestroy(h->ev_start);
@@ -1077,7 +1079,7 @@ int serinv_sb_selinv(serinv_handle_t h, const serinv_bta_t *A, int nlev, const i
   CallGuard guard(h, st);
   int nl = 0;
   if (sb::run(e->pl, e->d_tab, A->diag, A->lower, A->arrow, A->tip, (double *)d_ws, d_info,
-              d_logdet ? d_logdet : h->dummy, h->sms, st, &nl,
+              d_logdet ? d_logdet : h->dummy, h->sms, st, &nl, &h->sb_side,
               (h->trace && h->trace_cap * 96 >= (size_t)sb::kTraceWords * 8) ? h->trace : nullptr))
     return SERINV_ERR_CUDA;
   h->last_launches += nl;
