@@ -62,6 +62,16 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+// the same with an L2 evict-first policy (streamed operands that must not push other
+// kernels' working sets out of L2)
+__device__ __forceinline__ void cp_async16_ef(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile(
+      "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, pol;\n}\n" ::"r"(s),
+      "l"(gmem)
+      : "memory");
+}
 __device__ __forceinline__ void cp_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
@@ -81,13 +91,16 @@ __device__ void record_info(int *info, int v) {
 // s <- op(g) padded: (r, c) = trans ? g[c*ld + r] : g[r*ld + c] for r < rows, c < cols,
 // else (pad && r == c).  Full 64 x 64 untransposed blocks go by cp.async (caller waits).
 __device__ void ld_tile(double *s, const double *g, int rows_t, int rows, int cols, int ld, bool trans,
-                        bool pad) {
+                        bool pad, bool stream = false) {
   const int tid = threadIdx.x;
   if (!trans && rows == T && cols == T && ld == T && rows_t == T) {
 #pragma unroll 4
     for (int i = tid; i < TD / 2; i += NT) {
       const int r = i >> 5, c = (i & 31) * 2;
-      cp_async16(s + swz(r, c), g + r * T + c);
+      if (stream)
+        cp_async16_ef(s + swz(r, c), g + r * T + c);
+      else
+        cp_async16(s + swz(r, c), g + r * T + c);
     }
     return;
   }
@@ -95,7 +108,9 @@ __device__ void ld_tile(double *s, const double *g, int rows_t, int rows, int co
     // full 64-double rows (e.g. the arrow rows at b = 64): cp.async too, zero pad rows
     for (int i = tid; i < rows_t * (T / 2); i += NT) {
       const int r = i >> 5, c = (i & 31) * 2;
-      if (r < rows)
+      if (r < rows && stream)
+        cp_async16_ef(s + swz(r, c), g + r * T + c);
+      else if (r < rows)
         cp_async16(s + swz(r, c), g + r * T + c);
       else
         *(double2 *)(s + swz(r, c)) = make_double2(0.0, 0.0);
@@ -385,7 +400,7 @@ __device__ __forceinline__ void acc_st_smem(double *s, const double (&acc)[MI][N
 }
 
 // g <- sgn * acc (rows x cols of the block; trans: g[c*ld + r] = value (r, c)); LOW / MIR as above
-template <int MI, int NI, bool LOW = false, bool MIR = false>
+template <int MI, int NI, bool LOW = false, bool MIR = false, bool CS = false>
 __device__ __forceinline__ void acc_st_global(double *g, const double (&acc)[MI][NI][2], int ld, int rows,
                                               int cols, const Frags<MI, NI> &F, bool trans, double sgn) {
   const int l = threadIdx.x & 31, lr = l >> 2, lc = l & 3;
@@ -396,7 +411,11 @@ __device__ __forceinline__ void acc_st_global(double *g, const double (&acc)[MI]
       if (LOW && F.rf[i] < F.cf[j]) continue;
       const int m = 8 * F.rf[i] + lr, n = 8 * F.cf[j] + 2 * lc;
       if (!trans && !MIR && m < rows && n + 1 < cols && !(ld & 1) && !((uintptr_t)g & 15)) {  // 16-byte store
-        *(double2 *)(g + (int64_t)m * ld + n) = make_double2(sgn * acc[i][j][0], sgn * acc[i][j][1]);
+        const double2 v2 = make_double2(sgn * acc[i][j][0], sgn * acc[i][j][1]);
+        if (CS)
+          __stcs((double2 *)(g + (int64_t)m * ld + n), v2);  // streaming: evict first
+        else
+          *(double2 *)(g + (int64_t)m * ld + n) = v2;
         continue;
       }
 #pragma unroll
@@ -944,14 +963,14 @@ __global__ void __launch_bounds__(NT, 1) sb_pre_kernel(Params prm, int kmax, int
     if (node(it, c, k)) {
       const int64_t bk = c.blk(k);
       double *W = sm + s * SET, *Y = W + TD, *Z = Y + TD, *N = Z + TD;
-      ld_tile(W, L.D + bk * bb, T, b, b, b, false, true);
+      ld_tile(W, L.D + bk * bb, T, b, b, b, false, true, true);
       if (k + 1 < c.nn) {
         bool tr = false;
         const double *g = coupling(L, c, k, bb, &tr);
-        ld_tile(Y, g, T, b, b, b, tr, false);
+        ld_tile(Y, g, T, b, b, b, tr, false, true);
       }
-      if (c.type == P_MID) ld_tile(Z, L.Bf + bk * bb, T, b, b, b, false, false);
-      if (a > 0) ld_tile(N, L.Ar + bk * ab, AR, a, b, b, false, false);
+      if (c.type == P_MID) ld_tile(Z, L.Bf + bk * bb, T, b, b, b, false, false, true);
+      if (a > 0) ld_tile(N, L.Ar + bk * ab, AR, a, b, b, false, false, true);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -981,24 +1000,24 @@ __global__ void __launch_bounds__(NT, 1) sb_pre_kernel(Params prm, int kmax, int
       double aX[2][4][2];
       acc_zero(aX);
       mma64<true, false, false, B_GE>(aX, W, W, F);  // Lam = W^T W
-      acc_st_global(L.D + bk * bb, aX, b, b, b, F, false, 1.0);
+      acc_st_global<2, 4, false, false, true>(L.D + bk * bb, aX, b, b, b, F, false, 1.0);
       if (k + 1 < c.nn) {  // Lc~ = L_{k+1,k} W
         bool tr = false;
         double *cpl = coupling(L, c, k, bb, &tr);
         acc_zero(aX);
         mma64<false, false, false, B_GE>(aX, Y, W, F);
-        acc_st_global(cpl, aX, b, b, b, F, tr, 1.0);
+        acc_st_global<2, 4, false, false, true>(cpl, aX, b, b, b, F, tr, 1.0);
       }
       if (c.type == P_MID) {  // Lf~ = L_{f,k} W
         acc_zero(aX);
         mma64<false, false, false, B_GE>(aX, Z, W, F);
-        acc_st_global(L.Bf + bk * bb, aX, b, b, b, F, false, 1.0);
+        acc_st_global<2, 4, false, false, true>(L.Bf + bk * bb, aX, b, b, b, F, false, 1.0);
       }
       if (a > 0) {  // Ln~ = L_{n,k} W
         double aN[1][NA][2];
         acc_zero(aN);
         mma<1, NA, false, false, false, B_GE>(aN, N, W, FA, T);
-        acc_st_global(L.Ar + bk * ab, aN, b, a, b, FA, false, 1.0);
+        acc_st_global<1, NA, false, false, true>(L.Ar + bk * ab, aN, b, a, b, FA, false, 1.0);
       }
     }
     if (threadIdx.x == 0) s_next = nx < nit ? nn : nit;
