@@ -139,7 +139,7 @@ def parse():
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """SM clock and throttle reasons sampled every ~20 ms DURING the timed region
+    """SM clock and throttle reasons sampled every ~5 ms DURING the timed region
     (NVML; nvidia-smi as a fallback)."""
     NVML_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
                  "hw_thermal_slowdown": 0x40}
@@ -184,7 +184,7 @@ class ClockSampler:
                 self.samples.append(self._sample_nvml() if self._nvml else self._sample_smi())
             except Exception:
                 pass
-            self._stop.wait(0.02 if self._nvml else 0.2)
+            self._stop.wait(0.005 if self._nvml else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
